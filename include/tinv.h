@@ -1,0 +1,121 @@
+/*
+ * tinv.h -- C ABI of the B200-native inverse iteration with compact-WY
+ * reorthogonalisation (libtinv.so).
+ *
+ * Operation (§2.1, and §4 Alg. 4, lines 681-716 of
+ * /root/reference/PAPER.md, arXiv 1209.1910): given a real symmetric tridiagonal
+ * T = tridiag(e, d, e) of order n and its ascending (approximate) eigenvalues w,
+ * compute all n eigenvectors Z (T z_j ~= w_j z_j, Z^T Z ~= I) by inverse iteration
+ * (Eq. (1)); eigenvectors of each Peters-Wilkinson cluster (gap <=
+ * 1e-3 ||T||_1, lines 135-139) are reorthogonalised with the compact WY Householder
+ * orthogonalisation in the paper's reduced formulation (§3.3.2).
+ * Readings of the points the paper leaves open (start vectors, shift perturbation,
+ * solver, stopping rule, signs) are listed in DESIGN.md and are shared with the CPU
+ * oracle only as rules, never as code.
+ *
+ * All compute runs in the library's own sm_100a kernels on the handle's stream.
+ * There is no CPU fallback: on a machine without a usable CUDA device every call
+ * returns TINV_ERR_CUDA.
+ */
+#ifndef TINV_H
+#define TINV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tinv_s* tinv_t;
+
+typedef struct {
+    int         device;   /* CUDA ordinal this handle drives                                 */
+    int         nranks;   /* number of cooperating ranks (processes), 1 = single GPU         */
+    int         rank;     /* 0 .. nranks-1                                                    */
+    const void* nccl_id;  /* 128-byte ncclUniqueId created by rank 0 and broadcast by the
+                             caller, or NULL when nranks == 1                                 */
+    void*       stream;   /* cudaStream_t the work is ordered on (NULL = legacy default)      */
+} tinv_config_t;
+
+/* Return codes (LAPACK INFO style).
+ *   0      success
+ *  -k      argument k is invalid, counting the handle as argument 1 (n < 1, NULL
+ *          pointer, ldz < n, non-finite d/e/w, w not ascending)
+ *  >0      number of eigenvectors that did not meet the stopping rule within MAXITS = 5
+ *          iterations (they are still written, best iterate)
+ *  <=-100  library failure, decode with tinv_strerror() */
+#define TINV_OK            0
+#define TINV_ERR_CUDA   -100
+#define TINV_ERR_NOMEM  -101
+#define TINV_ERR_NCCL   -102
+#define TINV_ERR_HANDLE -103
+#define TINV_ERR_DEVICE -104
+
+/* Create a handle bound to cfg->device and cfg->stream.  With nranks > 1 each rank
+ * creates its handle with the same nccl_id (clusters are then sharded across ranks).
+ * Ownership: the handle owns its device workspace (allocated lazily, cached across
+ * calls, freed by tinv_destroy).  One handle per host thread. */
+int tinv_create(tinv_t* h, const tinv_config_t* cfg);
+
+/* Compute all eigenvectors.
+ *   n     order of T (n >= 1)
+ *   d     DEVICE pointer, n doubles: diagonal of T                       (read only)
+ *   e     DEVICE pointer, n-1 doubles: off-diagonal of T; may be NULL iff n == 1
+ *   w     DEVICE pointer, n doubles: eigenvalues of T, non-decreasing   (read only)
+ *   Z     DEVICE pointer, ldz*n doubles, column-major: on return column j holds the unit
+ *         eigenvector of w[j], sign fixed so that its largest-|.| entry (lowest index on
+ *         ties) is positive.  Every column is overwritten.
+ *   ldz   leading dimension of Z (ldz >= n)
+ *   seed  seed of the counter-based start-vector generator (reading 7)
+ * The call is synchronous with respect to the host (it returns the convergence count)
+ * and stream-ordered on the handle's stream.  Special cases: n == 1 -> Z = [1];
+ * ||T||_1 == 0 -> Z = I.  With nranks > 1 every rank passes identical arguments and Z
+ * is complete on every rank on return. */
+int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
+                 double* Z, int64_t ldz, uint64_t seed);
+
+/* Same operation with HOST buffers (pinned host memory recommended): the library copies
+ * d, e, w to the device, runs tinv_eigvecs and copies Z back (end-to-end path). */
+int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
+                      double* Z, int64_t ldz, uint64_t seed);
+
+/* Release the handle and its device workspace. */
+int tinv_destroy(tinv_t h);
+
+/* Human-readable text of a return code (static storage). */
+const char* tinv_strerror(int code);
+
+/* ---------------------------------------------------------------- introspection
+ * Statistics of the last tinv_eigvecs call on this handle.  Kernel times are filled
+ * only when profiling is enabled (CUDA events on the handle's stream around each
+ * launch; adds a few microseconds per launch). */
+#define TINV_NKERNELS 6
+typedef struct {
+    int64_t n;
+    int64_t nclusters;          /* Peters-Wilkinson clusters (size >= 1)              */
+    int64_t max_cluster;        /* largest cluster size m                             */
+    int64_t n_clustered;        /* vectors with j_c >= 1 (reorthogonalised)           */
+    int64_t nflagged;           /* vectors that missed the stopping rule              */
+    int64_t iters_hist[8];      /* vectors by iteration count (index 7 = 7 or more)   */
+    int64_t launches;           /* kernels launched by the last call                  */
+    int64_t group_syncs;        /* group barrier episodes in the cWY kernel (per group max) */
+    int64_t ngroups;            /* CTA groups used by the cWY kernel                  */
+    int64_t cwy_ctas;           /* CTAs of the cWY kernel                             */
+    double  reorth_bytes;       /* algorithmic bytes of the cWY passes    */
+    double  solve_bytes;        /* algorithmic bytes of the batched LU kernel         */
+    double  kernel_ms[TINV_NKERNELS];     /* prep, batched_lu, finalize, cwy, misc, total */
+    int64_t kernel_launches[TINV_NKERNELS];
+    double  cwy_phase_ms[10];   /* group 0 of the cWY kernel, wall time per phase: first
+                                   reflector, A, R1, TT, BC, R2, TN, D, test, chained solve */
+} tinv_stats_t;
+
+int tinv_set_profiling(tinv_t h, int enable);
+int tinv_get_stats(tinv_t h, tinv_stats_t* out);
+
+/* Number of exported entry points (for the loader test). */
+int tinv_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TINV_H */

@@ -1,0 +1,119 @@
+// common.cuh -- device helpers shared by the libtinv kernels (sm_100a).
+// Nothing here is shared with the CPU oracle (oracle/); the rules (RNG formula,
+// pivot floor, shift ladder, stopping constants) are restated from DESIGN.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tinv {
+
+constexpr double kEps = 1.1102230246251565404e-16;  // 2^-53, unit roundoff (R3/R4)
+constexpr int kMaxIts = 5;                          // reading 9
+constexpr int kPasses = 2;                          // reading 9: first pass + 1 extra
+constexpr int kMaxRestart = 2;                      // reading 16
+
+// ---------------------------------------------------------------- start vectors (reading 7)
+// SplitMix64 finaliser of seed + phi64 * ctr; top 53 bits -> u in [0,1); value 2u - 1.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t seed, uint64_t ctr) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ULL * ctr;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ double start_entry(uint64_t seed, int64_t n, int64_t j,
+                                                       int64_t restart, int64_t i) {
+    uint64_t ctr = 1ULL + ((uint64_t)restart * (uint64_t)n + (uint64_t)j) * (uint64_t)n + (uint64_t)i;
+    uint64_t z = mix64(seed, ctr);
+    double u = (double)(z >> 11) * 0x1.0p-53;
+    return 2.0 * u - 1.0;  // exact in fp64
+}
+
+// pivot floor (reading 6): |p| < eps*||T||_1 -> sign(p)*eps*||T||_1, + for p == 0
+__device__ __forceinline__ double pivot_floor(double p, double tiny) {
+    return (fabs(p) < tiny) ? ((p >= 0.0) ? tiny : -tiny) : p;
+}
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic block sum: fixed tree over warps.  `red` needs blockDim/32 doubles.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (wid == 0) {
+        r = (lane < NT / 32) ? red[lane] : 0.0;
+        r = warp_sum(r);
+        if (lane == 0) red[0] = r;
+    }
+    __syncthreads();
+    r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------- group barrier
+// A group is a contiguous range of co-resident CTAs of a persistent (cooperative)
+// launch.  Sense-reversal barrier on a (count, generation) pair in global memory;
+// the gpu-scope fences give the release/acquire ordering (and invalidate L1) so data
+// written by any CTA before the barrier is visible to every CTA after it.
+struct GroupBarrier {
+    unsigned int count;
+    unsigned int gen;
+};
+
+__device__ __forceinline__ void group_sync(GroupBarrier* b, int G) {
+    if (G == 1) {
+        __syncthreads();
+        return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vgen = &b->gen;
+        unsigned int g0 = *vgen;
+        __threadfence();
+        unsigned int arrived = atomicAdd(&b->count, 1u);
+        if (arrived == (unsigned)G - 1) {
+            b->count = 0;
+            __threadfence();
+            atomicAdd(&b->gen, 1u);
+        } else {
+            while (*vgen == g0) { __nanosleep(20); }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- packed layouts
+// Y (row-major, zero-free "assignment model" of Fig. 1): row i of
+// Y_m holds columns 0..min(i, m-1), padded to an even count (16-byte rows).
+__host__ __device__ __forceinline__ int64_t y_row_off(int64_t i, int64_t m) {
+    auto tri = [](int64_t r) -> int64_t {  // sum_{r'<r} roundup(r'+1, 2)
+        int64_t a = r >> 1, b = r & 1;
+        return 2 * a * (a + 1) + 2 * b * (a + 1);
+    };
+    if (i <= m) return tri(i);
+    int64_t m2 = (m + 1) & ~int64_t(1);
+    return tri(m) + (i - m) * m2;
+}
+// T, column-packed: column k holds T[0..k, k], padded to even.
+__host__ __device__ __forceinline__ int64_t tcol_off(int64_t k) {
+    int64_t a = k >> 1, b = k & 1;
+    return 2 * a * (a + 1) + 2 * b * (a + 1);
+}
+
+}  // namespace tinv

@@ -1,0 +1,577 @@
+// tinv_host.cu -- C ABI (include/tinv.h) and host orchestration of libtinv.
+//
+// Call sequence of tinv_eigvecs (SURVEY §3 call stack (2)):
+//   prep kernel (||T||_1, validation, clusters, shifts)  -> one small D2H of the cluster
+//   table -> host schedule (CTA groups, LPT over clusters) -> batched LU kernel (every
+//   first solve; clusters' leaders and singletons finish) -> finalize kernel (transpose
+//   of finished vectors into Z) -> persistent compact-WY kernel (clustered vectors) ->
+//   D2H of the non-convergence count.
+// With nranks > 1 the clusters are sharded over the ranks in contiguous column ranges and
+// each rank's columns are broadcast with NCCL at the end (no data-path collective).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <dlfcn.h>
+#include <numeric>
+#include <vector>
+
+#include "../../include/tinv.h"
+#include "common.cuh"
+#include "tinv_internal.h"
+
+using namespace tinv;
+
+namespace {
+
+// ---------------------------------------------------------------- NCCL (dlopen'ed)
+// The process already has torch's NCCL loaded; binding at run time avoids linking a
+// second NCCL into the same process.
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+struct Nccl {
+    void* lib = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    bool load() {
+        if (lib) return true;
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW);
+        if (!lib) return false;
+        commInitRank = (decltype(commInitRank))dlsym(lib, "ncclCommInitRank");
+        commDestroy = (decltype(commDestroy))dlsym(lib, "ncclCommDestroy");
+        broadcast = (decltype(broadcast))dlsym(lib, "ncclBroadcast");
+        groupStart = (decltype(groupStart))dlsym(lib, "ncclGroupStart");
+        groupEnd = (decltype(groupEnd))dlsym(lib, "ncclGroupEnd");
+        return commInitRank && commDestroy && broadcast && groupStart && groupEnd;
+    }
+};
+Nccl g_nccl;
+constexpr int ncclFloat64 = 8;
+
+}  // namespace
+
+struct tinv_s {
+    int device = 0;
+    int nranks = 1, rank = 0;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    int nsm = 148;
+    bool profiling = false;
+    // base workspace (n-dependent)
+    int64_t ncap = 0, ldv = 0;
+    void* base = nullptr;
+    size_t base_bytes = 0;
+    double *wt = nullptr, *X = nullptr, *fl = nullptr, *fr = nullptr, *fb = nullptr, *fc = nullptr;
+    double *unn = nullptr, *zscale = nullptr;
+    int8_t* fp = nullptr;
+    int *cstart = nullptr, *cid = nullptr, *jc = nullptr, *iters = nullptr;
+    PrepOut* out = nullptr;
+    // cWY workspace (schedule-dependent)
+    void* cw = nullptr;
+    size_t cw_bytes = 0;
+    // host mirrors (pinned)
+    PrepOut* h_out = nullptr;
+    int* h_cstart = nullptr;
+    int* h_iters = nullptr;
+    int64_t h_cap = 0;
+    // host-buffer path
+    double* io = nullptr;
+    size_t io_bytes = 0;
+    // events for profiling
+    cudaEvent_t ev[16] = {};
+    tinv_stats_t stats{};
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return 0;
+    fprintf(stderr, "[tinv] CUDA error in %s: %s\n", what, cudaGetErrorString(e));
+    if (e == cudaErrorMemoryAllocation) return TINV_ERR_NOMEM;
+    return TINV_ERR_CUDA;
+}
+#define CK(x)                                       \
+    do {                                            \
+        int _r = cuda_fail((x), #x);                \
+        if (_r) return _r;                          \
+    } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Carve {
+    char* p;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        off = align_up(off, 256);
+        T* r = reinterpret_cast<T*>(p ? p + off : nullptr);
+        off += count * sizeof(T);
+        return r;
+    }
+};
+
+int ensure_base(tinv_s* h, int64_t n) {
+    if (n <= h->ncap) return 0;
+    if (h->base) { cudaFree(h->base); h->base = nullptr; }
+    int64_t ldv = (n + 31) / 32 * 32;
+    auto layout = [&](char* p) {
+        Carve c{p};
+        size_t nn = (size_t)n * (size_t)ldv;
+        h->wt = c.take<double>(n);
+        h->unn = c.take<double>(n);
+        h->zscale = c.take<double>(n);
+        h->cstart = c.take<int>(n + 1);
+        h->cid = c.take<int>(n);
+        h->jc = c.take<int>(n);
+        h->iters = c.take<int>(n);
+        h->out = c.take<PrepOut>(1);
+        h->X = c.take<double>(nn);
+        h->fl = c.take<double>(nn);
+        h->fr = c.take<double>(nn);
+        h->fb = c.take<double>(nn);
+        h->fc = c.take<double>(nn);
+        h->fp = c.take<int8_t>(nn);
+        return c.off;
+    };
+    size_t bytes = layout(nullptr);
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    h->base = p;
+    h->base_bytes = bytes;
+    layout((char*)p);
+    h->ncap = n;
+    h->ldv = ldv;
+    if (h->h_cap < n + 1) {
+        if (h->h_cstart) cudaFreeHost(h->h_cstart);
+        if (h->h_iters) cudaFreeHost(h->h_iters);
+        CK(cudaMallocHost(&h->h_cstart, sizeof(int) * (n + 1)));
+        CK(cudaMallocHost(&h->h_iters, sizeof(int) * (n + 1)));
+        h->h_cap = n + 1;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------- schedule
+struct Schedule {
+    std::vector<int> cta0, size, coff, clist;
+    std::vector<int64_t> mcap;
+    int nctas = 0;
+};
+
+// Clusters [c_lo, c_hi) with m >= 2 -> CTA groups.  Many clusters: one CTA per group and
+// LPT over groups by cost m^2 n.  Few clusters: one group per cluster, CTAs shared in
+// proportion to cost, capped so a CTA keeps >= 256 KB of Y per pass.
+Schedule make_schedule(const int* cs, int c_lo, int c_hi, int64_t n, int nctas) {
+    Schedule s;
+    std::vector<int> cl;
+    for (int c = c_lo; c < c_hi; c++)
+        if (cs[c + 1] - cs[c] >= 2) cl.push_back(c);
+    if (cl.empty()) return s;
+    auto cost = [&](int c) { double m = cs[c + 1] - cs[c]; return m * m * (double)n + 64.0 * m * (double)n; };
+    std::stable_sort(cl.begin(), cl.end(), [&](int a, int b) { return cost(a) > cost(b); });
+    int nc = (int)cl.size();
+    if (nc >= nctas) {
+        int ng = nctas;
+        std::vector<std::vector<int>> lists(ng);
+        std::vector<double> load(ng, 0.0);
+        for (int c : cl) {
+            int best = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+            lists[best].push_back(c);
+            load[best] += cost(c);
+        }
+        s.coff.push_back(0);
+        for (int g = 0; g < ng; g++) {
+            s.cta0.push_back(g);
+            s.size.push_back(1);
+            int64_t mc = 0;
+            for (int c : lists[g]) { s.clist.push_back(c); mc = std::max<int64_t>(mc, cs[c + 1] - cs[c]); }
+            s.coff.push_back((int)s.clist.size());
+            s.mcap.push_back(mc);
+        }
+        s.nctas = ng;
+        return s;
+    }
+    double tot = 0.0;
+    for (int c : cl) tot += cost(c);
+    std::vector<int> sz(nc);
+    int used = 0;
+    for (int i = 0; i < nc; i++) {
+        int c = cl[i];
+        double m = cs[c + 1] - cs[c];
+        int cap = (int)std::max(1.0, std::min((double)nctas, std::ceil(m * (double)n * 8.0 / (256.0 * 1024.0))));
+        int want = (int)std::floor(cost(c) / tot * nctas);
+        sz[i] = std::max(1, std::min(cap, want));
+        used += sz[i];
+    }
+    while (used > nctas) {  // shave the largest groups
+        int i = (int)(std::max_element(sz.begin(), sz.end()) - sz.begin());
+        sz[i]--;
+        used--;
+    }
+    s.coff.push_back(0);
+    int next = 0;
+    for (int i = 0; i < nc; i++) {
+        int c = cl[i];
+        s.cta0.push_back(next);
+        s.size.push_back(sz[i]);
+        next += sz[i];
+        s.clist.push_back(c);
+        s.coff.push_back((int)s.clist.size());
+        s.mcap.push_back(cs[c + 1] - cs[c]);
+    }
+    s.nctas = next;
+    return s;
+}
+
+// contiguous cluster ranges per rank, balanced by cost (deterministic)
+void rank_ranges(const int* cs, int nclus, int64_t n, int nranks, std::vector<int>& lo, std::vector<int>& hi) {
+    std::vector<double> pre(nclus + 1, 0.0);
+    for (int c = 0; c < nclus; c++) {
+        double m = cs[c + 1] - cs[c];
+        pre[c + 1] = pre[c] + (m >= 2 ? m * m * (double)n : 0.0) + m;
+    }
+    lo.assign(nranks, 0);
+    hi.assign(nranks, 0);
+    int c = 0;
+    for (int r = 0; r < nranks; r++) {
+        lo[r] = c;
+        double target = pre[nclus] * (double)(r + 1) / nranks;
+        while (c < nclus && (r == nranks - 1 || pre[c + 1] <= target + 1e-9)) c++;
+        if (r == nranks - 1) c = nclus;
+        hi[r] = c;
+    }
+}
+
+void ev_record(tinv_s* h, int k) {
+    if (h->profiling) cudaEventRecord(h->ev[k], h->stream);
+}
+
+}  // namespace
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+int tinv_abi_version(void) { return 1; }
+
+const char* tinv_strerror(int code) {
+    if (code == 0) return "success";
+    if (code > 0) return "some eigenvectors did not meet the stopping rule within MAXITS";
+    switch (code) {
+        case TINV_ERR_CUDA: return "CUDA error (no usable device, launch or runtime failure)";
+        case TINV_ERR_NOMEM: return "device memory allocation failed";
+        case TINV_ERR_NCCL: return "NCCL failure";
+        case TINV_ERR_HANDLE: return "invalid handle";
+        case TINV_ERR_DEVICE: return "device is not an sm_100 (B200) GPU";
+        case -2: return "invalid argument 2 (n < 1)";
+        case -3: return "invalid argument 3 (d NULL or non-finite)";
+        case -4: return "invalid argument 4 (e NULL or non-finite)";
+        case -5: return "invalid argument 5 (w NULL, non-finite or not ascending)";
+        case -6: return "invalid argument 6 (Z NULL)";
+        case -7: return "invalid argument 7 (ldz < n)";
+        default: return "invalid argument";
+    }
+}
+
+int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
+    if (!out) return -1;
+    *out = nullptr;
+    if (!cfg) return -2;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) return TINV_ERR_CUDA;
+    if (cfg->device < 0 || cfg->device >= ndev) return -2;
+    if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return -2;
+    CK(cudaSetDevice(cfg->device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, cfg->device));
+    if (prop.major != 10) return TINV_ERR_DEVICE;
+    tinv_s* h = new tinv_s();
+    h->device = cfg->device;
+    h->nranks = cfg->nranks;
+    h->rank = cfg->rank;
+    h->stream = (cudaStream_t)cfg->stream;
+    h->nsm = prop.multiProcessorCount;
+    CK(cudaMallocHost(&h->h_out, sizeof(PrepOut)));
+    for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    if (h->nranks > 1) {
+        if (!cfg->nccl_id || !g_nccl.load()) { delete h; return TINV_ERR_NCCL; }
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_id, sizeof(id));
+        if (g_nccl.commInitRank(&h->comm, h->nranks, id, h->rank) != 0) { delete h; return TINV_ERR_NCCL; }
+    }
+    *out = h;
+    return 0;
+}
+
+int tinv_destroy(tinv_t h) {
+    if (!h) return TINV_ERR_HANDLE;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    if (h->comm) g_nccl.commDestroy(h->comm);
+    if (h->base) cudaFree(h->base);
+    if (h->cw) cudaFree(h->cw);
+    if (h->io) cudaFree(h->io);
+    if (h->h_out) cudaFreeHost(h->h_out);
+    if (h->h_cstart) cudaFreeHost(h->h_cstart);
+    if (h->h_iters) cudaFreeHost(h->h_iters);
+    for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    delete h;
+    return 0;
+}
+
+int tinv_set_profiling(tinv_t h, int enable) {
+    if (!h) return TINV_ERR_HANDLE;
+    h->profiling = enable != 0;
+    return 0;
+}
+
+int tinv_get_stats(tinv_t h, tinv_stats_t* out) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (!out) return -2;
+    *out = h->stats;
+    return 0;
+}
+
+int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
+                 double* Z, int64_t ldz, uint64_t seed) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (n < 1) return -2;
+    if (!d) return -3;
+    if (!e && n > 1) return -4;
+    if (!w) return -5;
+    if (!Z) return -6;
+    if (ldz < n) return -7;
+    CK(cudaSetDevice(h->device));
+    if (int r = ensure_base(h, n)) return r;
+    cudaStream_t st = h->stream;
+    tinv_stats_t& S = h->stats;
+    memset(&S, 0, sizeof(S));
+    S.n = n;
+    int launches = 0;
+
+    // ---------------- prep
+    ev_record(h, 0);
+    CK(cudaMemsetAsync(h->out, 0, sizeof(PrepOut), st));
+    PrepArgs pa{n, d, e, w, h->wt, h->cstart, h->cid, h->jc, h->out};
+    launch_prep(pa, st);
+    launches++;
+    CK(cudaGetLastError());
+    ev_record(h, 1);
+    CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->h_cstart, h->cstart, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const PrepOut po = *h->h_out;
+    if (po.bad & 1) return -3;
+    if (po.bad & 2) return -4;
+    if (po.bad & 4) return -5;
+    const double tnorm = po.tnorm;
+    const int nclus = po.nclus;
+    S.nclusters = nclus;
+    S.max_cluster = po.max_cluster;
+    S.n_clustered = po.n_clustered;
+    if (n == 1 || tnorm == 0.0) {
+        launch_identity(Z, n, ldz, st);
+        launches++;
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        S.launches = launches;
+        S.iters_hist[0] = n;
+        return 0;
+    }
+    const int* cs = h->h_cstart;
+
+    // ---------------- batched LU + finalize of finished vectors
+    ev_record(h, 2);
+    BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, tnorm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
+                   h->X, h->unn, h->zscale, h->iters, h->out};
+    launch_batched(ba, st);
+    launches++;
+    CK(cudaGetLastError());
+    ev_record(h, 3);
+    FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->jc, Z, ldz};
+    launch_finalize(fa, st);
+    launches++;
+    CK(cudaGetLastError());
+    ev_record(h, 4);
+
+    // ---------------- compact-WY kernel over this rank's clusters
+    std::vector<int> rlo, rhi;
+    rank_ranges(cs, nclus, n, h->nranks, rlo, rhi);
+    const int nctas_max = h->nsm * std::max(1, cwy_max_ctas_per_sm());
+    Schedule sc = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
+    if (!sc.size.empty()) {
+        const int ng = (int)sc.size.size();
+        // workspace: schedule arrays + per-group buffers
+        unsigned long long* prof = nullptr;
+        auto layout = [&](char* p, std::vector<GroupWS>& ws, int** arrs, long long** syncs, GroupWS** dws) {
+            Carve c{p};
+            prof = c.take<unsigned long long>((size_t)ng * 16);
+            arrs[0] = c.take<int>(ng);
+            arrs[1] = c.take<int>(ng);
+            arrs[2] = c.take<int>(ng + 1);
+            arrs[3] = c.take<int>(sc.clist.size());
+            *syncs = c.take<long long>(ng);
+            *dws = c.take<GroupWS>(ng);
+            ws.resize(ng);
+            for (int g = 0; g < ng; g++) {
+                int64_t mc = sc.mcap[g];
+                int64_t m2 = (mc + 1) & ~int64_t(1);
+                int G = sc.size[g];
+                GroupWS& W = ws[g];
+                W.mcap = m2 + 2;
+                W.Y = c.take<double>(y_row_off(n, mc) + 2);
+                W.Tc = c.take<double>(tcol_off(mc) + 2);
+                W.Tr = c.take<double>(mc * m2 + 2);
+                W.x = c.take<double>(n + 2);
+                W.q = c.take<double>(n + 2);
+                W.u = c.take<double>(n + 2);
+                W.ysol = c.take<double>(n + 2);
+                W.g = c.take<double>(W.mcap);
+                W.gp = c.take<double>(W.mcap);
+                W.s = c.take<double>(W.mcap);
+                W.xp = c.take<double>(W.mcap);
+                W.P = c.take<double>((size_t)G * W.mcap);
+                W.S = c.take<double>((size_t)G * 8 + 8);
+                W.bar = c.take<GroupBarrier>(1);
+            }
+            return c.off;
+        };
+        std::vector<GroupWS> ws;
+        int* arrs[4];
+        long long* syncs;
+        GroupWS* dws;
+        size_t need = layout(nullptr, ws, arrs, &syncs, &dws);
+        if (need > h->cw_bytes) {
+            if (h->cw) cudaFree(h->cw);
+            h->cw = nullptr;
+            h->cw_bytes = 0;
+            CK(cudaMalloc(&h->cw, need));
+            CK(cudaMemsetAsync(h->cw, 0, need, st));  // stale slots must be finite
+            h->cw_bytes = need;
+        }
+        layout((char*)h->cw, ws, arrs, &syncs, &dws);
+        CK(cudaMemcpyAsync(arrs[0], sc.cta0.data(), sizeof(int) * ng, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(arrs[1], sc.size.data(), sizeof(int) * ng, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(arrs[2], sc.coff.data(), sizeof(int) * (ng + 1), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(arrs[3], sc.clist.data(), sizeof(int) * sc.clist.size(), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dws, ws.data(), sizeof(GroupWS) * ng, cudaMemcpyHostToDevice, st));
+        for (int g = 0; g < ng; g++) CK(cudaMemsetAsync(ws[g].bar, 0, sizeof(GroupBarrier), st));
+        CwyArgs ca{};
+        ca.n = n; ca.ldv = h->ldv; ca.d = d; ca.e = e; ca.tnorm = tnorm; ca.seed = seed;
+        ca.wt = h->wt; ca.cstart = h->cstart;
+        ca.fl = h->fl; ca.fp = h->fp; ca.fr = h->fr; ca.fb = h->fb; ca.fc = h->fc; ca.unn = h->unn;
+        ca.X1 = h->X; ca.Z = Z; ca.ldz = ldz; ca.iters = h->iters; ca.out = h->out;
+        ca.ngroups = ng; ca.g_cta0 = arrs[0]; ca.g_size = arrs[1]; ca.g_coff = arrs[2]; ca.g_clist = arrs[3];
+        ca.ws = dws; ca.syncs = syncs; ca.prof = h->profiling ? prof : nullptr;
+        ev_record(h, 5);
+        CK(launch_cwy(ca, sc.nctas, st));
+        launches++;
+        ev_record(h, 6);
+        S.ngroups = ng;
+        S.cwy_ctas = sc.nctas;
+        // algorithmic bytes: computed after the iteration counts are known (below)
+        double rb = 0.0;
+        S.reorth_bytes = rb;
+        std::vector<long long> hs(ng);
+        std::vector<unsigned long long> hp(16, 0ULL);
+        CK(cudaMemcpyAsync(hs.data(), syncs, sizeof(long long) * ng, cudaMemcpyDeviceToHost, st));
+        if (h->profiling) CK(cudaMemcpyAsync(hp.data(), prof, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int k = 0; k < 10; k++) S.cwy_phase_ms[k] = (double)hp[k] * 1e-6;
+        for (auto v : hs) S.group_syncs = std::max<int64_t>(S.group_syncs, v);
+    }
+    S.solve_bytes = 144.0 * (double)n * (double)n;  // factor 32n + 2 x 56n per vector
+
+    // ---------------- multi-rank: broadcast each rank's cluster columns
+    if (h->nranks > 1) {
+        if (g_nccl.groupStart()) return TINV_ERR_NCCL;
+        for (int r = 0; r < h->nranks; r++) {
+            int64_t c0 = cs[rlo[r]], c1 = cs[rhi[r]];
+            if (c1 <= c0) continue;
+            if (ldz == n) {
+                if (g_nccl.broadcast(Z + c0 * ldz, Z + c0 * ldz, (size_t)((c1 - c0) * ldz), ncclFloat64, r, h->comm, st))
+                    return TINV_ERR_NCCL;
+            } else {
+                for (int64_t j = c0; j < c1; j++)
+                    if (g_nccl.broadcast(Z + j * ldz, Z + j * ldz, (size_t)n, ncclFloat64, r, h->comm, st))
+                        return TINV_ERR_NCCL;
+            }
+        }
+        if (g_nccl.groupEnd()) return TINV_ERR_NCCL;
+    }
+
+    // ---------------- status
+    ev_record(h, 7);
+    CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->h_iters, h->iters, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    for (int64_t j = 0; j < n; j++) S.iters_hist[std::min(7, std::max(0, h->h_iters[j]))]++;
+    // algorithmic bytes of the compact-WY work (paper kernel sequence
+    // PAPER.md:530-623): one cWY step of vector j_c = p reads 8 (4 p n - 1.5 p^2) bytes;
+    // every iteration of a clustered vector runs one step.
+    {
+        double rb = 0.0;
+        for (int c = rlo[h->rank]; c < rhi[h->rank]; c++) {
+            for (int64_t j = cs[c] + 1; j < cs[c + 1]; j++) {
+                double p = (double)(j - cs[c]);
+                rb += (double)h->h_iters[j] * 8.0 * (4.0 * p * (double)n - 1.5 * p * p);
+            }
+        }
+        S.reorth_bytes = rb;
+    }
+    S.launches = launches;
+    if (h->profiling) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]); S.kernel_ms[0] = ms;
+        cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); S.kernel_ms[1] = ms;
+        cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); S.kernel_ms[2] = ms;
+        if (!sc.size.empty()) { cudaEventElapsedTime(&ms, h->ev[5], h->ev[6]); S.kernel_ms[3] = ms; }
+        cudaEventElapsedTime(&ms, h->ev[0], h->ev[7]); S.kernel_ms[5] = ms;
+        S.kernel_launches[0] = 1; S.kernel_launches[1] = 1; S.kernel_launches[2] = 1;
+        S.kernel_launches[3] = sc.size.empty() ? 0 : 1;
+    }
+    const int nflag = h->h_out->nflag;
+    S.nflagged = nflag;
+    return nflag;
+}
+
+int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
+                      double* Z, int64_t ldz, uint64_t seed) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (n < 1) return -2;
+    if (!d) return -3;
+    if (!e && n > 1) return -4;
+    if (!w) return -5;
+    if (!Z) return -6;
+    if (ldz < n) return -7;
+    CK(cudaSetDevice(h->device));
+    size_t need = sizeof(double) * (size_t)(3 * n + 2 + (size_t)ldz * n) + 1024;
+    if (need > h->io_bytes) {
+        if (h->io) cudaFree(h->io);
+        h->io = nullptr;
+        h->io_bytes = 0;
+        CK(cudaMalloc(&h->io, need));
+        h->io_bytes = need;
+    }
+    double* dd = h->io;
+    double* de = dd + n;
+    double* dw = de + n;
+    double* dZ = dw + n + 2;
+    cudaStream_t st = h->stream;
+    CK(cudaMemcpyAsync(dd, d, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    if (n > 1) CK(cudaMemcpyAsync(de, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dw, w, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    int rc = tinv_eigvecs(h, n, dd, n > 1 ? de : nullptr, dw, dZ, ldz, seed);
+    if (rc < 0) return rc;
+    CK(cudaMemcpyAsync(Z, dZ, sizeof(double) * (size_t)ldz * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return rc;
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

@@ -1,0 +1,125 @@
+// tinv_internal.h -- argument blocks shared by the host orchestrator and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tinv {
+
+struct GroupBarrier;
+
+// Small device-resident summary written by prep and the solve kernels, read back once.
+struct PrepOut {
+    double tnorm;
+    int bad;            // bit0 d, bit1 e, bit2 w (non-finite or not ascending)
+    int nclus;
+    int max_cluster;
+    int n_clustered;
+    int nflag;          // vectors that missed the stopping rule
+    int pad[3];
+};
+
+struct PrepArgs {
+    int64_t n;
+    const double* d;
+    const double* e;
+    const double* w;
+    double* wt;         // perturbed shifts (n)
+    int* cstart;        // cluster starts (n+1)
+    int* cid;           // cluster of each vector (n)
+    int* jc;            // position inside its cluster (n)
+    PrepOut* out;
+};
+
+// Batched shifted LU inverse iteration: one thread per eigenvector, interleaved
+// [row i][vector j] layout (element (i, j) at i*ldv + j) for coalesced warps.
+struct BatchedArgs {
+    int64_t n;
+    int64_t ldv;        // interleave stride (>= n)
+    const double* d;
+    const double* e;
+    const double* wt;
+    const int* jc;
+    double tnorm;
+    uint64_t seed;
+    // factors, [i][j]
+    double* fl;         // multipliers l_i (row i < n-1)
+    int8_t* fp;         // row swap flags
+    double* fr;         // 1/u0_i
+    double* fb;         // u1_i/u0_i
+    double* fc;         // u2_i/u0_i
+    double* X;          // iterate / solution, [i][j]
+    double* unn;        // |u_{n-1,n-1}| per vector
+    double* zscale;     // sign/||x||_2 of finished (j_c == 0) vectors
+    int* iters;         // iteration count per vector
+    PrepOut* out;
+};
+
+struct FinalizeArgs {
+    int64_t n;
+    int64_t ldv;
+    const double* X;
+    const double* zscale;
+    const int* jc;
+    double* Z;
+    int64_t ldz;
+};
+
+// Per-group workspace of the persistent compact-WY kernel.
+struct GroupWS {
+    double* Y;          // packed row-major Y (y_row_off(n, mcap) doubles)
+    double* Tc;         // column-packed T (tcol_off(mcap))
+    double* Tr;         // row-major T, row stride m2cap (mcap * m2cap)
+    double* x;          // current iterate (n)
+    double* q;          // orthogonalised vector (n)
+    double* u;          // uhat / yhat (n)
+    double* g;          // Y^T x, then T^T g   (mcap)
+    double* gp;         // T^T g               (mcap)
+    double* s;          // Yhat^T yhat          (mcap)
+    double* xp;         // T_{p+1} y_row        (mcap + 1)
+    double* P;          // partial sums [G][mcap]
+    double* S;          // scalar partials [G][8]
+    double* ysol;       // forward-sweep workspace of the chained solve (n)
+    GroupBarrier* bar;
+    int64_t mcap;
+};
+
+struct CwyArgs {
+    int64_t n;
+    int64_t ldv;
+    const double* d;
+    const double* e;
+    double tnorm;
+    uint64_t seed;
+    const double* wt;
+    const int* cstart;
+    const double* fl;
+    const int8_t* fp;
+    const double* fr;
+    const double* fb;
+    const double* fc;
+    const double* unn;
+    const double* X1;   // x^(1) of every vector, [i][j]
+    double* Z;
+    int64_t ldz;
+    int* iters;
+    PrepOut* out;
+    // schedule
+    int ngroups;
+    const int* g_cta0;       // first CTA of each group
+    const int* g_size;       // CTAs per group
+    const int* g_coff;       // offsets into g_clist
+    const int* g_clist;      // cluster ids per group
+    GroupWS* ws;             // per group
+    long long* syncs;        // per group: barrier episodes (stats)
+    unsigned long long* prof;  // optional per-group phase times [g*16 + phase] (ns), or NULL
+};
+
+void launch_prep(const PrepArgs& a, cudaStream_t s);
+void launch_batched(const BatchedArgs& a, cudaStream_t s);
+void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
+void launch_identity(double* Z, int64_t n, int64_t ldz, cudaStream_t s);
+cudaError_t launch_cwy(const CwyArgs& a, int nctas, cudaStream_t s);
+int cwy_threads();
+int cwy_max_ctas_per_sm();
+
+}  // namespace tinv

@@ -1,0 +1,181 @@
+"""Python binding of libtinv.so (include/tinv.h): argument marshalling only.
+
+Every step of the path runs in the library's sm_100a kernels; this module only turns
+torch tensors / numpy arrays into pointers.  There is no CPU fallback: if the shared
+library is missing or no CUDA device is usable, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtinv.so")
+
+EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
+           "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version")
+
+KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
+PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve")
+
+
+class TinvConfig(C.Structure):
+    _fields_ = [("device", C.c_int), ("nranks", C.c_int), ("rank", C.c_int),
+                ("nccl_id", C.c_void_p), ("stream", C.c_void_p)]
+
+
+class TinvStats(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nclusters", C.c_int64), ("max_cluster", C.c_int64),
+                ("n_clustered", C.c_int64), ("nflagged", C.c_int64), ("iters_hist", C.c_int64 * 8),
+                ("launches", C.c_int64), ("group_syncs", C.c_int64), ("ngroups", C.c_int64),
+                ("cwy_ctas", C.c_int64), ("reorth_bytes", C.c_double), ("solve_bytes", C.c_double),
+                ("kernel_ms", C.c_double * 6), ("kernel_launches", C.c_int64 * 6),
+                ("cwy_phase_ms", C.c_double * 10)]
+
+    def as_dict(self):
+        return {
+            "n": self.n, "nclusters": self.nclusters, "max_cluster": self.max_cluster,
+            "n_clustered": self.n_clustered, "nflagged": self.nflagged,
+            "iters_hist": list(self.iters_hist), "launches": self.launches,
+            "group_syncs": self.group_syncs, "ngroups": self.ngroups, "cwy_ctas": self.cwy_ctas,
+            "reorth_bytes": self.reorth_bytes, "solve_bytes": self.solve_bytes,
+            "kernel_ms": dict(zip(KERNEL_NAMES, list(self.kernel_ms))),
+            "kernel_launches": dict(zip(KERNEL_NAMES, list(self.kernel_launches))),
+            "cwy_phase_ms": dict(zip(PHASE_NAMES, list(self.cwy_phase_ms))),
+        }
+
+
+class TinvError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libtinv.so and declare the C signatures (no CUDA needed for this step)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise TinvError(f"{path} is missing: build it with __graft_entry__.build() (make -C paper_1209_1910_b200/csrc)")
+    L = C.CDLL(path)
+    P = C.c_void_p
+    I64 = C.c_int64
+    L.tinv_create.argtypes = [C.POINTER(P), C.POINTER(TinvConfig)]
+    L.tinv_create.restype = C.c_int
+    L.tinv_eigvecs.argtypes = [P, I64, P, P, P, P, I64, C.c_uint64]
+    L.tinv_eigvecs.restype = C.c_int
+    L.tinv_eigvecs_host.argtypes = [P, I64, P, P, P, P, I64, C.c_uint64]
+    L.tinv_eigvecs_host.restype = C.c_int
+    L.tinv_destroy.argtypes = [P]
+    L.tinv_destroy.restype = C.c_int
+    L.tinv_strerror.argtypes = [C.c_int]
+    L.tinv_strerror.restype = C.c_char_p
+    L.tinv_set_profiling.argtypes = [P, C.c_int]
+    L.tinv_set_profiling.restype = C.c_int
+    L.tinv_get_stats.argtypes = [P, C.POINTER(TinvStats)]
+    L.tinv_get_stats.restype = C.c_int
+    L.tinv_abi_version.argtypes = []
+    L.tinv_abi_version.restype = C.c_int
+    _lib = L
+    return L
+
+
+def strerror(code: int) -> str:
+    return load_library().tinv_strerror(int(code)).decode()
+
+
+class Tinv:
+    """Handle on one GPU (tinv_create).  ``stream`` defaults to torch's current stream."""
+
+    def __init__(self, device: int = 0, stream=None, nranks: int = 1, rank: int = 0, nccl_id: bytes | None = None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise TinvError("no CUDA device: libtinv has no CPU fallback")
+        self._torch = torch
+        L = load_library()
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        self._idbuf = None
+        cfg = TinvConfig(device, nranks, rank, None, C.c_void_p(stream.cuda_stream))
+        if nccl_id is not None:
+            self._idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            cfg.nccl_id = C.cast(self._idbuf, C.c_void_p)
+        h = C.c_void_p()
+        rc = L.tinv_create(C.byref(h), C.byref(cfg))
+        if rc != 0:
+            raise TinvError(f"tinv_create failed: {rc} ({strerror(rc)})")
+        self._h = h
+        self._L = L
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tinv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_profiling(self, on: bool = True):
+        self._L.tinv_set_profiling(self._h, 1 if on else 0)
+
+    def stats(self) -> dict:
+        s = TinvStats()
+        self._L.tinv_get_stats(self._h, C.byref(s))
+        return s.as_dict()
+
+    def eigvecs(self, d, e, w, Z=None, seed: int = 1, check: bool = True):
+        """Device path: d, e, w are float64 CUDA tensors; returns (Z, info) with Z an
+        (n, n) tensor whose COLUMNS are the eigenvectors (column-major storage)."""
+        torch = self._torch
+        n = int(d.shape[0])
+        for name, t in (("d", d), ("w", w)) + ((("e", e),) if n > 1 else ()):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise TinvError(f"{name} must be a contiguous float64 CUDA tensor")
+        if Z is None:
+            Zt = torch.empty((n, n), dtype=torch.float64, device=d.device)  # Zt[j] = column j
+        else:
+            Zt = Z
+        rc = self._L.tinv_eigvecs(self._h, n, C.c_void_p(d.data_ptr()),
+                                  C.c_void_p(e.data_ptr()) if n > 1 else None,
+                                  C.c_void_p(w.data_ptr()), C.c_void_p(Zt.data_ptr()), n, int(seed))
+        if rc < 0 and check:
+            raise TinvError(f"tinv_eigvecs failed: {rc} ({strerror(rc)})")
+        return Zt.t(), rc
+
+    def eigvecs_host(self, d, e, w, Z=None, seed: int = 1, check: bool = True):
+        """End-to-end path with host buffers (numpy or pinned CPU tensors)."""
+        n = int(np.asarray(d).shape[0]) if not hasattr(d, "data_ptr") else int(d.shape[0])
+
+        def ptr(a):
+            if a is None:
+                return None
+            if hasattr(a, "data_ptr"):
+                return C.c_void_p(a.data_ptr())
+            return a.ctypes.data_as(C.c_void_p)
+
+        if Z is None:
+            Z = np.empty((n, n), dtype=np.float64)  # row j = column j of the column-major Z
+        rc = self._L.tinv_eigvecs_host(self._h, n, ptr(d), ptr(e) if n > 1 else None, ptr(w), ptr(Z), n, int(seed))
+        if rc < 0 and check:
+            raise TinvError(f"tinv_eigvecs_host failed: {rc} ({strerror(rc)})")
+        return Z, rc
+
+
+def eigvecs(d, e, w, seed: int = 1, device: int = 0):
+    """One-shot convenience wrapper (creates and destroys a handle)."""
+    h = Tinv(device)
+    try:
+        Z, rc = h.eigvecs(d, e, w, seed=seed)
+        return Z, rc, h.stats()
+    finally:
+        h.close()

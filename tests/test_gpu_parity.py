@@ -1,0 +1,249 @@
+"""GPU parity: the C-ABI product path (libtinv.so via paper_1209_1910_b200.tinv) against
+the CPU oracle on the same seeded inputs.
+
+Contract (BASELINE.json north_star):
+  P0  max_j ||T z_j - w_j z_j||_2 <= 10 n eps ||T||_1 and max|Z^T Z - I| <= 10 n eps
+  P1/P3  vectors whose gaps to both neighbours exceed 1e-6 ||T||_1 agree with the oracle
+      up to sign within 1e-10 (max-norm); P2/P3 runs chained at that gap agree as
+      subspaces: sigma_min(Z_gpu^T Z_oracle) >= 1 - 1e-10.
+Full-size configs the oracle cannot finish in seconds (cfg4, cfg5) are checked with the
+invariants at full size plus sampled columns the oracle computes (its range mode).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1209_1910_b200 import workloads as W
+from tests.helpers import EPS, groups, parity_report, sigma_min, vec_diff_upto_sign
+
+pytestmark = pytest.mark.gpu
+
+TOL_VEC = 1e-10
+TOL_SUB = 1e-10
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def handle(torch):
+    from paper_1209_1910_b200.tinv import Tinv
+
+    h = Tinv(0)
+    yield h
+    h.close()
+
+
+def run_gpu(handle, torch, d, e, w, seed=1):
+    dev = torch.device("cuda:0")
+    dt = torch.tensor(d, dtype=torch.float64, device=dev)
+    et = torch.tensor(e if len(d) > 1 else np.zeros(1), dtype=torch.float64, device=dev)
+    wt = torch.tensor(w, dtype=torch.float64, device=dev)
+    Z, rc = handle.eigvecs(dt, et, wt, seed=seed)
+    torch.cuda.synchronize()
+    return Z, rc
+
+
+def invariants_gpu(torch, d, e, w, Z):
+    """P0 on the device (fp64 cuBLAS for Z^T Z; elementwise residual)."""
+    n = len(d)
+    dev = Z.device
+    dt = torch.tensor(d, dtype=torch.float64, device=dev)
+    wt = torch.tensor(w, dtype=torch.float64, device=dev)
+    TZ = dt[:, None] * Z
+    if n > 1:
+        et = torch.tensor(e, dtype=torch.float64, device=dev)
+        TZ[:-1] += et[:, None] * Z[1:]
+        TZ[1:] += et[:, None] * Z[:-1]
+    tn = O.tnorm(d, e)
+    res = torch.linalg.vector_norm(TZ - Z * wt[None, :], dim=0).max().item() / (n * EPS * tn)
+    G = Z.t() @ Z
+    G.diagonal().sub_(1.0)
+    orth = G.abs().max().item() / (n * EPS)
+    return res, orth
+
+
+def full_parity(handle, torch, d, e, w, seed=1):
+    Zg, rc = run_gpu(handle, torch, d, e, w, seed)
+    assert rc == 0, f"tinv_eigvecs returned {rc}"
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0, f"residual {res} x n eps ||T||"
+    assert orth <= 10.0, f"orthogonality {orth} x n eps"
+    Zo, info = O.eigvecs(d, e, w, seed=seed)
+    assert info == 0
+    Zg_h = Zg.cpu().numpy()
+    wv, ws, nv, ng = parity_report(w, O.tnorm(d, e), Zg_h, Zo)
+    assert wv <= TOL_VEC, f"per-vector diff {wv}"
+    assert ws >= 1 - TOL_SUB, f"subspace sigma_min {ws}"
+    return Zg_h, Zo, (res, orth, wv, ws, nv, ng)
+
+
+# ------------------------------------------------------------------ BASELINE configs
+
+def test_cfg1_laplacian_full(handle, torch):
+    d, e, w = W.problem("cfg1")
+    Zg, Zo, rep = full_parity(handle, torch, d, e, w)
+    # the canonical sign rule (reading 15) makes determined vectors identical wherever the
+    # largest |entry| is unique beyond rounding (the Laplacian's symmetric vectors have two
+    # mirror-image maxima, where the rule is decided by rounding and only +-z is defined)
+    tn = O.tnorm(d, e)
+    nsame = 0
+    for s, t in groups(w, 1e-6 * tn):
+        if t - s == 1:
+            a = np.sort(np.abs(Zo[:, s]))
+            if a[-2] < a[-1] * (1 - 1e-8):
+                assert np.abs(Zg[:, s] - Zo[:, s]).max() <= TOL_VEC
+                nsame += 1
+    assert nsame >= 0
+
+
+def test_cfg2_random_full(handle, torch):
+    d, e, w = W.problem("cfg2")
+    full_parity(handle, torch, d, e, w)
+
+
+def test_cfg3_glued_wilkinson_full(handle, torch):
+    d, e, w = W.problem("cfg3")
+    full_parity(handle, torch, d, e, w)
+
+
+@pytest.mark.parametrize("cfg,n", [("cfg3", 1050), ("cfg4", 600), ("cfg5", 1500), ("type1", 2100),
+                                   ("type2", 700), ("type3", 1050)])
+def test_scaled_configs_full(handle, torch, cfg, n):
+    d, e, w = W.problem(cfg, n)
+    full_parity(handle, torch, d, e, w)
+
+
+def test_cfg4_giant_cluster_full_size(handle, torch):
+    d, e, w = W.problem("cfg4")
+    Zg, rc = run_gpu(handle, torch, d, e, w)
+    assert rc == 0
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
+    # sampled columns: the oracle's first K vectors of the (single) cluster; individual
+    # vectors of cfg4 are ill-determined (gaps < 1e-8 ||T||), so report, do not gate
+    K = 48
+    Zo, info = O.eigvecs(d, e, w, seed=1, j_lo=0, j_hi=K)
+    diff = max(vec_diff_upto_sign(Zg[:, k].cpu().numpy(), Zo[:, k]) for k in range(K))
+    print(f"cfg4 sampled per-vector diff (reported) {diff:.3e}")
+
+
+def test_cfg5_perturbed_laplacian_full_size(handle, torch):
+    d, e, w = W.problem("cfg5")
+    Zg, rc = run_gpu(handle, torch, d, e, w)
+    assert rc == 0
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
+    K = 96
+    Zo, info = O.eigvecs(d, e, w, seed=1, j_lo=0, j_hi=K)
+    Zs = Zg[:, :K].cpu().numpy()
+    tn = O.tnorm(d, e)
+    for s, t in groups(w[:K], 1e-6 * tn):
+        if t == K:       # a run that may continue past the sample is not complete
+            continue
+        if t - s == 1:
+            assert vec_diff_upto_sign(Zs[:, s], Zo[:, s]) <= TOL_VEC
+        else:
+            assert sigma_min(Zs[:, s:t], Zo[:, s:t]) >= 1 - TOL_SUB
+
+
+# ------------------------------------------------------------------ edge cases
+
+@pytest.mark.parametrize("n", [2, 3, 5, 31, 33, 37, 129, 1001])
+def test_ragged_sizes(handle, torch, n):
+    d, e, w = W.problem("type1", n, seed=n)
+    full_parity(handle, torch, d, e, w)
+
+
+def test_n1_and_zero_matrix(handle, torch):
+    Z, rc = run_gpu(handle, torch, np.array([3.0]), np.zeros(0), np.array([3.0]))
+    assert rc == 0 and Z.cpu().numpy().tolist() == [[1.0]]
+    Z, rc = run_gpu(handle, torch, np.zeros(5), np.zeros(4), np.zeros(5))
+    assert rc == 0 and np.array_equal(Z.cpu().numpy(), np.eye(5))
+
+
+def test_diagonal_and_split_matrix(handle, torch):
+    d = np.array([3.0, -1.0, 2.0, 7.0, 0.5])
+    w = np.sort(d)
+    full_parity(handle, torch, d, np.zeros(4), w)
+    # a zero off-diagonal splits T into blocks
+    d, e = W.random_sym(300, 7)
+    e[100] = 0.0
+    e[200] = 0.0
+    full_parity(handle, torch, d, e, W.eigenvalues(d, e))
+
+
+def test_exact_duplicates(handle, torch):
+    # two identical decoupled W21+ blocks: every eigenvalue exactly duplicated
+    d, e = W.glued_wilkinson(2, 0.0)
+    full_parity(handle, torch, d, e, W.eigenvalues(d, e))
+
+
+def test_invalid_arguments(handle, torch):
+    import ctypes as C
+
+    L = handle._L
+    dev = torch.device("cuda:0")
+    d = torch.ones(4, dtype=torch.float64, device=dev)
+    e = torch.ones(3, dtype=torch.float64, device=dev)
+    w = torch.arange(4, dtype=torch.float64, device=dev)
+    Z = torch.empty(16, dtype=torch.float64, device=dev)
+    P = lambda t: C.c_void_p(t.data_ptr())
+    assert L.tinv_eigvecs(handle._h, 0, P(d), P(e), P(w), P(Z), 4, 1) == -2
+    assert L.tinv_eigvecs(handle._h, 4, None, P(e), P(w), P(Z), 4, 1) == -3
+    assert L.tinv_eigvecs(handle._h, 4, P(d), None, P(w), P(Z), 4, 1) == -4
+    assert L.tinv_eigvecs(handle._h, 4, P(d), P(e), P(w), P(Z), 3, 1) == -7
+    bad = d.clone()
+    bad[2] = float("nan")
+    assert L.tinv_eigvecs(handle._h, 4, P(bad), P(e), P(w), P(Z), 4, 1) == -3
+    wdesc = torch.tensor([3.0, 2.0, 1.0, 0.0], dtype=torch.float64, device=dev)
+    assert L.tinv_eigvecs(handle._h, 4, P(d), P(e), P(wdesc), P(Z), 4, 1) == -5
+    assert L.tinv_eigvecs(None, 4, P(d), P(e), P(w), P(Z), 4, 1) == -103
+
+
+def test_ldz_larger_than_n(handle, torch):
+    import ctypes as C
+
+    d, e, w = W.problem("cfg2", 300)
+    n, ldz = 300, 317
+    dev = torch.device("cuda:0")
+    dt, et, wt = (torch.tensor(a, dtype=torch.float64, device=dev) for a in (d, e, w))  # kept alive
+    Zbuf = torch.full((n, ldz), 7.0, dtype=torch.float64, device=dev)
+    rc = handle._L.tinv_eigvecs(handle._h, n, C.c_void_p(dt.data_ptr()), C.c_void_p(et.data_ptr()),
+                                C.c_void_p(wt.data_ptr()), C.c_void_p(Zbuf.data_ptr()), ldz, 1)
+    torch.cuda.synchronize()
+    assert rc == 0
+    Zb = Zbuf.cpu().numpy()
+    assert (Zb[:, n:] == 7.0).all()              # padding rows untouched
+    Zg, _ = run_gpu(handle, torch, d, e, w)
+    assert np.array_equal(Zb[:, :n].T, Zg.cpu().numpy())
+
+
+# ------------------------------------------------------------------ determinism / paths
+
+def test_deterministic_bitwise(handle, torch):
+    d, e, w = W.problem("cfg3", 840)
+    Z1, _ = run_gpu(handle, torch, d, e, w)
+    Z2, _ = run_gpu(handle, torch, d, e, w)
+    assert torch.equal(Z1, Z2)
+
+
+def test_host_path_equals_device_path(handle, torch):
+    d, e, w = W.problem("cfg2", 500)
+    Zd, _ = run_gpu(handle, torch, d, e, w)
+    Zh, rc = handle.eigvecs_host(np.ascontiguousarray(d), np.ascontiguousarray(e), np.ascontiguousarray(w), seed=1)
+    assert rc == 0
+    assert np.array_equal(Zh.T, Zd.cpu().numpy())
+
+
+def test_stats_report_native_launches(handle, torch):
+    d, e, w = W.problem("cfg2", 400)
+    run_gpu(handle, torch, d, e, w)
+    st = handle.stats()
+    assert st["launches"] >= 3 and st["n"] == 400 and st["nclusters"] >= 1
+    assert sum(st["iters_hist"]) == 400
