@@ -28,8 +28,18 @@
 
 namespace tinv {
 
-constexpr int NT = 512;
+constexpr int NT = 256;
 constexpr int NW = NT / 32;
+constexpr int CFCH = 2048;   // rows whose coefficients are staged in shared memory at once
+constexpr int CH = 512;      // chained-solve chunk (rows)
+
+// Global accesses: data produced inside this kernel by other CTAs goes through L2 (.cg,
+// never a stale L1 line); explicit global-space intrinsics also let the compiler hoist
+// shared-memory loads across the stores (no generic-pointer aliasing).
+__device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ double2 ld2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ void st(double* p, double v) { __stcg(p, v); }
+__device__ __forceinline__ double ldro(const double* p) { return __ldg(p); }
 
 struct SSlots {  // scalar partial slots per CTA (ws.S[r*8 + slot])
     enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4 };
@@ -41,6 +51,12 @@ __device__ __forceinline__ int pow2ceil(int v) {
     return p;
 }
 
+__device__ __forceinline__ uint64_t gtime() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // smallest i in [lo, hi] with cum(i) >= target (cum non-decreasing)
 template <class F>
 __device__ __forceinline__ int64_t bsearch_cum(int64_t lo, int64_t hi, int64_t target, F cum) {
@@ -50,147 +66,217 @@ __device__ __forceinline__ int64_t bsearch_cum(int64_t lo, int64_t hi, int64_t t
     }
     return lo;
 }
-
 // rows of A / D weighted by their length min(i+1, P)
 __device__ __forceinline__ void part_rows_weighted(int64_t n, int64_t P, int r, int G, int64_t& a, int64_t& b) {
     auto cum = [P](int64_t i) -> int64_t { return i <= P ? i * (i + 1) / 2 : P * (P + 1) / 2 + (i - P) * P; };
     int64_t W = cum(n);
-    a = bsearch_cum(0, n, (W * r) / G, cum);
-    b = bsearch_cum(0, n, (W * (r + 1)) / G, cum);
-    if (r == G - 1) b = n;
-    if (r == 0) a = 0;
+    a = (r == 0) ? 0 : bsearch_cum(0, n, (W * r) / G, cum);
+    b = (r == G - 1) ? n : bsearch_cum(0, n, (W * (r + 1)) / G, cum);
 }
 __device__ __forceinline__ void part_uniform(int64_t lo, int64_t hi, int r, int G, int64_t& a, int64_t& b) {
     int64_t len = hi - lo;
     a = lo + (len * r) / G;
     b = lo + (len * (r + 1)) / G;
 }
-// k in [0,p) weighted by k+1 (T^T rows = packed columns of T)
+// k in [0,p) weighted by k+1 (packed columns of T)
 __device__ __forceinline__ void part_tt(int64_t p, int r, int G, int64_t& a, int64_t& b) {
     auto cum = [](int64_t k) -> int64_t { return k * (k + 1) / 2; };
     int64_t W = cum(p);
-    a = bsearch_cum(0, p, (W * r) / G, cum);
-    b = bsearch_cum(0, p, (W * (r + 1)) / G, cum);
-    if (r == G - 1) b = p;
-    if (r == 0) a = 0;
+    a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
+    b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
 }
 // l in [0,p) weighted by p-l (rows of T)
 __device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int64_t& b) {
     auto cum = [p](int64_t l) -> int64_t { return l * p - l * (l - 1) / 2; };
     int64_t W = cum(p);
-    a = bsearch_cum(0, p, (W * r) / G, cum);
-    b = bsearch_cum(0, p, (W * (r + 1)) / G, cum);
-    if (r == G - 1) b = p;
-    if (r == 0) a = 0;
+    a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
+    b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
 }
 
-__device__ __forceinline__ uint64_t gtime() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-struct Shared {
-    double red[NW];
-    double2 acc[NT];
+// dynamic shared memory carve-up
+struct Smem {
+    double* vs;      // staged vector (vcap + 2 doubles); aliased by the chained-solve buffers
+    double* cf;      // CFCH coefficients
+    double2* acc;    // NT
+    double* red;     // NW + 8
 };
 
-// ---------------------------------------------------------------- column accumulate
-// out[k] = sum_{i in [i0,i1), i >= k} Y[i][k] * coef(i)  for k < P   (coef(i) = cp[i*cs])
-__device__ void colacc(const double* __restrict__ Y, int64_t m, int64_t i0, int64_t i1, int64_t P,
-                       const double* cp, int64_t cs, double* __restrict__ out, Shared& sh) {
-    if (P <= 0) return;
-    const int tid = threadIdx.x;
-    const int CPT = min(NT, pow2ceil((int)((P + 1) / 2)));
-    const int RS = NT / CPT;
-    const int cpi = tid % CPT, rs = tid / CPT;
-    for (int64_t k0 = 0; k0 < P; k0 += 2 * CPT) {
-        const int64_t k = k0 + 2 * cpi;
-        double a0 = 0.0, a1 = 0.0;
-        if (k < P) {
-            const bool two = (k + 1 < P);
-            int64_t ia = (i0 > k) ? i0 : k;
-#pragma unroll 4
-            for (int64_t i = ia + rs; i < i1; i += RS) {
-                const double cf = cp[i * cs];
-                const double2 v = *reinterpret_cast<const double2*>(Y + y_row_off(i, m) + k);
-                a0 = fma(v.x, cf, a0);
-                const double vy = (two && k + 1 <= i) ? v.y : 0.0;
-                a1 = fma(vy, cf, a1);
-            }
-        }
-        if (RS > 1) {
-            __syncthreads();
-            sh.acc[tid] = make_double2(a0, a1);
-            __syncthreads();
-            if (rs == 0) {
-                for (int r2 = 1; r2 < RS; r2++) {
-                    double2 t = sh.acc[cpi + r2 * CPT];
-                    a0 += t.x;
-                    a1 += t.y;
-                }
-            }
-        }
-        if (rs == 0 && k < P) {
-            out[k] = a0;
-            if (k + 1 < P) out[k + 1] = a1;
-        }
+struct SolveBuf {    // lives in Smem::vs during the chained solve
+    double* a[2];
+    double* b[2];
+    double* c[2];
+    int8_t* sw[2];
+};
+__device__ __forceinline__ SolveBuf solve_buf(const Smem& sm) {
+    SolveBuf sb;
+    for (int t = 0; t < 2; t++) {
+        sb.a[t] = sm.vs + (0 + t) * CH;
+        sb.b[t] = sm.vs + (2 + t) * CH;
+        sb.c[t] = sm.vs + (4 + t) * CH;
+        sb.sw[t] = reinterpret_cast<int8_t*>(sm.vs + 6 * CH) + t * CH;
     }
+    return sb;
+}
+constexpr int64_t kSolveDoubles = 6 * CH + (2 * CH) / 8;
+
+// copy len doubles of a global vector into sm.vs (zero padded by 2), then barrier
+__device__ __forceinline__ void stage_vec(const Smem& sm, const double* src, int64_t len) {
+    for (int64_t k = threadIdx.x; k < len + 2; k += NT) sm.vs[k] = (k < len) ? ld(src + k) : 0.0;
     __syncthreads();
 }
 
 // ---------------------------------------------------------------- row dots
-// For rows i in [i0,i1): dot_i = sum_{k < L_i} R(i)[k] * v[k], L_i = min(len(i), P);
-// rowptr(i) gives a 16-byte aligned row start, k0(i) the first valid column (even-aligned
-// start handled by masking).  The epilogue f(i, dot) runs on one lane per row.
-template <class RowPtr, class RowRange, class Epi>
-__device__ __forceinline__ void rowdots(int64_t i0, int64_t i1, int64_t P, const double* __restrict__ v,
-                                        RowPtr rowptr, RowRange range, Epi f) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int LPR = min(32, pow2ceil((int)((P + 1) / 2 > 0 ? (P + 1) / 2 : 1)));
-    const int RPW = 32 / LPR;
-    const int sub = lane / LPR, sl = lane % LPR;
-    for (int64_t ib = i0 + (int64_t)warp * RPW; ib < i1; ib += (int64_t)NW * RPW) {
-        const int64_t i = ib + sub;
-        double acc = 0.0;
-        if (i < i1) {
-            const double* row = rowptr(i);
-            int64_t kb, ke;
-            range(i, kb, ke);  // valid columns [kb, ke)
-            const int64_t kstart = kb & ~int64_t(1);
-#pragma unroll 4
-            for (int64_t k = kstart + 2 * sl; k < ke; k += 2 * LPR) {
-                const double2 a = *reinterpret_cast<const double2*>(row + k);
-                const double2 b = *reinterpret_cast<const double2*>(v + k);
-                const bool vx = (k >= kb), vy = (k + 1 < ke);  // mask operands (stale slots)
-                acc = fma(vx ? a.x : 0.0, vx ? b.x : 0.0, acc);
-                acc = fma(vy ? a.y : 0.0, vy ? b.y : 0.0, acc);
+// For rows i in [i0,i1): dot_i = sum_{k < len(i)} R(i)[k] * vs[k] (len(i) <= P, R(i) 16-byte
+// aligned, vs staged in shared memory); epi(i, dot) runs on one lane per row.  Short rows
+// (P <= 64) pack several rows per warp and batch 4 rows of loads; long rows batch 8 loads
+// per lane.
+template <class RowPtr, class RowLen, class Epi>
+__device__ __forceinline__ void rowdots(int64_t i0, int64_t i1, int64_t P, const double* vs, RowPtr rowptr,
+                                        RowLen rowlen, Epi epi) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (P <= 0) {
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += NT) epi(i, 0.0);
+        return;
+    }
+    if (P <= 64) {
+        const int LPR = pow2ceil((int)((P + 1) / 2));
+        const int RPW = 32 / LPR;
+        const int sub = lane / LPR, sl = lane % LPR;
+        const int64_t k = 2 * sl;
+        const double vx = (k < P) ? vs[k] : 0.0, vy = (k + 1 < P) ? vs[k + 1] : 0.0;
+        constexpr int U = 4;
+        for (int64_t ib = i0 + (int64_t)warp * RPW * U; ib < i1; ib += (int64_t)NW * RPW * U) {
+            double2 a[U];
+            int64_t ke[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t i = ib + u * RPW + sub;
+                ke[u] = (i < i1) ? rowlen(i) : 0;
+                a[u] = (k < ke[u]) ? ld2(rowptr(i) + k) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t i = ib + u * RPW + sub;
+                double acc = fma(a[u].x, vx, 0.0);
+                acc = fma((k + 1 < ke[u]) ? a[u].y : 0.0, vy, acc);
+                for (int o = LPR >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (sl == 0 && i < i1) epi(i, acc);
             }
         }
-        for (int o = LPR >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sl == 0 && i < i1) f(i, acc);
+        return;
     }
+    constexpr int U = 8;
+    for (int64_t i = i0 + warp; i < i1; i += NW) {
+        const double* row = rowptr(i);
+        const int64_t ke = rowlen(i);
+        double acc = 0.0;
+        for (int64_t k0 = 2 * lane; k0 < ke; k0 += 64 * U) {
+            double2 a[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t k = k0 + 64 * u;
+                a[u] = (k < ke) ? ld2(row + k) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t k = k0 + 64 * u;
+                if (k < ke) {
+                    const double2 b = *reinterpret_cast<const double2*>(vs + k);
+                    acc = fma(a[u].x, b.x, acc);
+                    if (k + 1 < ke) acc = fma(a[u].y, b.y, acc);
+                }
+            }
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) epi(i, acc);
+    }
+}
+
+// ---------------------------------------------------------------- column accumulate
+// out[k] = sum_{i in [i0,i1), i >= k} Y[i][k] * coef(i)  for k < P, coef(i) = cp[i*cs].
+// Thread t owns a column pair (2 doubles, 16-byte loads) and a subset of the rows; the
+// coefficients of a row chunk are staged in shared memory.  Returns sum coef(i)^2.
+__device__ double colacc(const Smem& sm, const double* __restrict__ Y, int64_t m, int64_t i0, int64_t i1,
+                         int64_t P, const double* cp, int64_t cs, double* out) {
+    const int tid = threadIdx.x;
+    const int CPT = (P > 0) ? min(NT, pow2ceil((int)((P + 1) / 2))) : NT;
+    const int RS = NT / CPT;
+    const int cpi = tid % CPT, rs = tid / CPT;
+    double c2 = 0.0;
+    constexpr int U = 8;
+    if (i1 <= i0) {   // no rows: this CTA's partial is zero (it is still summed by R1/R2)
+        for (int64_t k = tid; k < P; k += NT) st(out + k, 0.0);
+        return 0.0;
+    }
+    for (int64_t rc0 = i0; rc0 < i1; rc0 += CFCH) {
+        const int64_t rc1 = (i1 - rc0 > CFCH) ? rc0 + CFCH : i1;
+        for (int64_t i = rc0 + tid; i < rc1; i += NT) {
+            const double c = ld(cp + i * cs);
+            sm.cf[i - rc0] = c;
+            c2 = fma(c, c, c2);
+        }
+        __syncthreads();
+        for (int64_t k0 = 0; k0 < P; k0 += 2 * CPT) {
+            const int64_t k = k0 + 2 * cpi;
+            double a0 = 0.0, a1 = 0.0;
+            if (k < P) {
+                const bool two = (k + 1 < P);
+                const int64_t ia = (rc0 > k) ? rc0 : k;
+                for (int64_t i = ia + rs; i < rc1; i += (int64_t)RS * U) {
+                    double2 v[U];
+                    double c[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int64_t ii = i + (int64_t)u * RS;
+                        const bool ok = ii < rc1;
+                        v[u] = ok ? ld2(Y + y_row_off(ii, m) + k) : make_double2(0.0, 0.0);
+                        c[u] = ok ? sm.cf[ii - rc0] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int64_t ii = i + (int64_t)u * RS;
+                        a0 = fma(v[u].x, c[u], a0);
+                        a1 = fma((two && k + 1 <= ii) ? v[u].y : 0.0, c[u], a1);
+                    }
+                }
+            }
+            if (RS > 1) {
+                sm.acc[tid] = make_double2(a0, a1);
+                __syncthreads();
+                if (rs == 0)
+                    for (int r2 = 1; r2 < RS; r2++) {
+                        const double2 t = sm.acc[cpi + r2 * CPT];
+                        a0 += t.x;
+                        a1 += t.y;
+                    }
+                __syncthreads();
+            }
+            if (rs == 0 && k < P) {
+                if (rc0 == i0) {
+                    st(out + k, a0);
+                    if (k + 1 < P) st(out + k + 1, a1);
+                } else {
+                    st(out + k, ld(out + k) + a0);
+                    if (k + 1 < P) st(out + k + 1, ld(out + k + 1) + a1);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    return c2;
 }
 
 // ---------------------------------------------------------------- chained single-vector solve
 // x = (T - wt_j I)^{-1} (sigma * rhs), sigma = n ||T||_1 max(eps,|u_nn|) / ||rhs||_1,
 // with the factors stored by the batched kernel.  rhs = q (mode 0) or the start vector of
-// restart `restart` (mode 1).  The recurrences are serial: lane 0 of warp 0 runs them out of
-// shared memory while warps 1..NW-1 stage the next chunk of factors (double buffer), so the
-// dependent chain is one FMA per row (forward: c <- alpha c + beta with alpha, beta
+// restart `restart` (mode 1).  The recurrences are serial: lane 0 of warp 0 runs them out
+// of shared memory while warps 1..NW-1 stage the next chunk of factors (double buffer);
+// the dependent chain is one FMA per row (forward: c <- alpha c + beta with alpha, beta
 // precomputed from the pivot bit; back: x_i <- -b_i x_{i+1} + (s y_i r_i - c_i x_{i+2})).
-constexpr int CH = 512;
-struct SolveSmem {
-    double a[2][CH];
-    double b[2][CH];
-    double c[2][CH];
-    int8_t sw[2][CH];
-};
-
 __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int mode, int restart,
-                            SolveSmem& sm, double* red) {
+                            const Smem& sm) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t n = a.n, ld = a.ldv;
+    const int64_t n = a.n, ld_ = a.ldv;
     const double* __restrict__ fl = a.fl + j;
     const int8_t* __restrict__ fp = a.fp + j;
     const double* __restrict__ fr = a.fr + j;
@@ -198,8 +284,9 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
     const double* __restrict__ fc = a.fc + j;
     double* __restrict__ ys = ws.ysol;
     const double* __restrict__ q = ws.q;
-    auto rhs = [&](int64_t i) -> double { return mode == 0 ? q[i] : start_entry(a.seed, n, j, restart, i); };
-    const int LT = NT - 32;  // loader threads
+    const SolveBuf sb = solve_buf(sm);
+    auto rhs = [&](int64_t i) -> double { return mode == 0 ? ld(q + i) : start_entry(a.seed, n, j, restart, i); };
+    const int LT = NT - 32;
     const int lt = tid - 32;
 
     // ---- forward elimination: steps i = 0 .. n-2
@@ -210,14 +297,14 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
         for (int idx = lt; idx < CH; idx += LT) {
             const int64_t i = ch * CH + idx;
             if (i < nf) {
-                const double l = fl[i * ld];
-                const int8_t sw = fp[i * ld];
+                const double l = ldro(fl + i * ld_);
+                const int8_t sw = __ldg(fp + i * ld_);
                 const double bn = rhs(i + 1);
                 r1 += fabs(bn);
-                sm.a[buf][idx] = sw ? 1.0 : -l;
-                sm.b[buf][idx] = sw ? -l * bn : bn;
-                sm.c[buf][idx] = bn;
-                sm.sw[buf][idx] = sw;
+                sb.a[buf][idx] = sw ? 1.0 : -l;
+                sb.b[buf][idx] = sw ? -l * bn : bn;
+                sb.c[buf][idx] = bn;
+                sb.sw[buf][idx] = sw;
             }
         }
     };
@@ -231,11 +318,23 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
             if (lane == 0) {
                 const int cnt = (int)((nf - ch * CH) < CH ? (nf - ch * CH) : CH);
                 double* yo = ys + ch * CH;
-#pragma unroll 8
-                for (int idx = 0; idx < cnt; idx++) {
-                    const double y = sm.sw[buf][idx] ? sm.c[buf][idx] : cc;
-                    cc = fma(sm.a[buf][idx], cc, sm.b[buf][idx]);
-                    yo[idx] = y;
+                const double* A = sb.a[buf];
+                const double* B = sb.b[buf];
+                const double* Cb = sb.c[buf];
+                const int8_t* SW = sb.sw[buf];
+                for (int idx = 0; idx < cnt; idx += 8) {
+                    double va[8], vb[8], vc[8];
+                    int8_t vs8[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) { va[u] = A[idx + u]; vb[u] = B[idx + u]; vc[u] = Cb[idx + u]; vs8[u] = SW[idx + u]; }
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        if (idx + u < cnt) {
+                            const double y = vs8[u] ? vc[u] : cc;
+                            cc = fma(va[u], cc, vb[u]);
+                            st(yo + idx + u, y);
+                        }
+                    }
                 }
             }
         } else if (ch + 1 < nchF) {
@@ -243,9 +342,9 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
         }
         __syncthreads();
     }
-    if (tid == 0) ys[n - 1] = cc;
-    r1 = block_sum<NT>(r1, red);   // includes the __syncthreads that publishes ys
-    const double sc = (double)n * a.tnorm * fmax(kEps, a.unn[j]) / r1;
+    if (tid == 0) st(ys + n - 1, cc);
+    r1 = block_sum<NT>(r1, sm.red);   // includes the barriers that publish ys
+    const double sc = (double)n * a.tnorm * fmax(kEps, ldro(a.unn + j)) / r1;
 
     // ---- back substitution: rows n-1 .. 0
     const int64_t nchB = (n + CH - 1) / CH;
@@ -253,10 +352,10 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
         for (int idx = lt; idx < CH; idx += LT) {
             const int64_t i = n - 1 - ch * CH - idx;
             if (i >= 0) {
-                const int64_t o = i * ld;
-                sm.a[buf][idx] = sc * ys[i] * fr[o];
-                sm.b[buf][idx] = fb[o];
-                sm.c[buf][idx] = fc[o];
+                const int64_t o = i * ld_;
+                sb.a[buf][idx] = sc * ld(ys + i) * ldro(fr + o);
+                sb.b[buf][idx] = ldro(fb + o);
+                sb.c[buf][idx] = ldro(fc + o);
             }
         }
     };
@@ -270,13 +369,23 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
             if (lane == 0) {
                 const int cnt = (int)((n - ch * CH) < CH ? (n - ch * CH) : CH);
                 const int64_t ib = n - 1 - ch * CH;
-#pragma unroll 8
-                for (int idx = 0; idx < cnt; idx++) {
-                    const double t = fma(-sm.c[buf][idx], xp2, sm.a[buf][idx]);
-                    const double xi = fma(-sm.b[buf][idx], xp1, t);
-                    x[ib - idx] = xi;
-                    xp2 = xp1;
-                    xp1 = xi;
+                const double* A = sb.a[buf];
+                const double* B = sb.b[buf];
+                const double* Cb = sb.c[buf];
+                for (int idx = 0; idx < cnt; idx += 8) {
+                    double va[8], vb[8], vc[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) { va[u] = A[idx + u]; vb[u] = B[idx + u]; vc[u] = Cb[idx + u]; }
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        if (idx + u < cnt) {
+                            const double t = fma(-vc[u], xp2, va[u]);
+                            const double xi = fma(-vb[u], xp1, t);
+                            st(x + ib - idx - u, xi);
+                            xp2 = xp1;
+                            xp1 = xi;
+                        }
+                    }
                 }
             }
         } else if (ch + 1 < nchB) {
@@ -288,10 +397,16 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
 
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
-    __shared__ Shared sh;
-    __shared__ SolveSmem ssm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem sm;
+    {
+        const int64_t vdoubles = ((a.vcap + 2 > kSolveDoubles ? a.vcap + 2 : kSolveDoubles) + 1) & ~int64_t(1);
+        sm.vs = reinterpret_cast<double*>(smem_raw);
+        sm.cf = sm.vs + vdoubles;
+        sm.acc = reinterpret_cast<double2*>(sm.cf + CFCH);
+        sm.red = reinterpret_cast<double*>(sm.acc + NT);
+    }
     const int tid = threadIdx.x;
-    // locate group
     int g = 0;
     for (int t = 0; t < a.ngroups; t++)
         if ((int)blockIdx.x >= a.g_cta0[t]) g = t;
@@ -318,6 +433,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     const double thr = sqrt(0.1 / (double)n);
     double* __restrict__ Y = ws.Y;
     double* __restrict__ S = ws.S;
+    double* __restrict__ P_ = ws.P;
+    const int64_t mc = ws.mcap;
 
     for (int ci = a.g_coff[g]; ci < a.g_coff[g + 1]; ci++) {
         const int cl = a.g_clist[ci];
@@ -327,29 +444,29 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         double* __restrict__ Tc = ws.Tc;
         double* __restrict__ Tr = ws.Tr;
 
-        // ================= first reflector from the accepted z_{j1} (p = 0)
+        // ================= first reflector from the accepted z_{j1} (p = 0, PAPER.md:733-742)
         {
             const double* z = a.Z + j1 * a.ldz;
             int64_t i0, i1;
             part_uniform(0, n, r, G, i0, i1);
             double u2 = 0.0;
             for (int64_t i = i0 + tid; i < i1; i += NT) {
-                const double zi = z[i];
-                ws.u[i] = zi;
+                const double zi = ld(z + i);
+                st(ws.u + i, zi);
                 u2 = fma(zi, zi, u2);
             }
-            u2 = block_sum<NT>(u2, sh.red);
-            if (tid == 0) S[r * 8 + SSlots::U2] = u2;
+            u2 = block_sum<NT>(u2, sm.red);
+            if (tid == 0) st(S + r * 8 + SSlots::U2, u2);
             gsync();
             double un = 0.0;
-            for (int t = 0; t < G; t++) un += S[t * 8 + SSlots::U2];
+            for (int t = 0; t < G; t++) un += ld(S + t * 8 + SSlots::U2);
             un = sqrt(un);
-            const double u0 = ws.u[0];
+            const double u0 = ld(ws.u);
             const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
             const double tt = 1.0 / (c * c - u0 * c);
             for (int64_t i = i0 + tid; i < i1; i += NT)
-                Y[y_row_off(i, m) + 0] = (i == 0) ? (u0 - c) : ws.u[i];
-            if (r == 0 && tid == 0) { Tc[tcol_off(0)] = tt; Tr[0] = tt; }
+                st(Y + y_row_off(i, m), (i == 0) ? (u0 - c) : ld(ws.u + i));
+            if (r == 0 && tid == 0) { st(Tc + tcol_off(0), tt); st(Tr, tt); }
             gsync();
             PH(0);
         }
@@ -366,11 +483,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t i0, i1;
                     part_rows_weighted(n, p, r, G, i0, i1);
-                    colacc(Y, m, i0, i1, p, xcur, xs, ws.P + (int64_t)r * ws.mcap, sh);
-                    double x2 = 0.0;
-                    for (int64_t i = i0 + tid; i < i1; i += NT) { double xi = xcur[i * xs]; x2 = fma(xi, xi, x2); }
-                    x2 = block_sum<NT>(x2, sh.red);
-                    if (tid == 0) S[r * 8 + SSlots::X2] = x2;
+                    double x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)r * mc);
+                    x2 = block_sum<NT>(x2, sm.red);
+                    if (tid == 0) st(S + r * 8 + SSlots::X2, x2);
                 }
                 gsync();
                 PH(1);
@@ -380,8 +495,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     part_uniform(0, p, r, G, k0, k1);
                     for (int64_t k = k0 + tid; k < k1; k += NT) {
                         double s = 0.0;
-                        for (int t = 0; t < G; t++) s += ws.P[(int64_t)t * ws.mcap + k];
-                        ws.g[k] = s;
+                        for (int t = 0; t < G; t++) s += ld(P_ + (int64_t)t * mc + k);
+                        st(ws.g + k, s);
                     }
                 }
                 gsync();
@@ -390,10 +505,13 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t k0, k1;
                     part_tt(p, r, G, k0, k1);
-                    rowdots(k0, k1, p, ws.g,
-                            [&](int64_t k) { return Tc + tcol_off(k); },
-                            [&](int64_t k, int64_t& kb, int64_t& ke) { kb = 0; ke = k + 1; },
-                            [&](int64_t k, double v) { ws.gp[k] = v; });
+                    if (k1 > k0) {
+                        stage_vec(sm, ws.g, p);
+                        rowdots(k0, k1, p, sm.vs,
+                                [&](int64_t k) { return Tc + tcol_off(k); },
+                                [&](int64_t k) -> int64_t { return k + 1; },
+                                [&](int64_t k, double v) { st(ws.gp + k, v); });
+                    }
                 }
                 gsync();
                 PH(3);
@@ -402,26 +520,26 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     int64_t i0, i1;
                     part_uniform(p, n, r, G, i0, i1);
                     double u2 = 0.0;
-                    rowdots(i0, i1, p, ws.gp,
+                    stage_vec(sm, ws.gp, p);
+                    rowdots(i0, i1, p, sm.vs,
                             [&](int64_t i) { return Y + y_row_off(i, m); },
-                            [&](int64_t i, int64_t& kb, int64_t& ke) { kb = 0; ke = p; },
+                            [&](int64_t i) -> int64_t { return p; },
                             [&](int64_t i, double v) {
-                                const double ui = xcur[i * xs] - v;
-                                ws.u[i] = ui;
+                                const double ui = ld(xcur + i * xs) - v;
+                                st(ws.u + i, ui);
                                 u2 = fma(ui, ui, u2);
                             });
-                    __syncthreads();
-                    u2 = block_sum<NT>(u2, sh.red);
-                    if (tid == 0) S[r * 8 + SSlots::U2] = u2;
-                    colacc(Y, m, i0, i1, p, ws.u, 1, ws.P + (int64_t)r * ws.mcap, sh);
+                    u2 = block_sum<NT>(u2, sm.red);
+                    if (tid == 0) st(S + r * 8 + SSlots::U2, u2);
+                    colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)r * mc);
                 }
                 gsync();
                 PH(4);
                 // ---------------- R2: scalars (every CTA, identical), s = s' - c Y[p,:]
                 double un = 0.0, x2 = 0.0;
-                for (int t = 0; t < G; t++) { un += S[t * 8 + SSlots::U2]; x2 += S[t * 8 + SSlots::X2]; }
+                for (int t = 0; t < G; t++) { un += ld(S + t * 8 + SSlots::U2); x2 += ld(S + t * 8 + SSlots::X2); }
                 un = sqrt(un);
-                double u0 = ws.u[p];
+                double u0 = ld(ws.u + p);
                 const bool zero_u = (un == 0.0);   // reading: exactly-zero uhat -> e_1
                 if (zero_u) { u0 = 1.0; un = 1.0; }
                 // degenerate iterate (reading 16): restart with a fresh start vector
@@ -430,7 +548,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     its++;
                     kin = 1;
                     passes = 0;
-                    if (r == 0) chain_solve(a, ws, j, 1, restart, ssm, sh.red);
+                    if (r == 0) chain_solve(a, ws, j, 1, restart, sm);
                     gsync();
                     PH(9);
                     xcur = ws.x;
@@ -447,9 +565,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     part_uniform(0, p, r, G, k0, k1);
                     for (int64_t k = k0 + tid; k < k1; k += NT) {
                         double s = 0.0;
-                        if (zero_u) s = yrow[k];
-                        else for (int t = 0; t < G; t++) s += ws.P[(int64_t)t * ws.mcap + k];
-                        ws.s[k] = s - c * yrow[k];
+                        if (zero_u) s = ld(yrow + k);
+                        else for (int t = 0; t < G; t++) s += ld(P_ + (int64_t)t * mc + k);
+                        st(ws.s + k, s - c * ld(yrow + k));
                     }
                 }
                 gsync();
@@ -458,37 +576,54 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t l0, l1;
                     part_tn(p, r, G, l0, l1);
-                    const int tid_ = tid, lane = tid_ & 31, warp = tid_ >> 5;
-                    for (int64_t l = l0 + warp; l < l1; l += NW) {
-                        const double* row = Tr + l * m2;
-                        double a1 = 0.0, a2 = 0.0;
-                        for (int64_t k = (l & ~int64_t(1)) + 2 * lane; k < p; k += 64) {
-                            const double2 tv = *reinterpret_cast<const double2*>(row + k);
-                            const double2 sv = *reinterpret_cast<const double2*>(ws.s + k);
-                            const double2 yv = *reinterpret_cast<const double2*>(yrow + k);
-                            const bool vx = (k >= l), vy = (k + 1 < p);
-                            const double tx = vx ? tv.x : 0.0, ty = vy ? tv.y : 0.0;
-                            a1 = fma(tx, vx ? sv.x : 0.0, a1); a1 = fma(ty, vy ? sv.y : 0.0, a1);
-                            a2 = fma(tx, vx ? yv.x : 0.0, a2); a2 = fma(ty, vy ? yv.y : 0.0, a2);
-                        }
-                        a1 = warp_sum(a1);
-                        a2 = warp_sum(a2);
-                        if (lane == 0) {
-                            const double that = -tt * a1;
-                            ws.xp[l] = a2 + y0 * that;
-                            Tc[tcol_off(p) + l] = that;
-                            Tr[l * m2 + p] = that;
+                    if (l1 > l0) {
+                        stage_vec(sm, ws.s, p);
+                        const int lane = tid & 31, warp = tid >> 5;
+                        constexpr int U = 4;
+                        for (int64_t l = l0 + warp; l < l1; l += NW) {
+                            const double* row = Tr + l * m2;
+                            double a1 = 0.0, a2 = 0.0;
+                            for (int64_t k0 = (l & ~int64_t(1)) + 2 * lane; k0 < p; k0 += 64 * U) {
+                                double2 tv[U], yv[U];
+#pragma unroll
+                                for (int u = 0; u < U; u++) {
+                                    const int64_t k = k0 + 64 * u;
+                                    tv[u] = (k < p) ? ld2(row + k) : make_double2(0.0, 0.0);
+                                    yv[u] = (k < p) ? ld2(yrow + k) : make_double2(0.0, 0.0);
+                                }
+#pragma unroll
+                                for (int u = 0; u < U; u++) {
+                                    const int64_t k = k0 + 64 * u;
+                                    if (k < p) {
+                                        const double2 sv = *reinterpret_cast<const double2*>(sm.vs + k);
+                                        const bool vx = (k >= l), vy = (k + 1 < p);
+                                        const double tx = vx ? tv[u].x : 0.0, ty = vy ? tv[u].y : 0.0;
+                                        a1 = fma(tx, vx ? sv.x : 0.0, a1);
+                                        a1 = fma(ty, vy ? sv.y : 0.0, a1);
+                                        a2 = fma(tx, vx ? yv[u].x : 0.0, a2);
+                                        a2 = fma(ty, vy ? yv[u].y : 0.0, a2);
+                                    }
+                                }
+                            }
+                            a1 = warp_sum(a1);
+                            a2 = warp_sum(a2);
+                            if (lane == 0) {
+                                const double that = -tt * a1;
+                                st(ws.xp + l, a2 + y0 * that);
+                                st(Tc + tcol_off(p) + l, that);
+                                st(Tr + l * m2 + p, that);
+                            }
                         }
                     }
                     if (r == 0 && tid == 0) {
-                        ws.xp[p] = tt * y0;
-                        Tc[tcol_off(p) + p] = tt;
-                        Tr[p * m2 + p] = tt;
+                        st(ws.xp + p, tt * y0);
+                        st(Tc + tcol_off(p) + p, tt);
+                        st(Tr + p * m2 + p, tt);
                     }
                     int64_t i0, i1;
                     part_uniform(p, n, r, G, i0, i1);
                     for (int64_t i = i0 + tid; i < i1; i += NT)
-                        Y[y_row_off(i, m) + p] = (i == p) ? y0 : (zero_u ? 0.0 : ws.u[i]);
+                        st(Y + y_row_off(i, m) + p, (i == p) ? y0 : (zero_u ? 0.0 : ld(ws.u + i)));
                 }
                 gsync();
                 PH(6);
@@ -498,34 +633,34 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     part_rows_weighted(n, p + 1, r, G, i0, i1);
                     double q2 = 0.0, qinf = -1.0;
                     int64_t qarg = 0;
-                    rowdots(i0, i1, p + 1, ws.xp,
+                    stage_vec(sm, ws.xp, p + 1);
+                    rowdots(i0, i1, p + 1, sm.vs,
                             [&](int64_t i) { return Y + y_row_off(i, m); },
-                            [&](int64_t i, int64_t& kb, int64_t& ke) { kb = 0; ke = (i + 1 < p + 1) ? i + 1 : p + 1; },
+                            [&](int64_t i) -> int64_t { return (i + 1 < p + 1) ? i + 1 : p + 1; },
                             [&](int64_t i, double v) {
                                 const double qi = (i == p) ? v - 1.0 : v;
-                                ws.q[i] = qi;
+                                st(ws.q + i, qi);
                                 q2 = fma(qi, qi, q2);
                                 const double aq = fabs(qi);
                                 if (aq > qinf || (aq == qinf && i < qarg)) { qinf = aq; qarg = i; }
                             });
-                    __syncthreads();
-                    q2 = block_sum<NT>(q2, sh.red);
+                    q2 = block_sum<NT>(q2, sm.red);
                     // block argmax (lowest index on ties)
                     for (int o = 16; o > 0; o >>= 1) {
                         double oq = __shfl_xor_sync(0xffffffffu, qinf, o);
                         long long oa = __shfl_xor_sync(0xffffffffu, (long long)qarg, o);
                         if (oq > qinf || (oq == qinf && oa < qarg)) { qinf = oq; qarg = oa; }
                     }
-                    if ((tid & 31) == 0) { sh.acc[tid >> 5] = make_double2(qinf, (double)qarg); }
+                    if ((tid & 31) == 0) sm.acc[tid >> 5] = make_double2(qinf, (double)qarg);
                     __syncthreads();
                     if (tid == 0) {
                         for (int w = 1; w < NW; w++) {
-                            double2 t = sh.acc[w];
+                            double2 t = sm.acc[w];
                             if (t.x > qinf || (t.x == qinf && (int64_t)t.y < qarg)) { qinf = t.x; qarg = (int64_t)t.y; }
                         }
-                        S[r * 8 + SSlots::Q2] = q2;
-                        S[r * 8 + SSlots::QINF] = qinf;
-                        S[r * 8 + SSlots::QARG] = (double)qarg;
+                        st(S + r * 8 + SSlots::Q2, q2);
+                        st(S + r * 8 + SSlots::QINF, qinf);
+                        st(S + r * 8 + SSlots::QARG, (double)qarg);
                     }
                 }
                 gsync();
@@ -534,21 +669,21 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 double q2 = 0.0, qinf = -1.0;
                 int64_t qarg = 0;
                 for (int t = 0; t < G; t++) {
-                    q2 += S[t * 8 + SSlots::Q2];
-                    const double v = S[t * 8 + SSlots::QINF];
-                    const int64_t ia = (int64_t)S[t * 8 + SSlots::QARG];
+                    q2 += ld(S + t * 8 + SSlots::Q2);
+                    const double v = ld(S + t * 8 + SSlots::QINF);
+                    const int64_t ia = (int64_t)ld(S + t * 8 + SSlots::QARG);
                     if (v > qinf || (v == qinf && ia < qarg)) { qinf = v; qarg = ia; }
                 }
                 if (fabs(c) * qinf >= thr) passes++;
                 if (passes >= kPasses) done = true;
                 else if (kin >= kMaxIts) { done = true; flagged = true; }
                 if (done) {
-                    const double sgn = (ws.q[qarg] < 0.0) ? -1.0 : 1.0;
+                    const double sgn = (ld(ws.q + qarg) < 0.0) ? -1.0 : 1.0;
                     const double scl = sgn / sqrt(q2);
                     int64_t i0, i1;
                     part_uniform(0, n, r, G, i0, i1);
                     double* zj = a.Z + j * a.ldz;
-                    for (int64_t i = i0 + tid; i < i1; i += NT) zj[i] = ws.q[i] * scl;
+                    for (int64_t i = i0 + tid; i < i1; i += NT) zj[i] = ld(ws.q + i) * scl;
                     if (r == 0 && tid == 0) {
                         a.iters[j] = its;
                         if (flagged) atomicAdd(&a.out->nflag, 1);
@@ -558,7 +693,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     its++;
                     kin++;
                     PH(8);
-                    if (r == 0) chain_solve(a, ws, j, 0, 0, ssm, sh.red);
+                    if (r == 0) chain_solve(a, ws, j, 0, 0, sm);
                     gsync();
                     PH(9);
                     xcur = ws.x;
@@ -576,15 +711,23 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
 
 int cwy_threads() { return NT; }
 
-int cwy_max_ctas_per_sm() {
+size_t cwy_smem_bytes(int64_t vcap) {
+    int64_t vd = ((vcap + 2 > kSolveDoubles ? vcap + 2 : kSolveDoubles) + 1) & ~int64_t(1);
+    return sizeof(double) * (size_t)(vd + CFCH) + sizeof(double2) * NT + sizeof(double) * (NW + 8);
+}
+
+int cwy_max_ctas_per_sm(size_t smem) {
+    cudaFuncSetAttribute(cwy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cwy_kernel, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cwy_kernel, NT, smem);
     return nb;
 }
 
-cudaError_t launch_cwy(const CwyArgs& a, int nctas, cudaStream_t s) {
+cudaError_t launch_cwy(const CwyArgs& a, int nctas, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(cwy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     void* args[] = {(void*)&a};
-    return cudaLaunchCooperativeKernel((void*)cwy_kernel, dim3(nctas), dim3(NT), args, 0, s);
+    return cudaLaunchCooperativeKernel((void*)cwy_kernel, dim3(nctas), dim3(NT), args, smem, s);
 }
 
 }  // namespace tinv

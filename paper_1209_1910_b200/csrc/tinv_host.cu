@@ -401,7 +401,13 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     // ---------------- compact-WY kernel over this rank's clusters
     std::vector<int> rlo, rhi;
     rank_ranges(cs, nclus, n, h->nranks, rlo, rhi);
-    const int nctas_max = h->nsm * std::max(1, cwy_max_ctas_per_sm());
+    const int64_t vcap = ((int64_t)po.max_cluster + 1) / 2 * 2 + 2;   // >= every group's mcap
+    const size_t smem = cwy_smem_bytes(vcap);
+    if (po.n_clustered > 0 && smem > 232448) {
+        fprintf(stderr, "[tinv] cluster of %d vectors exceeds the shared-memory staging limit\n", po.max_cluster);
+        return TINV_ERR_DEVICE;
+    }
+    const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
     Schedule sc = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
     if (!sc.size.empty()) {
         const int ng = (int)sc.size.size();
@@ -468,7 +474,8 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.ngroups = ng; ca.g_cta0 = arrs[0]; ca.g_size = arrs[1]; ca.g_coff = arrs[2]; ca.g_clist = arrs[3];
         ca.ws = dws; ca.syncs = syncs; ca.prof = h->profiling ? prof : nullptr;
         ev_record(h, 5);
-        CK(launch_cwy(ca, sc.nctas, st));
+        ca.vcap = vcap;
+        CK(launch_cwy(ca, sc.nctas, smem, st));
         launches++;
         ev_record(h, 6);
         S.ngroups = ng;

@@ -112,14 +112,16 @@ struct CwyArgs {
     GroupWS* ws;             // per group
     long long* syncs;        // per group: barrier episodes (stats)
     unsigned long long* prof;  // optional per-group phase times [g*16 + phase] (ns), or NULL
+    int64_t vcap;            // largest vector staged in shared memory (max mcap over groups)
 };
 
 void launch_prep(const PrepArgs& a, cudaStream_t s);
 void launch_batched(const BatchedArgs& a, cudaStream_t s);
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 void launch_identity(double* Z, int64_t n, int64_t ldz, cudaStream_t s);
-cudaError_t launch_cwy(const CwyArgs& a, int nctas, cudaStream_t s);
+cudaError_t launch_cwy(const CwyArgs& a, int nctas, size_t smem, cudaStream_t s);
 int cwy_threads();
-int cwy_max_ctas_per_sm();
+size_t cwy_smem_bytes(int64_t vcap);
+int cwy_max_ctas_per_sm(size_t smem);
 
 }  // namespace tinv
