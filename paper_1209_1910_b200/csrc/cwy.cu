@@ -40,9 +40,16 @@ __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ double2 ld2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ void st(double* p, double v) { __stcg(p, v); }
 __device__ __forceinline__ double ldro(const double* p) { return __ldg(p); }
+// bulk L2 prefetch (TMA engine; no registers held): 16-byte aligned, size multiple of 16
+__device__ __forceinline__ void l2_prefetch(const double* p, int64_t ndoubles) {
+    if (ndoubles <= 0) return;
+    uint32_t bytes = (uint32_t)(((ndoubles * 8) + 15) & ~int64_t(15));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+constexpr int64_t kPfDist = 2048;   // doubles prefetched ahead inside a row (16 KB)
 
 struct SSlots {  // scalar partial slots per CTA (ws.S[r*8 + slot])
-    enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4 };
+    enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4, GPN = 5, X2N = 6 };
 };
 
 __device__ __forceinline__ int pow2ceil(int v) {
@@ -102,22 +109,19 @@ struct Smem {
 };
 
 struct SolveBuf {    // lives in Smem::vs during the chained solve
-    double* a[2];
-    double* b[2];
-    double* c[2];
-    int8_t* sw[2];
+    double2* ab[2];  // forward: (alpha, beta);  back: (s y r, b)
+    double2* mn[2];  // forward: (mu, nu);       back: (c, 0)
 };
 __device__ __forceinline__ SolveBuf solve_buf(const Smem& sm) {
     SolveBuf sb;
+    double2* base = reinterpret_cast<double2*>(sm.vs);
     for (int t = 0; t < 2; t++) {
-        sb.a[t] = sm.vs + (0 + t) * CH;
-        sb.b[t] = sm.vs + (2 + t) * CH;
-        sb.c[t] = sm.vs + (4 + t) * CH;
-        sb.sw[t] = reinterpret_cast<int8_t*>(sm.vs + 6 * CH) + t * CH;
+        sb.ab[t] = base + (0 + t) * CH;
+        sb.mn[t] = base + (2 + t) * CH;
     }
     return sb;
 }
-constexpr int64_t kSolveDoubles = 6 * CH + (2 * CH) / 8;
+constexpr int64_t kSolveDoubles = 8 * CH;
 
 // copy len doubles of a global vector into sm.vs (zero padded by 2), then barrier
 __device__ __forceinline__ void stage_vec(const Smem& sm, const double* src, int64_t len) {
@@ -166,11 +170,23 @@ __device__ __forceinline__ void rowdots(int64_t i0, int64_t i1, int64_t P, const
         return;
     }
     constexpr int U = 8;
+    if (lane == 0 && i0 + warp < i1) {   // prime: head of the warp's first row
+        const int64_t ke0 = rowlen(i0 + warp);
+        l2_prefetch(rowptr(i0 + warp), ke0 < kPfDist ? ke0 : kPfDist);
+    }
     for (int64_t i = i0 + warp; i < i1; i += NW) {
         const double* row = rowptr(i);
         const int64_t ke = rowlen(i);
+        if (lane == 0 && i + NW < i1) {   // head of the warp's next row
+            const int64_t kn = rowlen(i + NW);
+            l2_prefetch(rowptr(i + NW), kn < kPfDist ? kn : kPfDist);
+        }
         double acc = 0.0;
         for (int64_t k0 = 2 * lane; k0 < ke; k0 += 64 * U) {
+            if (lane == 0) {   // stay kPfDist doubles ahead inside the row
+                const int64_t kp = k0 + kPfDist;
+                if (kp < ke) l2_prefetch(row + kp, (ke - kp) < 64 * U ? (ke - kp) : 64 * U);
+            }
             double2 a[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
@@ -266,6 +282,75 @@ __device__ double colacc(const Smem& sm, const double* __restrict__ Y, int64_t m
     return c2;
 }
 
+
+// ---------------------------------------------------------------- deterministic reductions
+// sum over t < G of S[t*8 + slot] (fixed thread mapping + fixed tree)
+__device__ __forceinline__ double reduce_slot(const Smem& sm, const double* S, int G, int slot) {
+    double v = 0.0;
+    for (int t = threadIdx.x; t < G; t += NT) v += ld(S + t * 8 + slot);
+    return block_sum<NT>(v, sm.red);
+}
+// max over t < G of S[t*8 + QINF] with the lowest S[t*8 + QARG] on ties
+__device__ __forceinline__ void reduce_argmax(const Smem& sm, const double* S, int G, double& vmax, int64_t& arg) {
+    double v = -1.0;
+    int64_t ia = 0x7fffffffffffffffLL;
+    for (int t = threadIdx.x; t < G; t += NT) {
+        const double x = ld(S + t * 8 + 3);
+        const int64_t a = (int64_t)ld(S + t * 8 + 4);
+        if (x > v || (x == v && a < ia)) { v = x; ia = a; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const long long oa = __shfl_xor_sync(0xffffffffu, (long long)ia, o);
+        if (ov > v || (ov == v && oa < ia)) { v = ov; ia = oa; }
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sm.acc[threadIdx.x >> 5] = make_double2(v, (double)ia);
+    __syncthreads();
+    v = -1.0;
+    ia = 0x7fffffffffffffffLL;
+    for (int w = 0; w < NW; w++) {
+        const double2 t = sm.acc[w];
+        if (t.x > v || (t.x == v && (int64_t)t.y < ia)) { v = t.x; ia = (int64_t)t.y; }
+    }
+    __syncthreads();
+    vmax = v;
+    arg = ia;
+}
+// out[k] = sum_{t<G} P[t*mc + k] for k in [k0, k1): threads split (k, t-group); the
+// t-groups are combined in a fixed order (deterministic).
+template <class Post>
+__device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P, int64_t mc, int G, int64_t k0,
+                                                int64_t k1, Post post) {
+    const int tid = threadIdx.x;
+    for (int64_t kb = k0; kb < k1; kb += NT) {
+        const int64_t K = (k1 - kb < NT) ? (k1 - kb) : NT;
+        const int KP = (int)((K + 31) & ~int64_t(31));
+        const int TG = NT / KP;
+        const int kk = tid % KP, tg = tid / KP;
+        double acc = 0.0;
+        if (tg < TG && kk < K) {
+            const double* col = P + kb + kk;
+            int t = tg;
+            for (; t + 3 * TG < G; t += 4 * TG) {
+                const double v0 = ld(col + (int64_t)t * mc), v1 = ld(col + (int64_t)(t + TG) * mc);
+                const double v2 = ld(col + (int64_t)(t + 2 * TG) * mc), v3 = ld(col + (int64_t)(t + 3 * TG) * mc);
+                acc += v0; acc += v1; acc += v2; acc += v3;
+            }
+            for (; t < G; t += TG) acc += ld(col + (int64_t)t * mc);
+        }
+        if (TG > 1) {
+            __syncthreads();
+            sm.cf[tid] = acc;
+            __syncthreads();
+            if (tg == 0 && kk < K)
+                for (int u = 1; u < TG; u++) acc += sm.cf[kk + u * KP];
+            __syncthreads();
+        }
+        if (tg == 0 && kk < K) post(kb + kk, acc);
+    }
+}
+
 // ---------------------------------------------------------------- chained single-vector solve
 // x = (T - wt_j I)^{-1} (sigma * rhs), sigma = n ||T||_1 max(eps,|u_nn|) / ||rhs||_1,
 // with the factors stored by the batched kernel.  rhs = q (mode 0) or the start vector of
@@ -273,38 +358,50 @@ __device__ double colacc(const Smem& sm, const double* __restrict__ Y, int64_t m
 // of shared memory while warps 1..NW-1 stage the next chunk of factors (double buffer);
 // the dependent chain is one FMA per row (forward: c <- alpha c + beta with alpha, beta
 // precomputed from the pivot bit; back: x_i <- -b_i x_{i+1} + (s y_i r_i - c_i x_{i+2})).
-__device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int mode, int restart,
-                            const Smem& sm) {
+__device__ __forceinline__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int mode,
+                                            int restart, const Smem& sm) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t n = a.n, ld_ = a.ldv;
-    const double* __restrict__ fl = a.fl + j;
-    const int8_t* __restrict__ fp = a.fp + j;
-    const double* __restrict__ fr = a.fr + j;
-    const double* __restrict__ fb = a.fb + j;
-    const double* __restrict__ fc = a.fc + j;
-    double* __restrict__ ys = ws.ysol;
+    const int64_t n = a.n;
+    const double* __restrict__ F = a.F + j * n * 4;      // (l, 1/u0, u1/u0, u2/u0) per row
+    const int8_t* __restrict__ FP = a.FP + j * n;
+    double* __restrict__ ys = ws.ysol;   // n + CH slots
     const double* __restrict__ q = ws.q;
     const SolveBuf sb = solve_buf(sm);
     auto rhs = [&](int64_t i) -> double { return mode == 0 ? ld(q + i) : start_entry(a.seed, n, j, restart, i); };
     const int LT = NT - 32;
     const int lt = tid - 32;
+    constexpr int LU = (CH + (NT - 32) - 1) / (NT - 32);   // rows per loader thread
 
-    // ---- forward elimination: steps i = 0 .. n-2
+    // ---- forward elimination, steps i = 0 .. n-2 (rows >= n-1 are identity padding):
+    //      y_i = mu_i c + nu_i,  c <- alpha_i c + beta_i
     double r1 = 0.0;
     const int64_t nf = n - 1;
     const int64_t nchF = (nf + CH - 1) / CH;
     auto loadF = [&](int64_t ch, int buf) {
-        for (int idx = lt; idx < CH; idx += LT) {
+        double l[LU], bn[LU];
+        int8_t sw[LU];
+#pragma unroll
+        for (int u = 0; u < LU; u++) {                  // all loads first (independent)
+            const int idx = lt + u * LT;
             const int64_t i = ch * CH + idx;
-            if (i < nf) {
-                const double l = ldro(fl + i * ld_);
-                const int8_t sw = __ldg(fp + i * ld_);
-                const double bn = rhs(i + 1);
-                r1 += fabs(bn);
-                sb.a[buf][idx] = sw ? 1.0 : -l;
-                sb.b[buf][idx] = sw ? -l * bn : bn;
-                sb.c[buf][idx] = bn;
-                sb.sw[buf][idx] = sw;
+            const bool ok = idx < CH && i < nf;
+            l[u] = ok ? ldro(F + i * 4) : 0.0;
+            sw[u] = ok ? __ldg(FP + i) : (int8_t)0;
+            bn[u] = ok ? rhs(i + 1) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < LU; u++) {
+            const int idx = lt + u * LT;
+            const int64_t i = ch * CH + idx;
+            if (idx < CH) {
+                if (i < nf) {
+                    r1 += fabs(bn[u]);
+                    sb.ab[buf][idx] = sw[u] ? make_double2(1.0, -l[u] * bn[u]) : make_double2(-l[u], bn[u]);
+                    sb.mn[buf][idx] = sw[u] ? make_double2(0.0, bn[u]) : make_double2(1.0, 0.0);
+                } else {
+                    sb.ab[buf][idx] = make_double2(1.0, 0.0);
+                    sb.mn[buf][idx] = make_double2(0.0, 0.0);
+                }
             }
         }
     };
@@ -316,25 +413,23 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
         const int buf = (int)(ch & 1);
         if (warp == 0) {
             if (lane == 0) {
-                const int cnt = (int)((nf - ch * CH) < CH ? (nf - ch * CH) : CH);
                 double* yo = ys + ch * CH;
-                const double* A = sb.a[buf];
-                const double* B = sb.b[buf];
-                const double* Cb = sb.c[buf];
-                const int8_t* SW = sb.sw[buf];
+                const double2* AB = sb.ab[buf];
+                const double2* MN = sb.mn[buf];
+                const int cnt = (int)((nf - ch * CH) < CH ? ((nf - ch * CH + 7) & ~int64_t(7)) : CH);
                 for (int idx = 0; idx < cnt; idx += 8) {
-                    double va[8], vb[8], vc[8];
-                    int8_t vs8[8];
+                    double2 ab[8], mn[8];
 #pragma unroll
-                    for (int u = 0; u < 8; u++) { va[u] = A[idx + u]; vb[u] = B[idx + u]; vc[u] = Cb[idx + u]; vs8[u] = SW[idx + u]; }
+                    for (int u = 0; u < 8; u++) { ab[u] = AB[idx + u]; mn[u] = MN[idx + u]; }
+                    double y[8];
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
-                        if (idx + u < cnt) {
-                            const double y = vs8[u] ? vc[u] : cc;
-                            cc = fma(va[u], cc, vb[u]);
-                            st(yo + idx + u, y);
-                        }
+                        y[u] = fma(mn[u].x, cc, mn[u].y);
+                        cc = fma(ab[u].x, cc, ab[u].y);
                     }
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2)
+                        __stcg(reinterpret_cast<double2*>(yo + idx + u), make_double2(y[u], y[u + 1]));
                 }
             }
         } else if (ch + 1 < nchF) {
@@ -346,20 +441,34 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
     r1 = block_sum<NT>(r1, sm.red);   // includes the barriers that publish ys
     const double sc = (double)n * a.tnorm * fmax(kEps, ldro(a.unn + j)) / r1;
 
-    // ---- back substitution: rows n-1 .. 0
-    const int64_t nchB = (n + CH - 1) / CH;
+    // ---- back substitution from row nb-1 = roundup(n,8)-1 down to 0; rows >= n are
+    //      identity (x = 0):  x_i = -b_i x_{i+1} + (s y_i r_i - c_i x_{i+2})
+    const int64_t nb = (n + 7) & ~int64_t(7);
+    const int64_t nchB = (nb + CH - 1) / CH;
     auto loadB = [&](int64_t ch, int buf) {
-        for (int idx = lt; idx < CH; idx += LT) {
-            const int64_t i = n - 1 - ch * CH - idx;
-            if (i >= 0) {
-                const int64_t o = i * ld_;
-                sb.a[buf][idx] = sc * ld(ys + i) * ldro(fr + o);
-                sb.b[buf][idx] = ldro(fb + o);
-                sb.c[buf][idx] = ldro(fc + o);
+        double y[LU], rr[LU], bb[LU], cc_[LU];
+#pragma unroll
+        for (int u = 0; u < LU; u++) {
+            const int idx = lt + u * LT;
+            const int64_t i = nb - 1 - ch * CH - idx;
+            const bool ok = idx < CH && i >= 0 && i < n;
+            const int64_t o = ok ? i * 4 : 0;
+            y[u] = ok ? ld(ys + i) : 0.0;
+            rr[u] = ok ? ldro(F + o + 1) : 0.0;
+            const double2 bc = ok ? __ldg(reinterpret_cast<const double2*>(F + o + 2)) : make_double2(0.0, 0.0);
+            bb[u] = bc.x;
+            cc_[u] = bc.y;
+        }
+#pragma unroll
+        for (int u = 0; u < LU; u++) {
+            const int idx = lt + u * LT;
+            if (idx < CH) {
+                sb.ab[buf][idx] = make_double2(sc * y[u] * rr[u], bb[u]);
+                sb.mn[buf][idx] = make_double2(cc_[u], 0.0);
             }
         }
     };
-    double* __restrict__ x = ws.x;
+    double* __restrict__ x = ws.x;       // n + CH slots
     double xp1 = 0.0, xp2 = 0.0;
     if (warp > 0) loadB(0, 0);
     __syncthreads();
@@ -367,25 +476,26 @@ __device__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int 
         const int buf = (int)(ch & 1);
         if (warp == 0) {
             if (lane == 0) {
-                const int cnt = (int)((n - ch * CH) < CH ? (n - ch * CH) : CH);
-                const int64_t ib = n - 1 - ch * CH;
-                const double* A = sb.a[buf];
-                const double* B = sb.b[buf];
-                const double* Cb = sb.c[buf];
+                const int cnt = (int)((nb - ch * CH) < CH ? (nb - ch * CH) : CH);   // multiple of 8
+                const int64_t ib = nb - 1 - ch * CH;
+                const double2* AB = sb.ab[buf];
+                const double2* MN = sb.mn[buf];
                 for (int idx = 0; idx < cnt; idx += 8) {
-                    double va[8], vb[8], vc[8];
+                    double2 ab[8], mn[8];
 #pragma unroll
-                    for (int u = 0; u < 8; u++) { va[u] = A[idx + u]; vb[u] = B[idx + u]; vc[u] = Cb[idx + u]; }
+                    for (int u = 0; u < 8; u++) { ab[u] = AB[idx + u]; mn[u] = MN[idx + u]; }
+                    double xv[8];
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
-                        if (idx + u < cnt) {
-                            const double t = fma(-vc[u], xp2, va[u]);
-                            const double xi = fma(-vb[u], xp1, t);
-                            st(x + ib - idx - u, xi);
-                            xp2 = xp1;
-                            xp1 = xi;
-                        }
+                        const double t = fma(-mn[u].x, xp2, ab[u].x);
+                        xv[u] = fma(-ab[u].y, xp1, t);
+                        xp2 = xp1;
+                        xp1 = xv[u];
                     }
+                    // rows ib-idx-7 .. ib-idx: 16-byte aligned pairs (nb is a multiple of 8)
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2)
+                        __stcg(reinterpret_cast<double2*>(x + ib - idx - u - 1), make_double2(xv[u + 1], xv[u]));
                 }
             }
         } else if (ch + 1 < nchB) {
@@ -458,9 +568,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             u2 = block_sum<NT>(u2, sm.red);
             if (tid == 0) st(S + r * 8 + SSlots::U2, u2);
             gsync();
-            double un = 0.0;
-            for (int t = 0; t < G; t++) un += ld(S + t * 8 + SSlots::U2);
-            un = sqrt(un);
+            const double un = sqrt(reduce_slot(sm, S, G, SSlots::U2));
             const double u0 = ld(ws.u);
             const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
             const double tt = 1.0 / (c * c - u0 * c);
@@ -472,31 +580,42 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         }
 
         // ================= vectors j_c = 1 .. m-1
+        bool la_have = false;   // look-ahead of this vector's first pass A is ready
         for (int64_t p = 1; p < m; p++) {
             const int64_t j = j1 + p;
             const double* xcur = a.X1 + j;   // x^(1), interleaved
             int64_t xs = a.ldv;
             int its = 1, kin = 1, passes = 0, restart = 0;
             bool done = false, flagged = false;
+            bool use_la = la_have;           // first iteration: A already done in look-ahead
+            bool la_done = false;            // look-ahead for vector p+1 issued
+            la_have = false;
             while (!done) {
-                // ---------------- A: partial g = Y_p^T x, ||x||^2
-                {
-                    int64_t i0, i1;
-                    part_rows_weighted(n, p, r, G, i0, i1);
-                    double x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)r * mc);
-                    x2 = block_sum<NT>(x2, sm.red);
-                    if (tid == 0) st(S + r * 8 + SSlots::X2, x2);
+                if (!use_la) {
+                    // ---------------- A: partial g = Y_p^T x, ||x||^2
+                    {
+                        int64_t i0, i1;
+                        part_rows_weighted(n, p, r, G, i0, i1);
+                        double x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)r * mc);
+                        x2 = block_sum<NT>(x2, sm.red);
+                        if (tid == 0) st(S + r * 8 + SSlots::X2, x2);
+                    }
+                    gsync();
+                    PH(1);
                 }
-                gsync();
-                PH(1);
-                // ---------------- R1: g = sum_r partials
+                // ---------------- R1: g = sum_r partials (look-ahead: columns < p from the
+                // partials of Y_{p}^T x computed during the previous vector's solve, column p-1
+                // from the previous vector's last pass D)
                 {
                     int64_t k0, k1;
-                    part_uniform(0, p, r, G, k0, k1);
-                    for (int64_t k = k0 + tid; k < k1; k += NT) {
-                        double s = 0.0;
-                        for (int t = 0; t < G; t++) s += ld(P_ + (int64_t)t * mc + k);
-                        st(ws.g + k, s);
+                    if (use_la) {
+                        part_uniform(0, p - 1, r, G, k0, k1);
+                        reduce_partials(sm, ws.P2, mc, G, k0, k1, [&](int64_t k, double v) { st(ws.g + k, v); });
+                        const double gl = reduce_slot(sm, S, G, SSlots::GPN);
+                        if (r == 0 && tid == 0) st(ws.g + p - 1, gl);
+                    } else {
+                        part_uniform(0, p, r, G, k0, k1);
+                        reduce_partials(sm, P_, mc, G, k0, k1, [&](int64_t k, double v) { st(ws.g + k, v); });
                     }
                 }
                 gsync();
@@ -536,9 +655,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 gsync();
                 PH(4);
                 // ---------------- R2: scalars (every CTA, identical), s = s' - c Y[p,:]
-                double un = 0.0, x2 = 0.0;
-                for (int t = 0; t < G; t++) { un += ld(S + t * 8 + SSlots::U2); x2 += ld(S + t * 8 + SSlots::X2); }
-                un = sqrt(un);
+                double un = sqrt(reduce_slot(sm, S, G, SSlots::U2));
+                const double x2 = reduce_slot(sm, S, G, use_la ? SSlots::X2N : SSlots::X2);
+                use_la = false;
                 double u0 = ld(ws.u + p);
                 const bool zero_u = (un == 0.0);   // reading: exactly-zero uhat -> e_1
                 if (zero_u) { u0 = 1.0; un = 1.0; }
@@ -563,11 +682,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t k0, k1;
                     part_uniform(0, p, r, G, k0, k1);
-                    for (int64_t k = k0 + tid; k < k1; k += NT) {
-                        double s = 0.0;
-                        if (zero_u) s = ld(yrow + k);
-                        else for (int t = 0; t < G; t++) s += ld(P_ + (int64_t)t * mc + k);
-                        st(ws.s + k, s - c * ld(yrow + k));
+                    if (zero_u) {
+                        for (int64_t k = k0 + tid; k < k1; k += NT) st(ws.s + k, ld(yrow + k) - c * ld(yrow + k));
+                    } else {
+                        reduce_partials(sm, P_, mc, G, k0, k1,
+                                        [&](int64_t k, double v) { st(ws.s + k, v - c * ld(yrow + k)); });
                     }
                 }
                 gsync();
@@ -633,6 +752,15 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     part_rows_weighted(n, p + 1, r, G, i0, i1);
                     double q2 = 0.0, qinf = -1.0;
                     int64_t qarg = 0;
+                    // y_p^T x^(1)_{p+1}: the last column of the next vector's first pass A
+                    double gpn = 0.0;
+                    if (p + 1 < m) {
+                        const double* xn = a.X1 + j + 1;
+                        for (int64_t i = (i0 > p ? i0 : p) + tid; i < i1; i += NT)
+                            gpn = fma(ld(Y + y_row_off(i, m) + p), ld(xn + i * a.ldv), gpn);
+                    }
+                    gpn = block_sum<NT>(gpn, sm.red);
+                    if (tid == 0) st(S + r * 8 + SSlots::GPN, gpn);
                     stage_vec(sm, ws.xp, p + 1);
                     rowdots(i0, i1, p + 1, sm.vs,
                             [&](int64_t i) { return Y + y_row_off(i, m); },
@@ -666,14 +794,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 gsync();
                 PH(7);
                 // ---------------- TEST
-                double q2 = 0.0, qinf = -1.0;
-                int64_t qarg = 0;
-                for (int t = 0; t < G; t++) {
-                    q2 += ld(S + t * 8 + SSlots::Q2);
-                    const double v = ld(S + t * 8 + SSlots::QINF);
-                    const int64_t ia = (int64_t)ld(S + t * 8 + SSlots::QARG);
-                    if (v > qinf || (v == qinf && ia < qarg)) { qinf = v; qarg = ia; }
-                }
+                const double q2 = reduce_slot(sm, S, G, SSlots::Q2);
+                double qinf;
+                int64_t qarg;
+                reduce_argmax(sm, S, G, qinf, qarg);
                 if (fabs(c) * qinf >= thr) passes++;
                 if (passes >= kPasses) done = true;
                 else if (kin >= kMaxIts) { done = true; flagged = true; }
@@ -688,12 +812,33 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         a.iters[j] = its;
                         if (flagged) atomicAdd(&a.out->nflag, 1);
                     }
+                    la_have = la_done;
                     PH(8);
                 } else {
                     its++;
                     kin++;
                     PH(8);
-                    if (r == 0) chain_solve(a, ws, j, 0, 0, sm);
+                    const bool la = !la_done && p + 1 < m;
+                    if (r == 0) {
+                        if (la) {   // CTA 0 solves; its look-ahead partial is zero when G > 1
+                            if (G > 1) {
+                                for (int64_t k = tid; k < p; k += NT) st(ws.P2 + k, 0.0);
+                                if (tid == 0) st(S + SSlots::X2N, 0.0);
+                            }
+                        }
+                        chain_solve(a, ws, j, 0, 0, sm);
+                    }
+                    if (la && (r > 0 || G == 1)) {
+                        // look-ahead: Y_{p}^T x^(1)_{p+1} over the accepted columns 0..p-1,
+                        // overlapped with the chained solve (PAPER.md:534-535 for vector j+1)
+                        const int Gl = (G > 1) ? G - 1 : 1, rl = (G > 1) ? r - 1 : 0;
+                        int64_t i0, i1;
+                        part_rows_weighted(n, p, rl, Gl, i0, i1);
+                        double x2n = colacc(sm, Y, m, i0, i1, p, a.X1 + j + 1, a.ldv, ws.P2 + (int64_t)r * mc);
+                        x2n = block_sum<NT>(x2n, sm.red);
+                        if (tid == 0) st(S + r * 8 + SSlots::X2N, x2n);
+                    }
+                    if (la) la_done = true;
                     gsync();
                     PH(9);
                     xcur = ws.x;

@@ -67,8 +67,8 @@ struct tinv_s {
     void* base = nullptr;
     size_t base_bytes = 0;
     double *wt = nullptr, *X = nullptr, *fl = nullptr, *fr = nullptr, *fb = nullptr, *fc = nullptr;
-    double *unn = nullptr, *zscale = nullptr;
-    int8_t* fp = nullptr;
+    double *unn = nullptr, *zscale = nullptr, *F = nullptr;
+    int8_t *fp = nullptr, *FP = nullptr;
     int *cstart = nullptr, *cid = nullptr, *jc = nullptr, *iters = nullptr;
     PrepOut* out = nullptr;
     // cWY workspace (schedule-dependent)
@@ -136,6 +136,8 @@ int ensure_base(tinv_s* h, int64_t n) {
         h->fb = c.take<double>(nn);
         h->fc = c.take<double>(nn);
         h->fp = c.take<int8_t>(nn);
+        h->F = c.take<double>((size_t)n * (size_t)n * 4);
+        h->FP = c.take<int8_t>((size_t)n * (size_t)n);
         return c.off;
     };
     size_t bytes = layout(nullptr);
@@ -410,6 +412,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
     Schedule sc = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
     if (!sc.size.empty()) {
+        PackArgs pk{n, h->ldv, h->jc, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP};
+        launch_pack(pk, st);
+        launches++;
+        CK(cudaGetLastError());
         const int ng = (int)sc.size.size();
         // workspace: schedule arrays + per-group buffers
         unsigned long long* prof = nullptr;
@@ -432,15 +438,16 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.Y = c.take<double>(y_row_off(n, mc) + 2);
                 W.Tc = c.take<double>(tcol_off(mc) + 2);
                 W.Tr = c.take<double>(mc * m2 + 2);
-                W.x = c.take<double>(n + 2);
+                W.x = c.take<double>(n + 1024);
                 W.q = c.take<double>(n + 2);
                 W.u = c.take<double>(n + 2);
-                W.ysol = c.take<double>(n + 2);
+                W.ysol = c.take<double>(n + 1024);
                 W.g = c.take<double>(W.mcap);
                 W.gp = c.take<double>(W.mcap);
                 W.s = c.take<double>(W.mcap);
                 W.xp = c.take<double>(W.mcap);
                 W.P = c.take<double>((size_t)G * W.mcap);
+                W.P2 = c.take<double>((size_t)G * W.mcap);
                 W.S = c.take<double>((size_t)G * 8 + 8);
                 W.bar = c.take<GroupBarrier>(1);
             }
@@ -469,7 +476,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         CwyArgs ca{};
         ca.n = n; ca.ldv = h->ldv; ca.d = d; ca.e = e; ca.tnorm = tnorm; ca.seed = seed;
         ca.wt = h->wt; ca.cstart = h->cstart;
-        ca.fl = h->fl; ca.fp = h->fp; ca.fr = h->fr; ca.fb = h->fb; ca.fc = h->fc; ca.unn = h->unn;
+        ca.fl = h->fl; ca.fp = h->fp; ca.fr = h->fr; ca.fb = h->fb; ca.fc = h->fc; ca.unn = h->unn; ca.F = h->F; ca.FP = h->FP;
         ca.X1 = h->X; ca.Z = Z; ca.ldz = ldz; ca.iters = h->iters; ca.out = h->out;
         ca.ngroups = ng; ca.g_cta0 = arrs[0]; ca.g_size = arrs[1]; ca.g_coff = arrs[2]; ca.g_clist = arrs[3];
         ca.ws = dws; ca.syncs = syncs; ca.prof = h->profiling ? prof : nullptr;

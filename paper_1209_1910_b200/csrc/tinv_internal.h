@@ -54,6 +54,19 @@ struct BatchedArgs {
     PrepOut* out;
 };
 
+struct PackArgs {
+    int64_t n;
+    int64_t ldv;
+    const int* jc;
+    const double* fl;
+    const double* fr;
+    const double* fb;
+    const double* fc;
+    const int8_t* fp;
+    double* F;          // [j][i][4]: l, 1/u0, u1/u0, u2/u0
+    int8_t* FP;         // [j][i] pivot bits
+};
+
 struct FinalizeArgs {
     int64_t n;
     int64_t ldv;
@@ -77,6 +90,7 @@ struct GroupWS {
     double* s;          // Yhat^T yhat          (mcap)
     double* xp;         // T_{p+1} y_row        (mcap + 1)
     double* P;          // partial sums [G][mcap]
+    double* P2;         // look-ahead partial sums [G][mcap]
     double* S;          // scalar partials [G][8]
     double* ysol;       // forward-sweep workspace of the chained solve (n)
     GroupBarrier* bar;
@@ -98,6 +112,8 @@ struct CwyArgs {
     const double* fb;
     const double* fc;
     const double* unn;
+    const double* F;    // per-vector packed factors [j][i][4] (clustered vectors)
+    const int8_t* FP;   // per-vector pivot bits [j][i]
     const double* X1;   // x^(1) of every vector, [i][j]
     double* Z;
     int64_t ldz;
@@ -118,6 +134,7 @@ struct CwyArgs {
 void launch_prep(const PrepArgs& a, cudaStream_t s);
 void launch_batched(const BatchedArgs& a, cudaStream_t s);
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
+void launch_pack(const PackArgs& a, cudaStream_t s);
 void launch_identity(double* Z, int64_t n, int64_t ldz, cudaStream_t s);
 cudaError_t launch_cwy(const CwyArgs& a, int nctas, size_t smem, cudaStream_t s);
 int cwy_threads();
