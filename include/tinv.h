@@ -105,8 +105,12 @@ typedef struct {
     double  solve_bytes;        /* algorithmic bytes of the batched LU kernel         */
     double  kernel_ms[TINV_NKERNELS];     /* prep, batched_lu, finalize, cwy, misc, total */
     int64_t kernel_launches[TINV_NKERNELS];
-    double  cwy_phase_ms[10];   /* group 0 of the cWY kernel, wall time per phase: first
-                                   reflector, A, R1, TT, BC, R2, TN, D, test, chained solve */
+    double  cwy_phase_ms[16];   /* group 0 of the cWY kernel, wall time per phase: first
+                                   reflector, A, R1, TT, BC, R2, TN, D, test, chained solve
+                                   (forward sweep), chained solve (back sweep), wait for the
+                                   look-ahead pass overlapped with the back sweep; then the
+                                   narrow-cluster streams: ring wait, stage compute, stage
+                                   barrier; one spare */
 } tinv_stats_t;
 
 int tinv_set_profiling(tinv_t h, int enable);

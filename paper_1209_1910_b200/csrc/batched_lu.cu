@@ -22,7 +22,9 @@
 namespace tinv {
 
 constexpr int RB = 8;    // rows per stage
-constexpr int NS = 4;    // pipeline stages
+// pipeline stages: deep when the grid has at most one warp per SM (small n, latency-bound),
+// shallow when several warps share an SM
+constexpr int NS_DEEP = 20, NS_SHALLOW = 4;
 
 struct Stage {
     double v[4][RB][32];   // up to four double arrays
@@ -61,8 +63,10 @@ __device__ __forceinline__ void stage_rows(Stage& S, int na, const double* const
     }
 }
 
+template <int NS>
 __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
-    __shared__ __align__(16) Stage stages[NS];
+    extern __shared__ __align__(16) unsigned char bl_smem[];
+    Stage* stages = reinterpret_cast<Stage*>(bl_smem);
     const int lane = threadIdx.x;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
     const int64_t j = j0 + lane;
@@ -259,11 +263,12 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     a.iters[j] = its;
 }
 
-// Per-vector contiguous copy of the factors of clustered vectors (j_c >= 1) for the serial
-// chained solves of the compact-WY kernel: F[j][i] = (l_i, 1/u0_i, u1_i/u0_i, u2_i/u0_i) and
-// the pivot byte, via 32x32 shared-memory tiles (coalesced on both sides).
+// Per-vector contiguous copy of the factors of clustered vectors (j_c >= 1) for the chained
+// solves of the compact-WY kernel: F[j][i] = (l_i, 1/u0_i, u1_i/u0_i, u2_i/u0_i), the pivot
+// byte, and the first iterate x^(1) (contiguous per vector, so the compact-WY passes can
+// bulk-copy it), via 32x32 shared-memory tiles (coalesced on both sides).
 __global__ void pack_factors_kernel(PackArgs a) {
-    __shared__ double tile[4][32][33];
+    __shared__ double tile[5][32][33];
     __shared__ int8_t ptile[32][33];
     __shared__ int any;
     const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
@@ -273,11 +278,11 @@ __global__ void pack_factors_kernel(PackArgs a) {
     if (ty == 0 && j0 + tx < a.n && a.jc[j0 + tx] != 0) any = 1;
     __syncthreads();
     if (!any) return;
-    const double* src[4] = {a.fl, a.fr, a.fb, a.fc};
+    const double* src[5] = {a.fl, a.fr, a.fb, a.fc, a.X};
     for (int r = ty; r < 32; r += 8) {
         const int64_t i = i0 + r, j = j0 + tx;
         const bool ok = i < a.n && j < a.n;
-        for (int c = 0; c < 4; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + i * a.ldv + j) : 0.0;
+        for (int c = 0; c < 5; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + i * a.ldv + j) : 0.0;
         ptile[r][tx] = ok ? a.fp[i * a.ldv + j] : (int8_t)0;
     }
     __syncthreads();
@@ -291,6 +296,7 @@ __global__ void pack_factors_kernel(PackArgs a) {
             __stcg(reinterpret_cast<double2*>(dst), make_double2(tile[0][tx][r], tile[1][tx][r]));
             __stcg(reinterpret_cast<double2*>(dst + 2), make_double2(tile[2][tx][r], tile[3][tx][r]));
             a.FP[j * a.n + i] = ptile[tx][r];
+            __stcg(a.X1c + j * ((a.n + 1) & ~int64_t(1)) + i, tile[4][tx][r]);
         }
     }
 }
@@ -322,9 +328,15 @@ __global__ void identity_kernel(double* Z, int64_t n, int64_t ldz) {
         Z[j * ldz + i] = (i == j) ? 1.0 : 0.0;
 }
 
-void launch_batched(const BatchedArgs& a, cudaStream_t s) {
+void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm) {
     int64_t nb = (a.n + 31) / 32;
-    batched_lu_kernel<<<(unsigned)nb, 32, 0, s>>>(a);
+    if (nb <= nsm) {
+        const size_t sm = sizeof(Stage) * NS_DEEP;
+        cudaFuncSetAttribute(batched_lu_kernel<NS_DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        batched_lu_kernel<NS_DEEP><<<(unsigned)nb, 32, sm, s>>>(a);
+    } else {
+        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 32, sizeof(Stage) * NS_SHALLOW, s>>>(a);
+    }
 }
 
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s) {

@@ -100,8 +100,12 @@ __device__ __forceinline__ void group_sync(GroupBarrier* b, int G) {
 
 // ---------------------------------------------------------------- packed layouts
 // Y (row-major, zero-free "assignment model" of Fig. 1): row i of
-// Y_m holds columns 0..min(i, m-1), padded to an even count (16-byte rows).
+// Y_m holds columns 0..min(i, m-1), padded to an even count (16-byte rows).  Narrow clusters
+// (m <= kNarrowM) use a uniform row stride roundup(m, 2) instead (the padding of the leading
+// triangle is < m^2/2 doubles), so any row range is one contiguous span with a fixed stride.
+constexpr int kNarrowM = 64;
 __host__ __device__ __forceinline__ int64_t y_row_off(int64_t i, int64_t m) {
+    if (m <= kNarrowM) return i * ((m + 1) & ~int64_t(1));
     auto tri = [](int64_t r) -> int64_t {  // sum_{r'<r} roundup(r'+1, 2)
         int64_t a = r >> 1, b = r & 1;
         return 2 * a * (a + 1) + 2 * b * (a + 1);
@@ -114,6 +118,56 @@ __host__ __device__ __forceinline__ int64_t y_row_off(int64_t i, int64_t m) {
 __host__ __device__ __forceinline__ int64_t tcol_off(int64_t k) {
     int64_t a = k >> 1, b = k & 1;
     return 2 * a * (a + 1) + 2 * b * (a + 1);
+}
+
+}  // namespace tinv
+
+// ---------------------------------------------------------------- TMA bulk copies (sm_90+ / sm_100a)
+// Non-tensor bulk copies global -> shared completed on an mbarrier (transaction bytes).  A
+// non-cluster launch is a cluster of one CTA, so the CTA's own shared addresses are valid
+// shared::cluster addresses.
+namespace tinv {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// generic-proxy global writes (possibly by other CTAs, ordered by a barrier) -> later bulk reads
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// bytes: multiple of 16; src, dst 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 }  // namespace tinv

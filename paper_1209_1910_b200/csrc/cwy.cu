@@ -31,7 +31,9 @@ namespace tinv {
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int CFCH = 2048;   // rows whose coefficients are staged in shared memory at once
-constexpr int CH = 512;      // chained-solve chunk (rows)
+constexpr int CH = 256;                              // back-sweep ring chunk (rows)
+constexpr int kRing = 4;                             // back-sweep ring depth
+constexpr int64_t kSolveDoubles = kRing * 5 * CH;    // ring slots (4 CH factor doubles + CH t) in Smem::vs
 
 // Global accesses: data produced inside this kernel by other CTAs goes through L2 (.cg,
 // never a stale L1 line); explicit global-space intrinsics also let the compiler hoist
@@ -48,9 +50,10 @@ __device__ __forceinline__ void l2_prefetch(const double* p, int64_t ndoubles) {
 }
 constexpr int64_t kPfDist = 2048;   // doubles prefetched ahead inside a row (16 KB)
 
-struct SSlots {  // scalar partial slots per CTA (ws.S[r*8 + slot])
-    enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4, GPN = 5, X2N = 6 };
+struct SSlots {  // scalar partial slots per CTA (ws.S[r*SST + slot])
+    enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4, GPN = 5, X2N = 6, Q1 = 7, FA = 8, FB = 9 };
 };
+constexpr int SST = 16;   // scalar slots per CTA
 
 __device__ __forceinline__ int pow2ceil(int v) {
     int p = 1;
@@ -102,26 +105,12 @@ __device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int
 
 // dynamic shared memory carve-up
 struct Smem {
-    double* vs;      // staged vector (vcap + 2 doubles); aliased by the chained-solve buffers
+    double* vs;      // staged vector (vcap + 2 doubles)
     double* cf;      // CFCH coefficients
     double2* acc;    // NT
     double* red;     // NW + 8
+    uint64_t* mbar;  // kRing mbarriers (back-sweep ring)
 };
-
-struct SolveBuf {    // lives in Smem::vs during the chained solve
-    double2* ab[2];  // forward: (alpha, beta);  back: (s y r, b)
-    double2* mn[2];  // forward: (mu, nu);       back: (c, 0)
-};
-__device__ __forceinline__ SolveBuf solve_buf(const Smem& sm) {
-    SolveBuf sb;
-    double2* base = reinterpret_cast<double2*>(sm.vs);
-    for (int t = 0; t < 2; t++) {
-        sb.ab[t] = base + (0 + t) * CH;
-        sb.mn[t] = base + (2 + t) * CH;
-    }
-    return sb;
-}
-constexpr int64_t kSolveDoubles = 8 * CH;
 
 // copy len doubles of a global vector into sm.vs (zero padded by 2), then barrier
 __device__ __forceinline__ void stage_vec(const Smem& sm, const double* src, int64_t len) {
@@ -287,7 +276,7 @@ __device__ double colacc(const Smem& sm, const double* __restrict__ Y, int64_t m
 // sum over t < G of S[t*8 + slot] (fixed thread mapping + fixed tree)
 __device__ __forceinline__ double reduce_slot(const Smem& sm, const double* S, int G, int slot) {
     double v = 0.0;
-    for (int t = threadIdx.x; t < G; t += NT) v += ld(S + t * 8 + slot);
+    for (int t = threadIdx.x; t < G; t += NT) v += ld(S + t * SST + slot);
     return block_sum<NT>(v, sm.red);
 }
 // max over t < G of S[t*8 + QINF] with the lowest S[t*8 + QARG] on ties
@@ -295,8 +284,8 @@ __device__ __forceinline__ void reduce_argmax(const Smem& sm, const double* S, i
     double v = -1.0;
     int64_t ia = 0x7fffffffffffffffLL;
     for (int t = threadIdx.x; t < G; t += NT) {
-        const double x = ld(S + t * 8 + 3);
-        const int64_t a = (int64_t)ld(S + t * 8 + 4);
+        const double x = ld(S + t * SST + 3);
+        const int64_t a = (int64_t)ld(S + t * SST + 4);
         if (x > v || (x == v && a < ia)) { v = x; ia = a; }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -352,157 +341,372 @@ __device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P,
 }
 
 // ---------------------------------------------------------------- chained single-vector solve
-// x = (T - wt_j I)^{-1} (sigma * rhs), sigma = n ||T||_1 max(eps,|u_nn|) / ||rhs||_1,
-// with the factors stored by the batched kernel.  rhs = q (mode 0) or the start vector of
-// restart `restart` (mode 1).  The recurrences are serial: lane 0 of warp 0 runs them out
-// of shared memory while warps 1..NW-1 stage the next chunk of factors (double buffer);
-// the dependent chain is one FMA per row (forward: c <- alpha c + beta with alpha, beta
-// precomputed from the pivot bit; back: x_i <- -b_i x_{i+1} + (s y_i r_i - c_i x_{i+2})).
-__device__ __forceinline__ void chain_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int mode,
-                                            int restart, const Smem& sm) {
+// x = (T - wt_j I)^{-1} (sigma * rhs), sigma = n ||T||_1 max(eps,|u_nn|) / ||rhs||_1, with the
+// factors stored by the batched kernel (Eq. (1); rhs = q, Alg. 4 l.16
+// PAPER.md:708, or the start vector of restart `restart`).  Runs on one CTA:
+//   forward  c_{i+1} = sw ? c_i - l_i b_{i+1} : b_{i+1} - l_i c_i  is first order with
+//            |l_i| <= 1 (partial pivoting), so it is partitioned: one chunk of rows per
+//            thread reduces to c_out = A c_in + B, a block scan of these maps gives every
+//            chunk its exact incoming carry, and each chunk reruns its rows serially
+//            (y_i -> t_i = s y_i / u0_i);
+//   back     x_i = t_i - b_i x_{i+1} - c_i x_{i+2} stays strictly serial: its homogeneous
+//            solutions grow by up to 1/eps at the near-singular pivot (that growth is the
+//            inverse iteration), so any composition of row maps cancels catastrophically
+//            (measured: relative errors 1e-2 .. overflow on the glued-Wilkinson config with
+//            2-row blocks).  Lane 0 of warp 0 runs it out of shared memory (one dependent FMA
+//            per row) while warps 1..NW-1 stage the next chunk of (t_i, b_i, c_i).
+struct Aff1 {
+    double a, b;   // c -> a c + b
+};
+__device__ __forceinline__ Aff1 comp(const Aff1& f, const Aff1& g) {   // f o g
+    return Aff1{f.a * g.a, fma(f.a, g.b, f.b)};
+}
+__device__ __forceinline__ Aff1 shfl_up(const Aff1& f, int o) {
+    return Aff1{__shfl_up_sync(0xffffffffu, f.a, o), __shfl_up_sync(0xffffffffu, f.b, o)};
+}
+__device__ __forceinline__ Aff1 ident(Aff1) { return Aff1{1.0, 0.0}; }
+
+// Exclusive scan of per-thread maps in the order u = 0..NT-1 (later o earlier); returns the
+// thread's exclusive prefix, `total` = composition of all NT maps.  `buf` holds NW maps.
+template <class M>
+__device__ __forceinline__ M block_scan_excl(M f, M* buf, M& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    M inc = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const M g = shfl_up(inc, o);
+        if (lane >= o) inc = comp(inc, g);
+    }
+    M ex = shfl_up(inc, 1);
+    if (lane == 0) ex = ident(f);
+    __syncthreads();
+    if (lane == 31) buf[w] = inc;
+    __syncthreads();
+    M pre = ident(f);
+    for (int k = 0; k < w; k++) pre = comp(buf[k], pre);
+    total = pre;
+    for (int k = w; k < NW; k++) total = comp(buf[k], total);
+    __syncthreads();
+    return comp(ex, pre);
+}
+
+
+
+// Serial back substitution x_i = t_i - b_i x_{i+1} - c_i x_{i+2} (rows n-1 .. 0, x_n = x_{n+1}
+// = 0) by one thread.  Its inputs stream through a kRing-deep shared-memory ring filled by TMA
+// bulk copies: per chunk of CH rows the factor records F[i][0..3] (32 B/row) and t_i.  The
+// same thread issues the copies and consumes them (one mbarrier per slot), so the chain only
+// waits for data that was requested kRing chunks earlier.
+__device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const Smem& sm, uint32_t& mbph) {
+    const int64_t n = a.n;
+    const double* __restrict__ F = a.F + j * n * 4;
+    const double* __restrict__ ts = ws.ysol;
+    double* __restrict__ x = ws.x;
+    double* ring = sm.vs;                                    // kRing x (4 CH + CH) doubles
+    const int64_t C = (n + CH - 1) / CH;
+    fence_proxy_async_global();
+    auto issue = [&](int64_t k) {
+        const int slot = (int)(k % kRing);
+        const int64_t c = C - 1 - k;
+        const int64_t lo = c * CH, hi = (lo + CH < n) ? lo + CH : n;
+        const uint32_t fb = (uint32_t)((hi - lo) * 32), tb = (uint32_t)(((hi - lo + 1) & ~int64_t(1)) * 8);
+        double* dst = ring + (int64_t)slot * 5 * CH;
+        mbar_expect_tx(sm.mbar + slot, fb + tb);
+        bulk_g2s(dst, F + lo * 4, fb, sm.mbar + slot);
+        bulk_g2s(dst + 4 * CH, ts + lo, tb, sm.mbar + slot);
+    };
+    for (int64_t k = 0; k < C && k < kRing; k++) issue(k);
+    double x1 = 0.0, x2 = 0.0;
+    for (int64_t k = 0; k < C; k++) {
+        const int slot = (int)(k % kRing);
+        mbar_wait(sm.mbar + slot, (mbph >> slot) & 1u);
+        mbph ^= 1u << slot;
+        const double* Fs = ring + (int64_t)slot * 5 * CH;
+        const double* Ts = Fs + 4 * CH;
+        const int64_t c = C - 1 - k;
+        const int64_t lo = c * CH, hi = (lo + CH < n) ? lo + CH : n;
+        const int cnt = (int)(hi - lo);
+        // top remainder (only in the first chunk): scalar rows
+        int top = cnt & ~7;
+        for (int u = cnt - 1; u >= top; u--) {
+            const double2 bc = *reinterpret_cast<const double2*>(Fs + u * 4 + 2);
+            const double xi = fma(-bc.x, x1, fma(-bc.y, x2, Ts[u]));
+            __stcg(x + lo + u, xi);
+            x2 = x1;
+            x1 = xi;
+        }
+        // 8-row batches, loads of the next batch issued before the current chain (measured
+        // 13 cycles/row on B200 vs 20-30 for per-row forms; DFMA latency is 8)
+        if (top > 0) {
+            double b[8], c[8], t[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const double2 bc = *reinterpret_cast<const double2*>(Fs + (top - 8 + u) * 4 + 2);
+                b[u] = bc.x; c[u] = bc.y; t[u] = Ts[top - 8 + u];
+            }
+            for (int u0 = top - 8; u0 >= 0; u0 -= 8) {
+                double bn[8], cn[8], tn[8], xv[8];
+                const int nx = u0 >= 8 ? u0 - 8 : 0;
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const double2 bc = *reinterpret_cast<const double2*>(Fs + (nx + u) * 4 + 2);
+                    bn[u] = bc.x; cn[u] = bc.y; tn[u] = Ts[nx + u];
+                }
+#pragma unroll
+                for (int u = 7; u >= 0; u--) {
+                    xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u]));
+                    x2 = x1;
+                    x1 = xv[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u += 2)
+                    __stcg(reinterpret_cast<double2*>(x + lo + u0 + u), make_double2(xv[u], xv[u + 1]));
+#pragma unroll
+                for (int u = 0; u < 8; u++) { b[u] = bn[u]; c[u] = cn[u]; t[u] = tn[u]; }
+            }
+        }
+        if (k + kRing < C) issue(k + kRing);
+    }
+}
+
+// Composition of the forward maps of CTAs 0..cnt-1 (S slots FA, FB), applied in CTA order, by
+// warp 0 (lane-serial pieces + a warp scan); broadcast through `buf`.
+__device__ __forceinline__ Aff1 compose_ctas(const double* S, int cnt, Aff1* buf) {
+    if ((threadIdx.x >> 5) == 0) {
+        const int lane = threadIdx.x & 31;
+        const int per = (cnt + 31) / 32;
+        Aff1 f{1.0, 0.0};
+        for (int q = lane * per; q < cnt && q < (lane + 1) * per; q++)
+            f = comp(Aff1{ld(S + q * SST + SSlots::FA), ld(S + q * SST + SSlots::FB)}, f);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const Aff1 g = shfl_up(f, o);
+            if (lane >= o) f = comp(f, g);
+        }
+        if (lane == 31) buf[0] = f;
+    }
+    __syncthreads();
+    const Aff1 r = buf[0];
+    __syncthreads();
+    return r;
+}
+
+template <class Mark>
+__device__ void cta_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int mode, int restart, const Smem& sm,
+                          Mark mark, uint32_t& mbph) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t n = a.n;
     const double* __restrict__ F = a.F + j * n * 4;      // (l, 1/u0, u1/u0, u2/u0) per row
     const int8_t* __restrict__ FP = a.FP + j * n;
-    double* __restrict__ ys = ws.ysol;   // n + CH slots
     const double* __restrict__ q = ws.q;
-    const SolveBuf sb = solve_buf(sm);
+    double* __restrict__ ts = ws.ysol;
+    double* __restrict__ x = ws.x;
     auto rhs = [&](int64_t i) -> double { return mode == 0 ? ld(q + i) : start_entry(a.seed, n, j, restart, i); };
-    const int LT = NT - 32;
-    const int lt = tid - 32;
-    constexpr int LU = (CH + (NT - 32) - 1) / (NT - 32);   // rows per loader thread
-
-    // ---- forward elimination, steps i = 0 .. n-2 (rows >= n-1 are identity padding):
-    //      y_i = mu_i c + nu_i,  c <- alpha_i c + beta_i
-    double r1 = 0.0;
-    const int64_t nf = n - 1;
-    const int64_t nchF = (nf + CH - 1) / CH;
-    auto loadF = [&](int64_t ch, int buf) {
-        double l[LU], bn[LU];
-        int8_t sw[LU];
+    {   // bulk L2 prefetch of the factors (32 B per row) and pivot bytes, 64 KB pieces
+        const int64_t nbytes = n * 32;
+        for (int64_t o = (int64_t)tid * 65536; o < nbytes; o += (int64_t)NT * 65536)
+            l2_prefetch(F + o / 8, (nbytes - o < 65536 ? nbytes - o : 65536) / 8);
+        if (tid == NT - 1) {
+            const uintptr_t pa = reinterpret_cast<uintptr_t>(FP) & ~uintptr_t(15);
+            const int64_t nb16 = (int64_t)(reinterpret_cast<uintptr_t>(FP) + n - pa + 15) / 16 * 2;
+            l2_prefetch(reinterpret_cast<const double*>(pa), nb16 < 8192 ? nb16 : 8192);
+        }
+    }
+    // ---- forward, pass 1: chunk maps and ||rhs||_1 (loads batched FB rows at a time)
+    constexpr int FB = 8;
+    const int64_t L = (n + NT - 1) / NT;
+    const int64_t ta = min(n, (int64_t)tid * L), tb = min(n, (int64_t)(tid + 1) * L);
+    const int64_t tf = tb < n - 1 ? tb : n - 1;          // forward steps [ta, tf)
+    auto fetch = [&](int64_t i0, double* l, int* sw, double* bn, double* rr, bool want_r) {
 #pragma unroll
-        for (int u = 0; u < LU; u++) {                  // all loads first (independent)
-            const int idx = lt + u * LT;
-            const int64_t i = ch * CH + idx;
-            const bool ok = idx < CH && i < nf;
+        for (int u = 0; u < FB; u++) {
+            const int64_t i = i0 + u;
+            const bool ok = i < tf;
             l[u] = ok ? ldro(F + i * 4) : 0.0;
-            sw[u] = ok ? __ldg(FP + i) : (int8_t)0;
+            sw[u] = ok ? (int)FP[i] : 0;
             bn[u] = ok ? rhs(i + 1) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < LU; u++) {
-            const int idx = lt + u * LT;
-            const int64_t i = ch * CH + idx;
-            if (idx < CH) {
-                if (i < nf) {
-                    r1 += fabs(bn[u]);
-                    sb.ab[buf][idx] = sw[u] ? make_double2(1.0, -l[u] * bn[u]) : make_double2(-l[u], bn[u]);
-                    sb.mn[buf][idx] = sw[u] ? make_double2(0.0, bn[u]) : make_double2(1.0, 0.0);
-                } else {
-                    sb.ab[buf][idx] = make_double2(1.0, 0.0);
-                    sb.mn[buf][idx] = make_double2(0.0, 0.0);
-                }
-            }
+            if (want_r) rr[u] = ok ? ldro(F + i * 4 + 1) : 0.0;
         }
     };
-    double cc = 0.0;
-    if (tid == 0) { cc = rhs(0); r1 = fabs(cc); }
-    if (warp > 0 && nchF > 0) loadF(0, 0);
-    __syncthreads();
-    for (int64_t ch = 0; ch < nchF; ch++) {
-        const int buf = (int)(ch & 1);
-        if (warp == 0) {
-            if (lane == 0) {
-                double* yo = ys + ch * CH;
-                const double2* AB = sb.ab[buf];
-                const double2* MN = sb.mn[buf];
-                const int cnt = (int)((nf - ch * CH) < CH ? ((nf - ch * CH + 7) & ~int64_t(7)) : CH);
-                for (int idx = 0; idx < cnt; idx += 8) {
-                    double2 ab[8], mn[8];
+    double r1 = 0.0;
+    Aff1 f{1.0, 0.0};
+    if (ta < tb) r1 = fabs(rhs(ta));
+    for (int64_t i0 = ta; i0 < tf; i0 += FB) {
+        double l[FB], bn[FB], rr[FB];
+        int sw[FB];
+        fetch(i0, l, sw, bn, rr, false);
 #pragma unroll
-                    for (int u = 0; u < 8; u++) { ab[u] = AB[idx + u]; mn[u] = MN[idx + u]; }
-                    double y[8];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) {
-                        y[u] = fma(mn[u].x, cc, mn[u].y);
-                        cc = fma(ab[u].x, cc, ab[u].y);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; u += 2)
-                        __stcg(reinterpret_cast<double2*>(yo + idx + u), make_double2(y[u], y[u + 1]));
-                }
+        for (int u = 0; u < FB; u++) {
+            if (i0 + u < tf) {
+                if (i0 + u + 1 < tb) r1 += fabs(bn[u]);
+                if (sw[u]) f.b = fma(-l[u], bn[u], f.b);
+                else { f.a = -l[u] * f.a; f.b = fma(-l[u], f.b, bn[u]); }
             }
-        } else if (ch + 1 < nchF) {
-            loadF(ch + 1, buf ^ 1);
         }
-        __syncthreads();
     }
-    if (tid == 0) st(ys + n - 1, cc);
-    r1 = block_sum<NT>(r1, sm.red);   // includes the barriers that publish ys
+    Aff1 tot;
+    const Aff1 ex = block_scan_excl(f, reinterpret_cast<Aff1*>(sm.acc), tot);
+    r1 = block_sum<NT>(r1, sm.red);
     const double sc = (double)n * a.tnorm * fmax(kEps, ldro(a.unn + j)) / r1;
-
-    // ---- back substitution from row nb-1 = roundup(n,8)-1 down to 0; rows >= n are
-    //      identity (x = 0):  x_i = -b_i x_{i+1} + (s y_i r_i - c_i x_{i+2})
-    const int64_t nb = (n + 7) & ~int64_t(7);
-    const int64_t nchB = (nb + CH - 1) / CH;
-    auto loadB = [&](int64_t ch, int buf) {
-        double y[LU], rr[LU], bb[LU], cc_[LU];
+    // ---- forward, pass 2: y_i from the exact incoming carry; t_i = s y_i / u0_i
+    {
+        double c = fma(ex.a, rhs(0), ex.b);
+        for (int64_t i0 = ta; i0 < tf; i0 += FB) {
+            double l[FB], bn[FB], rr[FB];
+            int sw[FB];
+            fetch(i0, l, sw, bn, rr, true);
 #pragma unroll
-        for (int u = 0; u < LU; u++) {
-            const int idx = lt + u * LT;
-            const int64_t i = nb - 1 - ch * CH - idx;
-            const bool ok = idx < CH && i >= 0 && i < n;
-            const int64_t o = ok ? i * 4 : 0;
-            y[u] = ok ? ld(ys + i) : 0.0;
-            rr[u] = ok ? ldro(F + o + 1) : 0.0;
-            const double2 bc = ok ? __ldg(reinterpret_cast<const double2*>(F + o + 2)) : make_double2(0.0, 0.0);
-            bb[u] = bc.x;
-            cc_[u] = bc.y;
-        }
-#pragma unroll
-        for (int u = 0; u < LU; u++) {
-            const int idx = lt + u * LT;
-            if (idx < CH) {
-                sb.ab[buf][idx] = make_double2(sc * y[u] * rr[u], bb[u]);
-                sb.mn[buf][idx] = make_double2(cc_[u], 0.0);
-            }
-        }
-    };
-    double* __restrict__ x = ws.x;       // n + CH slots
-    double xp1 = 0.0, xp2 = 0.0;
-    if (warp > 0) loadB(0, 0);
-    __syncthreads();
-    for (int64_t ch = 0; ch < nchB; ch++) {
-        const int buf = (int)(ch & 1);
-        if (warp == 0) {
-            if (lane == 0) {
-                const int cnt = (int)((nb - ch * CH) < CH ? (nb - ch * CH) : CH);   // multiple of 8
-                const int64_t ib = nb - 1 - ch * CH;
-                const double2* AB = sb.ab[buf];
-                const double2* MN = sb.mn[buf];
-                for (int idx = 0; idx < cnt; idx += 8) {
-                    double2 ab[8], mn[8];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) { ab[u] = AB[idx + u]; mn[u] = MN[idx + u]; }
-                    double xv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) {
-                        const double t = fma(-mn[u].x, xp2, ab[u].x);
-                        xv[u] = fma(-ab[u].y, xp1, t);
-                        xp2 = xp1;
-                        xp1 = xv[u];
-                    }
-                    // rows ib-idx-7 .. ib-idx: 16-byte aligned pairs (nb is a multiple of 8)
-#pragma unroll
-                    for (int u = 0; u < 8; u += 2)
-                        __stcg(reinterpret_cast<double2*>(x + ib - idx - u - 1), make_double2(xv[u + 1], xv[u]));
+            for (int u = 0; u < FB; u++) {
+                if (i0 + u < tf) {
+                    double y;
+                    if (sw[u]) { y = bn[u]; c = fma(-l[u], bn[u], c); }
+                    else { y = c; c = fma(-l[u], c, bn[u]); }
+                    st(ts + i0 + u, sc * y * rr[u]);
                 }
             }
-        } else if (ch + 1 < nchB) {
-            loadB(ch + 1, buf ^ 1);
         }
-        __syncthreads();
+        if (tb == n && ta < tb) st(ts + n - 1, sc * c * ldro(F + (n - 1) * 4 + 1));
     }
+    __syncthreads();
+    mark(9);
+    if (tid == 0) {
+        st(ts + n, 0.0);
+        back_sweep(a, ws, j, sm, mbph);
+    }
+}
+
+// ---------------------------------------------------------------- TMA streaming, narrow clusters
+// Clusters with m <= kNarrowM store Y with a uniform row stride m2 = roundup(m, 2) (common.cuh),
+// so a CTA's rows [i0, i1) are one contiguous span.  Passes A, BC and D stream it through a
+// kNStg-deep shared-memory ring of TMA bulk copies (stage = RPS whole rows + the matching
+// coefficient rows x_i), one mbarrier per slot; thread 0 issues, all threads consume.
+constexpr int SBD = 4096;                    // Y doubles per stage (32 KB)
+constexpr int kMaxRPS = 512;                 // rows per stage cap (coefficient slots)
+constexpr int SXD = kMaxRPS + 4;             // coefficient doubles per stage
+constexpr int kStgD = SBD + SXD;             // doubles per ring slot
+constexpr int kNStg = 4;                     // ring depth
+
+struct Ring {
+    double* base;      // kNStg slots of kStgD doubles
+    uint64_t* mbar;    // kNStg mbarriers
+    uint32_t* ph;      // phase bits (per thread copy)
+    uint64_t* tacc;    // optional timers (wait, body, sync) of the timing thread, or nullptr
+};
+
+// Stream rows [i0, i1) of Y (and coef[i0, i1) if coef != nullptr) through the ring; for each
+// stage call body(ra, rb, Ys, Xs) with Ys = the stage's rows (row i at Ys + (i - ra) m2) and
+// Xs = coefficients (x_i at Xs[i - ra]).  All threads call; body may __syncthreads.
+template <class Body>
+__device__ void narrow_stream(const Ring& rg, const double* Y, int m2, int i0, int i1, const double* coef,
+                              Body body) {
+    if (i1 <= i0) return;
+    const int tid = threadIdx.x;
+    const int RPS = min(kMaxRPS, SBD / m2);
+    const int nst = (i1 - i0 + RPS - 1) / RPS;
+    int ps = 0;   // stages issued (thread 0)
+    auto issue = [&]() {
+        const int slot = ps % kNStg;
+        const int ra = i0 + ps * RPS, rb = min(i1, ra + RPS);
+        double* dst = rg.base + slot * kStgD;
+        const uint32_t yb = (uint32_t)((rb - ra) * m2 * 8);
+        const int xa = ra & ~1, xb = (rb + 1) & ~1;
+        const uint32_t xbytes = coef ? (uint32_t)((xb - xa) * 8) : 0u;
+        mbar_expect_tx(rg.mbar + slot, yb + xbytes);
+        bulk_g2s(dst, Y + (int64_t)ra * m2, yb, rg.mbar + slot);
+        if (coef) bulk_g2s(dst + SBD, coef + xa, xbytes, rg.mbar + slot);
+        ps++;
+    };
+    if (tid == 0) {
+        fence_proxy_async_global();
+        while (ps < nst && ps < kNStg) issue();
+    }
+    for (int s = 0; s < nst; s++) {
+        const int slot = s % kNStg;
+        const int ra = i0 + s * RPS, rb = min(i1, ra + RPS);
+        const uint64_t c0 = rg.tacc ? gtime() : 0;
+        mbar_wait(rg.mbar + slot, (*rg.ph >> slot) & 1u);
+        *rg.ph ^= 1u << slot;
+        const uint64_t c1 = rg.tacc ? gtime() : 0;
+        const double* Ys = rg.base + slot * kStgD;
+        double* Xs = const_cast<double*>(Ys) + SBD + (ra & 1);
+        body(ra, rb, Ys, Xs);       // (a body that writes the slot fences the async proxy itself)
+        const uint64_t c2 = rg.tacc ? gtime() : 0;
+        __syncthreads();            // slot free
+        if (tid == 0 && ps < nst) issue();
+        if (rg.tacc) {
+            rg.tacc[0] += c1 - c0;
+            rg.tacc[1] += c2 - c1;
+            rg.tacc[2] += gtime() - c2;
+        }
+    }
+}
+
+// Row dots over a stage, P <= kNarrowM: one thread per row (no shuffle reductions: the
+// rows are short), vector v staged in shared memory (broadcast reads); epi(i, dot).
+template <class Len, class Epi>
+__device__ __forceinline__ void narrow_rowdots(int ra, int rb, int m2, const double* Ys, const double* v, Len len,
+                                               Epi epi) {
+    for (int i = ra + (int)threadIdx.x; i < rb; i += NT) {
+        const double* row = Ys + (i - ra) * m2;
+        const int le = len(i);
+        double a0 = 0.0, a1 = 0.0;
+        int k = 0;
+        for (; k + 1 < le; k += 2) {
+            const double2 y = *reinterpret_cast<const double2*>(row + k);
+            const double2 w = *reinterpret_cast<const double2*>(v + k);
+            a0 = fma(y.x, w.x, a0);
+            a1 = fma(y.y, w.y, a1);
+        }
+        if (k < le) a0 = fma(row[k], v[k], a0);
+        epi(i, a0 + a1);
+    }
+}
+
+// Column accumulate over a stage: thread (cp, rs) adds Y[i][2cp..2cp+1] * c_i for the stage's
+// rows i with (i - ra) % RS == rs into (a0, a1); columns k < len(i) only.
+template <class Len>
+__device__ __forceinline__ void narrow_colacc(int ra, int rb, int m2, const double* Ys, const double* Xs, int CPT,
+                                              Len len, double& a0, double& a1) {
+    const int RS = NT / CPT, cp = threadIdx.x % CPT, rs = threadIdx.x / CPT;
+    const int k = 2 * cp;
+    constexpr int U = 4;
+    for (int ib = ra + rs; ib < rb; ib += RS * U) {
+        double2 av[U];
+        double cv[U];
+        int le[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = ib + u * RS;
+            le[u] = (i < rb) ? len(i) : 0;
+            av[u] = (k < le[u]) ? *reinterpret_cast<const double2*>(Ys + (i - ra) * m2 + k) : make_double2(0.0, 0.0);
+            cv[u] = (i < rb) ? Xs[i - ra] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (k < le[u]) a0 = fma(av[u].x, cv[u], a0);
+            if (k + 1 < le[u]) a1 = fma(av[u].y, cv[u], a1);
+        }
+    }
+}
+
+// Fixed-order reduction of the row-slice column accumulators; writes out[k] for k < P.
+__device__ __forceinline__ void narrow_colacc_finish(const Smem& sm, int CPT, int64_t P, double a0, double a1,
+                                                     double* out) {
+    const int tid = threadIdx.x, RS = NT / CPT, cp = tid % CPT, rs = tid / CPT;
+    __syncthreads();
+    sm.acc[tid] = make_double2(a0, a1);
+    __syncthreads();
+    if (rs == 0) {
+        for (int q = 1; q < RS; q++) {
+            const double2 t = sm.acc[cp + q * CPT];
+            a0 += t.x;
+            a1 += t.y;
+        }
+        const int64_t k = 2 * cp;
+        if (k < P) st(out + k, a0);
+        if (k + 1 < P) st(out + k + 1, a1);
+    }
+    __syncthreads();
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -515,7 +719,19 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         sm.cf = sm.vs + vdoubles;
         sm.acc = reinterpret_cast<double2*>(sm.cf + CFCH);
         sm.red = reinterpret_cast<double*>(sm.acc + NT);
+        sm.mbar = reinterpret_cast<uint64_t*>(sm.red + NW + 8);
     }
+    double* ring_base = reinterpret_cast<double*>(sm.mbar + kRing + kNStg);   // 16-B aligned (see cwy_smem_bytes)
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kRing + kNStg; k++) mbar_init(sm.mbar + k, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t mbph = 0;   // back-sweep ring phase bits (thread 0)
+    uint32_t rph = 0;    // pass ring phase bits (every thread)
+    const bool timing0 = (a.prof != nullptr) && threadIdx.x == 0 && (int)blockIdx.x == a.g_cta0[0];
+    uint64_t ntim[3] = {0, 0, 0};
+    const Ring rg{ring_base, sm.mbar + kRing, &rph, timing0 ? ntim : nullptr};
     const int tid = threadIdx.x;
     int g = 0;
     for (int t = 0; t < a.ngroups; t++)
@@ -528,8 +744,15 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     auto gsync = [&]() { group_sync(ws.bar, G); nsync++; };
     // optional phase timers (thread 0 of each group's first CTA; globaltimer ns)
     const bool timing = (a.prof != nullptr) && r == 0 && tid == 0;
-    uint64_t tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint64_t tacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     uint64_t tmark = timing ? gtime() : 0;
+    auto mark = [&](int k) {
+        if (timing) {
+            uint64_t _t = gtime();
+            tacc[k] += _t - tmark;
+            tmark = _t;
+        }
+    };
 #define PH(k)                                         \
     do {                                              \
         if (timing) {                                 \
@@ -540,6 +763,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     } while (0)
 
     const int64_t n = a.n;
+    const int64_t n2v = (n + 1) & ~int64_t(1);   // vector stride of X1c
     const double thr = sqrt(0.1 / (double)n);
     double* __restrict__ Y = ws.Y;
     double* __restrict__ S = ws.S;
@@ -551,6 +775,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         const int64_t j1 = a.cstart[cl];
         const int64_t m = a.cstart[cl + 1] - j1;
         const int64_t m2 = (m + 1) & ~int64_t(1);
+        const bool narrow = (m <= kNarrowM) && a.nstg > 0;
         double* __restrict__ Tc = ws.Tc;
         double* __restrict__ Tr = ws.Tr;
 
@@ -566,7 +791,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 u2 = fma(zi, zi, u2);
             }
             u2 = block_sum<NT>(u2, sm.red);
-            if (tid == 0) st(S + r * 8 + SSlots::U2, u2);
+            if (tid == 0) st(S + r * SST + SSlots::U2, u2);
             gsync();
             const double un = sqrt(reduce_slot(sm, S, G, SSlots::U2));
             const double u0 = ld(ws.u);
@@ -583,8 +808,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         bool la_have = false;   // look-ahead of this vector's first pass A is ready
         for (int64_t p = 1; p < m; p++) {
             const int64_t j = j1 + p;
-            const double* xcur = a.X1 + j;   // x^(1), interleaved
-            int64_t xs = a.ldv;
+            const double* xcur = a.X1c + j * n2v;   // x^(1), contiguous copy
+            int64_t xs = 1;
             int its = 1, kin = 1, passes = 0, restart = 0;
             bool done = false, flagged = false;
             bool use_la = la_have;           // first iteration: A already done in look-ahead
@@ -596,9 +821,20 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     {
                         int64_t i0, i1;
                         part_rows_weighted(n, p, r, G, i0, i1);
-                        double x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)r * mc);
+                        double x2 = 0.0;
+                        if (narrow) {
+                            const int CPT = pow2ceil((int)((p + 1) / 2));
+                            double a0 = 0.0, a1 = 0.0;
+                            narrow_stream(rg, Y, (int)m2, (int)i0, (int)i1, xcur, [&](int ra, int rb, const double* Ys, double* Xs) {
+                                for (int ii = tid; ii < rb - ra; ii += NT) x2 = fma(Xs[ii], Xs[ii], x2);
+                                narrow_colacc(ra, rb, (int)m2, Ys, Xs, CPT, [&](int i) -> int { return i + 1 < p ? i + 1 : (int)p; }, a0, a1);
+                            });
+                            narrow_colacc_finish(sm, CPT, p, a0, a1, P_ + (int64_t)r * mc);
+                        } else {
+                            x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)r * mc);
+                        }
                         x2 = block_sum<NT>(x2, sm.red);
-                        if (tid == 0) st(S + r * 8 + SSlots::X2, x2);
+                        if (tid == 0) st(S + r * SST + SSlots::X2, x2);
                     }
                     gsync();
                     PH(1);
@@ -639,18 +875,41 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     int64_t i0, i1;
                     part_uniform(p, n, r, G, i0, i1);
                     double u2 = 0.0;
-                    stage_vec(sm, ws.gp, p);
-                    rowdots(i0, i1, p, sm.vs,
-                            [&](int64_t i) { return Y + y_row_off(i, m); },
-                            [&](int64_t i) -> int64_t { return p; },
-                            [&](int64_t i, double v) {
-                                const double ui = ld(xcur + i * xs) - v;
+                    if (narrow) {
+                        // one read of Yhat per stage: row dots -> uhat (into the stage's
+                        // coefficient slots), then the column accumulate with uhat
+                        const int LPR = pow2ceil((int)((p + 1) / 2));
+                        stage_vec(sm, ws.gp, p);
+                        double a0 = 0.0, a1 = 0.0;
+                        auto lenp = [&](int) -> int { return (int)p; };
+                        narrow_stream(rg, Y, (int)m2, (int)i0, (int)i1, xcur, [&](int ra, int rb, const double* Ys, double* Xs) {
+                            narrow_rowdots(ra, rb, (int)m2, Ys, sm.vs, lenp, [&](int i, double v) {
+                                const double ui = Xs[i - ra] - v;
+                                Xs[i - ra] = ui;
                                 st(ws.u + i, ui);
                                 u2 = fma(ui, ui, u2);
                             });
-                    u2 = block_sum<NT>(u2, sm.red);
-                    if (tid == 0) st(S + r * 8 + SSlots::U2, u2);
-                    colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)r * mc);
+                            __syncthreads();
+                            narrow_colacc(ra, rb, (int)m2, Ys, Xs, LPR, lenp, a0, a1);
+                            fence_proxy_async_smem();   // uhat written into the slot before its next bulk fill
+                        });
+                        narrow_colacc_finish(sm, LPR, p, a0, a1, P_ + (int64_t)r * mc);
+                        u2 = block_sum<NT>(u2, sm.red);
+                        if (tid == 0) st(S + r * SST + SSlots::U2, u2);
+                    } else {
+                        stage_vec(sm, ws.gp, p);
+                        rowdots(i0, i1, p, sm.vs,
+                                [&](int64_t i) { return Y + y_row_off(i, m); },
+                                [&](int64_t i) -> int64_t { return p; },
+                                [&](int64_t i, double v) {
+                                    const double ui = ld(xcur + i * xs) - v;
+                                    st(ws.u + i, ui);
+                                    u2 = fma(ui, ui, u2);
+                                });
+                        u2 = block_sum<NT>(u2, sm.red);
+                        if (tid == 0) st(S + r * SST + SSlots::U2, u2);
+                        colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)r * mc);
+                    }
                 }
                 gsync();
                 PH(4);
@@ -667,9 +926,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     its++;
                     kin = 1;
                     passes = 0;
-                    if (r == 0) chain_solve(a, ws, j, 1, restart, sm);
+                    if (r == 0) cta_solve(a, ws, j, 1, restart, sm, mark, mbph);
                     gsync();
-                    PH(9);
+                    PH(10);
                     xcur = ws.x;
                     xs = 1;
                     continue;
@@ -747,32 +1006,48 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 gsync();
                 PH(6);
                 // ---------------- D: q = Y_{p+1} x' - e_p, norms and argmax
+                Aff1 fex{1.0, 0.0};   // forward-sweep state kept from D to the solve
+                int64_t fs0 = 0, fta = 0, ftb = 0;
+                bool flast = false;
                 {
                     int64_t i0, i1;
                     part_rows_weighted(n, p + 1, r, G, i0, i1);
-                    double q2 = 0.0, qinf = -1.0;
+                    double q2 = 0.0, q1 = 0.0, qinf = -1.0;
                     int64_t qarg = 0;
+                    if (tid == 0) {   // this CTA's factor rows (forward sweep below, back sweep)
+                        const int64_t fa = i0 > 0 ? i0 - 1 : 0;
+                        if (i1 > fa) l2_prefetch(a.F + (j * n + fa) * 4, (i1 - fa) * 4);
+                    }
                     // y_p^T x^(1)_{p+1}: the last column of the next vector's first pass A
                     double gpn = 0.0;
-                    if (p + 1 < m) {
-                        const double* xn = a.X1 + j + 1;
+                    if (p + 1 < m && G > 1) {
+                        const double* xn = a.X1c + (j + 1) * n2v;
                         for (int64_t i = (i0 > p ? i0 : p) + tid; i < i1; i += NT)
-                            gpn = fma(ld(Y + y_row_off(i, m) + p), ld(xn + i * a.ldv), gpn);
+                            gpn = fma(ld(Y + y_row_off(i, m) + p), ld(xn + i), gpn);
                     }
                     gpn = block_sum<NT>(gpn, sm.red);
-                    if (tid == 0) st(S + r * 8 + SSlots::GPN, gpn);
-                    stage_vec(sm, ws.xp, p + 1);
-                    rowdots(i0, i1, p + 1, sm.vs,
-                            [&](int64_t i) { return Y + y_row_off(i, m); },
-                            [&](int64_t i) -> int64_t { return (i + 1 < p + 1) ? i + 1 : p + 1; },
-                            [&](int64_t i, double v) {
-                                const double qi = (i == p) ? v - 1.0 : v;
-                                st(ws.q + i, qi);
-                                q2 = fma(qi, qi, q2);
-                                const double aq = fabs(qi);
-                                if (aq > qinf || (aq == qinf && i < qarg)) { qinf = aq; qarg = i; }
-                            });
+                    if (tid == 0) st(S + r * SST + SSlots::GPN, gpn);
+                    auto epiq = [&](int64_t i, double v) {
+                        const double qi = (i == p) ? v - 1.0 : v;
+                        st(ws.q + i, qi);
+                        q2 = fma(qi, qi, q2);
+                        const double aq = fabs(qi);
+                        q1 += aq;
+                        if (aq > qinf || (aq == qinf && i < qarg)) { qinf = aq; qarg = i; }
+                    };
+                    auto lend = [&](int64_t i) -> int64_t { return (i + 1 < p + 1) ? i + 1 : p + 1; };
+                    if (narrow) {
+                        stage_vec(sm, ws.xp, p + 1);
+                        auto lendn = [&](int i) -> int { return (i + 1 < p + 1) ? i + 1 : (int)p + 1; };
+                        narrow_stream(rg, Y, (int)m2, (int)i0, (int)i1, nullptr, [&](int ra, int rb, const double* Ys, double*) {
+                            narrow_rowdots(ra, rb, (int)m2, Ys, sm.vs, lendn, epiq);
+                        });
+                    } else {
+                        stage_vec(sm, ws.xp, p + 1);
+                        rowdots(i0, i1, p + 1, sm.vs, [&](int64_t i) { return Y + y_row_off(i, m); }, lend, epiq);
+                    }
                     q2 = block_sum<NT>(q2, sm.red);
+                    q1 = block_sum<NT>(q1, sm.red);
                     // block argmax (lowest index on ties)
                     for (int o = 16; o > 0; o >>= 1) {
                         double oq = __shfl_xor_sync(0xffffffffu, qinf, o);
@@ -786,9 +1061,48 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                             double2 t = sm.acc[w];
                             if (t.x > qinf || (t.x == qinf && (int64_t)t.y < qarg)) { qinf = t.x; qarg = (int64_t)t.y; }
                         }
-                        st(S + r * 8 + SSlots::Q2, q2);
-                        st(S + r * 8 + SSlots::QINF, qinf);
-                        st(S + r * 8 + SSlots::QARG, (double)qarg);
+                        st(S + r * SST + SSlots::Q2, q2);
+                        st(S + r * SST + SSlots::QINF, qinf);
+                        st(S + r * SST + SSlots::QARG, (double)qarg);
+                        st(S + r * SST + SSlots::Q1, q1);
+                    }
+                    // forward sweep of the chained solve with rhs q, pass 1: steps s in
+                    // [i0-1, i1-1) use q_{s+1} from this CTA's rows (reduced to one map per
+                    // thread and per CTA; needed only if the test below asks for another
+                    // iteration)
+                    __syncthreads();
+                    fs0 = i0 > 0 ? i0 - 1 : 0;
+                    const int64_t fs1 = (i1 - 1 < n - 1) ? i1 - 1 : n - 1;
+                    const int64_t FL = fs1 > fs0 ? (fs1 - fs0 + NT - 1) / NT : 0;
+                    fta = fs0 + min(fs1 > fs0 ? fs1 - fs0 : 0, (int64_t)tid * FL);
+                    ftb = fs0 + min(fs1 > fs0 ? fs1 - fs0 : 0, (int64_t)(tid + 1) * FL);
+                    flast = (ftb == n - 1) && (fta < ftb);
+                    const double* Fj = a.F + j * n * 4;
+                    const int8_t* FPj = a.FP + j * n;
+                    Aff1 f{1.0, 0.0};
+                    for (int64_t s0 = fta; s0 < ftb; s0 += 8) {
+                        double l[8], bn[8];
+                        int sw[8];
+#pragma unroll
+                        for (int u = 0; u < 8; u++) {
+                            const bool ok = s0 + u < ftb;
+                            l[u] = ok ? ldro(Fj + (s0 + u) * 4) : 0.0;
+                            sw[u] = ok ? (int)FPj[s0 + u] : 0;
+                            bn[u] = ok ? ld(ws.q + s0 + u + 1) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; u++) {
+                            if (s0 + u < ftb) {
+                                if (sw[u]) f.b = fma(-l[u], bn[u], f.b);
+                                else { f.a = -l[u] * f.a; f.b = fma(-l[u], f.b, bn[u]); }
+                            }
+                        }
+                    }
+                    Aff1 tot;
+                    fex = block_scan_excl(f, reinterpret_cast<Aff1*>(sm.acc), tot);
+                    if (tid == 0) {
+                        st(S + r * SST + SSlots::FA, tot.a);
+                        st(S + r * SST + SSlots::FB, tot.b);
                     }
                 }
                 gsync();
@@ -818,29 +1132,66 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     its++;
                     kin++;
                     PH(8);
-                    const bool la = !la_done && p + 1 < m;
+                    // look-ahead only when other CTAs can overlap it with the solve
+                    const bool la = !la_done && p + 1 < m && G > 1;
                     if (r == 0) {
                         if (la) {   // CTA 0 solves; its look-ahead partial is zero when G > 1
-                            if (G > 1) {
-                                for (int64_t k = tid; k < p; k += NT) st(ws.P2 + k, 0.0);
-                                if (tid == 0) st(S + SSlots::X2N, 0.0);
+                            for (int64_t k = tid; k < p; k += NT) st(ws.P2 + k, 0.0);
+                            if (tid == 0) st(S + SSlots::X2N, 0.0);
+                        }
+                    }
+                    {   // forward sweep, pass 2: exact carries from the CTA maps -> t_s = sc y_s / u0_s
+                        const double* Fj = a.F + j * n * 4;
+                        const int8_t* FPj = a.FP + j * n;
+                        const Aff1 pre = compose_ctas(S, r, reinterpret_cast<Aff1*>(sm.acc));
+                        const double q0 = ld(ws.q);
+                        double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
+                        const double q1 = reduce_slot(sm, S, G, SSlots::Q1);
+                        const double sc = (double)n * a.tnorm * fmax(kEps, ldro(a.unn + j)) / q1;
+                        double* ts = ws.ysol;
+                        for (int64_t s0 = fta; s0 < ftb; s0 += 8) {
+                            double l[8], bn[8], rr[8];
+                            int sw[8];
+#pragma unroll
+                            for (int u = 0; u < 8; u++) {
+                                const bool ok = s0 + u < ftb;
+                                l[u] = ok ? ldro(Fj + (s0 + u) * 4) : 0.0;
+                                rr[u] = ok ? ldro(Fj + (s0 + u) * 4 + 1) : 0.0;
+                                sw[u] = ok ? (int)FPj[s0 + u] : 0;
+                                bn[u] = ok ? ld(ws.q + s0 + u + 1) : 0.0;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; u++) {
+                                if (s0 + u < ftb) {
+                                    double y;
+                                    if (sw[u]) { y = bn[u]; cc = fma(-l[u], bn[u], cc); }
+                                    else { y = cc; cc = fma(-l[u], cc, bn[u]); }
+                                    st(ts + s0 + u, sc * y * rr[u]);
+                                }
                             }
                         }
-                        chain_solve(a, ws, j, 0, 0, sm);
+                        if (flast) {
+                            st(ts + n - 1, sc * cc * ldro(Fj + (n - 1) * 4 + 1));
+                            st(ts + n, 0.0);
+                        }
                     }
-                    if (la && (r > 0 || G == 1)) {
+                    gsync();
+                    PH(9);
+                    if (r == 0 && tid == 0) back_sweep(a, ws, j, sm, mbph);
+                    mark(10);
+                    if (la && r > 0) {
                         // look-ahead: Y_{p}^T x^(1)_{p+1} over the accepted columns 0..p-1,
                         // overlapped with the chained solve (PAPER.md:534-535 for vector j+1)
                         const int Gl = (G > 1) ? G - 1 : 1, rl = (G > 1) ? r - 1 : 0;
                         int64_t i0, i1;
                         part_rows_weighted(n, p, rl, Gl, i0, i1);
-                        double x2n = colacc(sm, Y, m, i0, i1, p, a.X1 + j + 1, a.ldv, ws.P2 + (int64_t)r * mc);
+                        double x2n = colacc(sm, Y, m, i0, i1, p, a.X1c + (j + 1) * n2v, 1, ws.P2 + (int64_t)r * mc);
                         x2n = block_sum<NT>(x2n, sm.red);
-                        if (tid == 0) st(S + r * 8 + SSlots::X2N, x2n);
+                        if (tid == 0) st(S + r * SST + SSlots::X2N, x2n);
                     }
                     if (la) la_done = true;
                     gsync();
-                    PH(9);
+                    PH(11);
                     xcur = ws.x;
                     xs = 1;
                 }
@@ -850,15 +1201,20 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     }
     if (r == 0 && tid == 0) a.syncs[g] = nsync;
     if (timing)
-        for (int k = 0; k < 10; k++) a.prof[g * 16 + k] = tacc[k];
+        for (int k = 0; k < 12; k++) a.prof[g * 16 + k] = tacc[k];
+    if (timing0)
+        for (int k = 0; k < 3; k++) a.prof[12 + k] = ntim[k];
 #undef PH
 }
 
 int cwy_threads() { return NT; }
+int cwy_narrow_max() { return kNarrowM; }
+int cwy_ring_stages() { return kNStg; }
 
-size_t cwy_smem_bytes(int64_t vcap) {
+size_t cwy_smem_bytes(int64_t vcap, int nstg) {
     int64_t vd = ((vcap + 2 > kSolveDoubles ? vcap + 2 : kSolveDoubles) + 1) & ~int64_t(1);
-    return sizeof(double) * (size_t)(vd + CFCH) + sizeof(double2) * NT + sizeof(double) * (NW + 8);
+    return sizeof(double) * (size_t)(vd + CFCH) + sizeof(double2) * NT + sizeof(double) * (NW + 8) +
+           sizeof(uint64_t) * (kRing + kNStg) + (nstg > 0 ? sizeof(double) * (size_t)kNStg * kStgD : 0);
 }
 
 int cwy_max_ctas_per_sm(size_t smem) {

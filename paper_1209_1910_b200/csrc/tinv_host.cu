@@ -67,7 +67,7 @@ struct tinv_s {
     void* base = nullptr;
     size_t base_bytes = 0;
     double *wt = nullptr, *X = nullptr, *fl = nullptr, *fr = nullptr, *fb = nullptr, *fc = nullptr;
-    double *unn = nullptr, *zscale = nullptr, *F = nullptr;
+    double *unn = nullptr, *zscale = nullptr, *F = nullptr, *X1c = nullptr;
     int8_t *fp = nullptr, *FP = nullptr;
     int *cstart = nullptr, *cid = nullptr, *jc = nullptr, *iters = nullptr;
     PrepOut* out = nullptr;
@@ -138,6 +138,7 @@ int ensure_base(tinv_s* h, int64_t n) {
         h->fp = c.take<int8_t>(nn);
         h->F = c.take<double>((size_t)n * (size_t)n * 4);
         h->FP = c.take<int8_t>((size_t)n * (size_t)n);
+        h->X1c = c.take<double>((size_t)n * (size_t)((n + 1) & ~int64_t(1)) + 1024);
         return c.off;
     };
     size_t bytes = layout(nullptr);
@@ -390,7 +391,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     ev_record(h, 2);
     BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, tnorm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
                    h->X, h->unn, h->zscale, h->iters, h->out};
-    launch_batched(ba, st);
+    launch_batched(ba, st, h->nsm);
     launches++;
     CK(cudaGetLastError());
     ev_record(h, 3);
@@ -404,7 +405,13 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     std::vector<int> rlo, rhi;
     rank_ranges(cs, nclus, n, h->nranks, rlo, rhi);
     const int64_t vcap = ((int64_t)po.max_cluster + 1) / 2 * 2 + 2;   // >= every group's mcap
-    const size_t smem = cwy_smem_bytes(vcap);
+    int nstg = 0;   // TMA ring for narrow clusters (2 <= m <= cwy_narrow_max()) of this rank
+    for (int c = rlo[h->rank]; c < rhi[h->rank] && !nstg; c++) {
+        const int m = cs[c + 1] - cs[c];
+        if (m >= 2 && m <= cwy_narrow_max()) nstg = cwy_ring_stages();
+    }
+    size_t smem = cwy_smem_bytes(vcap, nstg);
+    if (smem > 232448 && nstg) { nstg = 0; smem = cwy_smem_bytes(vcap, 0); }
     if (po.n_clustered > 0 && smem > 232448) {
         fprintf(stderr, "[tinv] cluster of %d vectors exceeds the shared-memory staging limit\n", po.max_cluster);
         return TINV_ERR_DEVICE;
@@ -412,7 +419,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
     Schedule sc = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
     if (!sc.size.empty()) {
-        PackArgs pk{n, h->ldv, h->jc, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP};
+        PackArgs pk{n, h->ldv, h->jc, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP, h->X, h->X1c};
         launch_pack(pk, st);
         launches++;
         CK(cudaGetLastError());
@@ -448,7 +455,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.xp = c.take<double>(W.mcap);
                 W.P = c.take<double>((size_t)G * W.mcap);
                 W.P2 = c.take<double>((size_t)G * W.mcap);
-                W.S = c.take<double>((size_t)G * 8 + 8);
+                W.S = c.take<double>((size_t)G * 16 + 16);
                 W.bar = c.take<GroupBarrier>(1);
             }
             return c.off;
@@ -477,11 +484,12 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.n = n; ca.ldv = h->ldv; ca.d = d; ca.e = e; ca.tnorm = tnorm; ca.seed = seed;
         ca.wt = h->wt; ca.cstart = h->cstart;
         ca.fl = h->fl; ca.fp = h->fp; ca.fr = h->fr; ca.fb = h->fb; ca.fc = h->fc; ca.unn = h->unn; ca.F = h->F; ca.FP = h->FP;
-        ca.X1 = h->X; ca.Z = Z; ca.ldz = ldz; ca.iters = h->iters; ca.out = h->out;
+        ca.X1c = h->X1c; ca.Z = Z; ca.ldz = ldz; ca.iters = h->iters; ca.out = h->out;
         ca.ngroups = ng; ca.g_cta0 = arrs[0]; ca.g_size = arrs[1]; ca.g_coff = arrs[2]; ca.g_clist = arrs[3];
         ca.ws = dws; ca.syncs = syncs; ca.prof = h->profiling ? prof : nullptr;
         ev_record(h, 5);
         ca.vcap = vcap;
+        ca.nstg = nstg;
         CK(launch_cwy(ca, sc.nctas, smem, st));
         launches++;
         ev_record(h, 6);
@@ -495,7 +503,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         CK(cudaMemcpyAsync(hs.data(), syncs, sizeof(long long) * ng, cudaMemcpyDeviceToHost, st));
         if (h->profiling) CK(cudaMemcpyAsync(hp.data(), prof, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        for (int k = 0; k < 10; k++) S.cwy_phase_ms[k] = (double)hp[k] * 1e-6;
+        for (int k = 0; k < 16; k++) S.cwy_phase_ms[k] = (double)hp[k] * 1e-6;
         for (auto v : hs) S.group_syncs = std::max<int64_t>(S.group_syncs, v);
     }
     S.solve_bytes = 144.0 * (double)n * (double)n;  // factor 32n + 2 x 56n per vector

@@ -65,6 +65,8 @@ struct PackArgs {
     const int8_t* fp;
     double* F;          // [j][i][4]: l, 1/u0, u1/u0, u2/u0
     int8_t* FP;         // [j][i] pivot bits
+    const double* X;    // x^(1), [i][j]
+    double* X1c;        // x^(1) of clustered vectors, [j][i], vector stride roundup(n, 2)
 };
 
 struct FinalizeArgs {
@@ -90,8 +92,8 @@ struct GroupWS {
     double* s;          // Yhat^T yhat          (mcap)
     double* xp;         // T_{p+1} y_row        (mcap + 1)
     double* P;          // partial sums [G][mcap]
-    double* P2;         // look-ahead partial sums [G][mcap]
     double* S;          // scalar partials [G][8]
+    double* P2;         // look-ahead partial sums [G][mcap]
     double* ysol;       // forward-sweep workspace of the chained solve (n)
     GroupBarrier* bar;
     int64_t mcap;
@@ -114,7 +116,7 @@ struct CwyArgs {
     const double* unn;
     const double* F;    // per-vector packed factors [j][i][4] (clustered vectors)
     const int8_t* FP;   // per-vector pivot bits [j][i]
-    const double* X1;   // x^(1) of every vector, [i][j]
+    const double* X1c;  // x^(1) of clustered vectors, [j][i], vector stride roundup(n, 2)
     double* Z;
     int64_t ldz;
     int* iters;
@@ -129,16 +131,19 @@ struct CwyArgs {
     long long* syncs;        // per group: barrier episodes (stats)
     unsigned long long* prof;  // optional per-group phase times [g*16 + phase] (ns), or NULL
     int64_t vcap;            // largest vector staged in shared memory (max mcap over groups)
+    int nstg;                // TMA ring stages for narrow clusters (0 = ring not allocated)
 };
 
 void launch_prep(const PrepArgs& a, cudaStream_t s);
-void launch_batched(const BatchedArgs& a, cudaStream_t s);
+void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm);
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 void launch_pack(const PackArgs& a, cudaStream_t s);
 void launch_identity(double* Z, int64_t n, int64_t ldz, cudaStream_t s);
 cudaError_t launch_cwy(const CwyArgs& a, int nctas, size_t smem, cudaStream_t s);
 int cwy_threads();
-size_t cwy_smem_bytes(int64_t vcap);
+size_t cwy_smem_bytes(int64_t vcap, int nstg);
+int cwy_narrow_max();
+int cwy_ring_stages();
 int cwy_max_ctas_per_sm(size_t smem);
 
 }  // namespace tinv

@@ -18,7 +18,7 @@ EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version")
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
-PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve")
+PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "nw_wait", "nw_body", "nw_sync", "spare")
 
 
 class TinvConfig(C.Structure):
@@ -32,7 +32,7 @@ class TinvStats(C.Structure):
                 ("launches", C.c_int64), ("group_syncs", C.c_int64), ("ngroups", C.c_int64),
                 ("cwy_ctas", C.c_int64), ("reorth_bytes", C.c_double), ("solve_bytes", C.c_double),
                 ("kernel_ms", C.c_double * 6), ("kernel_launches", C.c_int64 * 6),
-                ("cwy_phase_ms", C.c_double * 10)]
+                ("cwy_phase_ms", C.c_double * 16)]
 
     def as_dict(self):
         return {
