@@ -21,67 +21,64 @@
 
 namespace tinv {
 
-constexpr int RB = 8;    // rows per stage
+constexpr int RB = 16;   // rows per stage
 // pipeline stages: deep when the grid has at most one warp per SM (small n, latency-bound),
 // shallow when several warps share an SM
-constexpr int NS_DEEP = 20, NS_SHALLOW = 4;
+constexpr int NS_DEEP = 8, NS_SHALLOW = 2;
 
 struct Stage {
-    double v[4][RB][32];   // up to four double arrays
+    double v[4][RB][32];   // up to four double arrays, rows of the warp's 32 vectors
     int8_t pv[RB][32];     // pivot bits
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// Stage RB rows (row(rr) for rr < RB, skipped when outside [0, n)) of `na` double arrays
-// (and optionally the pivot bytes) for the warp's 32 vectors starting at column j0.
-__device__ __forceinline__ void stage_rows(Stage& S, int na, const double* const* arr, const int8_t* piv,
-                                           int64_t ld, int64_t j0, int64_t n, int64_t base, int dir, int lane) {
-    // each 256-byte row segment is 16 chunks of 16 B: lanes 0..15 take even rows, 16..31 odd
-    const int half = lane >> 4, ch = lane & 15;
-    for (int a = 0; a < na; a++) {
-#pragma unroll
-        for (int rr = half; rr < RB; rr += 2) {
-            const int64_t i = base + dir * rr;
-            if (i >= 0 && i < n) cp_async16(&S.v[a][rr][ch * 2], arr[a] + i * ld + j0 + ch * 2);
-        }
+// One lane issues TMA bulk copies of rows [lo, hi) of `na` arrays (block-row layout: the
+// warp's rows are contiguous, 256 B each) into stage S, completing on `bar`.
+__device__ __forceinline__ void stage_bulk(Stage& S, uint64_t* bar, int na, const double* const* base, int64_t lo,
+                                           int64_t hi, int64_t dst_row0, const int8_t* pbase) {
+    if (hi <= lo) {   // nothing to copy: complete the phase with a plain arrive
+        mbar_expect_tx(bar, 0);
+        return;
     }
-    if (piv) {   // 32 bytes per row: lanes 0..1 of each half
-        if (ch < 2) {
-#pragma unroll
-            for (int rr = half; rr < RB; rr += 2) {
-                const int64_t i = base + dir * rr;
-                if (i >= 0 && i < n) cp_async16(&S.pv[rr][ch * 16], piv + i * ld + j0 + ch * 16);
-            }
-        }
-    }
+    const uint32_t rows = (uint32_t)(hi - lo);
+    mbar_expect_tx(bar, rows * 256u * (uint32_t)na + (pbase ? rows * 32u : 0u));
+    for (int a = 0; a < na; a++) bulk_g2s(&S.v[a][dst_row0][0], base[a] + lo * 32, rows * 256u, bar);
+    if (pbase) bulk_g2s(&S.pv[dst_row0][0], pbase + lo * 32, rows * 32u, bar);
 }
 
 template <int NS>
 __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
-    extern __shared__ __align__(16) unsigned char bl_smem[];
+    extern __shared__ __align__(128) unsigned char bl_smem[];
     Stage* stages = reinterpret_cast<Stage*>(bl_smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bl_smem + sizeof(Stage) * NS);
     const int lane = threadIdx.x;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
     const int64_t j = j0 + lane;
     const int64_t n = a.n;
     const bool live = j < n;
     const int64_t jj = live ? j : n - 1;          // dead lanes shadow a live vector (no stores)
-    const int64_t ld = a.ldv;
     const double shift = a.wt[jj];
     const int p = a.jc[jj];
-    double tiny = kEps * a.tnorm;
+    const double tnorm = __ldcg(&a.out->tnorm);   // written by the prep kernel (same stream)
+    if (a.out->bad) return;                       // invalid input: nothing is computed
+    double tiny = kEps * tnorm;
     if (tiny == 0.0) tiny = 2.2250738585072014e-308;
     const double thr = sqrt(0.1 / (double)n);
-    double* __restrict__ X = a.X;
+    // this warp's block of rows (block-row layout, common.cuh bix)
+    const int64_t boff = (int64_t)blockIdx.x * n * 32;
+    double* __restrict__ X = a.X + boff;
+    double* __restrict__ FL = a.fl + boff;
+    double* __restrict__ FR = a.fr + boff;
+    double* __restrict__ FB = a.fb + boff;
+    double* __restrict__ FC = a.fc + boff;
+    int8_t* __restrict__ FPv = a.fp + boff;
     const double* __restrict__ dd = a.d;
     const double* __restrict__ ee = a.e;
+    if (lane == 0) {
+        for (int s = 0; s < NS; s++) mbar_init(bars + s, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t ph = 0;
 
     // ---------------- iteration 1: factor + forward elimination of the random start
     double pv_last;
@@ -122,56 +119,52 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
                 c = bn - l * c;
                 sw = 0;
             }
-            if (live) {
-                const int64_t o = i * ld + j;
-                __stcg(a.fl + o, l);
-                a.fp[o] = sw;
-                __stcg(a.fr + o, r);
-                __stcg(a.fb + o, u1 * r);
-                __stcg(a.fc + o, u2 * r);
-                __stcg(X + o, y);
-            }
+            const int64_t o = i * 32 + lane;
+            __stcg(FL + o, l);
+            FPv[o] = sw;
+            __stcg(FR + o, r);
+            __stcg(FB + o, u1 * r);
+            __stcg(FC + o, u2 * r);
+            __stcg(X + o, y);
         }
         pv_last = pivot_floor(pp, tiny);
-        if (live) {
-            const int64_t o = (n - 1) * ld + j;
-            __stcg(a.fr + o, 1.0 / pv_last);
-            __stcg(a.fb + o, 0.0);
-            __stcg(a.fc + o, 0.0);
-            __stcg(X + o, c);
-        }
+        const int64_t o = (n - 1) * 32 + lane;
+        __stcg(FR + o, 1.0 / pv_last);
+        __stcg(FB + o, 0.0);
+        __stcg(FC + o, 0.0);
+        __stcg(X + o, c);
     }
     const double unn = fabs(pv_last);
     if (live) a.unn[j] = unn;
-    const double sfac = (double)n * a.tnorm * fmax(kEps, unn);
+    const double sfac = (double)n * tnorm * fmax(kEps, unn);
+    // generic writes above -> bulk (async proxy) reads below
+    fence_proxy_async_global();
     __syncwarp();
-    __threadfence_block();
 
-    // back substitution, in place: x_i = s y_i r_i - b_i x_{i+1} - c_i x_{i+2}
+    // back substitution, in place: x_i = s y_i r_i - b_i x_{i+1} - c_i x_{i+2}; stage b holds
+    // rows [n - (b+1) RB, n - b RB) (clipped at 0), consumed top-down
     const int64_t nblk = (n + RB - 1) / RB;
     auto back = [&](double sc, bool keep, double& xinf, double& x1, double& x2, int64_t& imax) {
-        const double* arr[4] = {X, a.fr, a.fb, a.fc};
+        const double* arr[4] = {X, FR, FB, FC};
         double xp1 = 0.0, xp2 = 0.0;
         xinf = -1.0; x1 = 0.0; x2 = 0.0; imax = 0;
-#pragma unroll
-        for (int s = 0; s < NS - 1; s++) {
-            if (s < nblk) stage_rows(stages[s], 4, arr, nullptr, ld, j0, n, n - 1 - (int64_t)s * RB, -1, lane);
-            cp_async_commit();
-        }
+        auto issue = [&](int64_t b) {
+            const int64_t hi = n - b * RB, lo = hi - RB > 0 ? hi - RB : 0;
+            stage_bulk(stages[b % NS], bars + (b % NS), 4, arr, lo, hi, RB - (hi - lo), nullptr);
+        };
+        if (lane == 0)
+            for (int64_t b = 0; b < NS && b < nblk; b++) issue(b);
         for (int64_t b = 0; b < nblk; b++) {
-            const int64_t bn = b + NS - 1;
-            if (bn < nblk) stage_rows(stages[bn % NS], 4, arr, nullptr, ld, j0, n, n - 1 - bn * RB, -1, lane);
-            cp_async_commit();
-            cp_async_wait<NS - 1>();
-            __syncwarp();
+            mbar_wait(bars + (b % NS), (ph >> (b % NS)) & 1u);
+            ph ^= 1u << (b % NS);
             const Stage& S = stages[b % NS];
 #pragma unroll
-            for (int rr = 0; rr < RB; rr++) {
-                const int64_t i = n - 1 - b * RB - rr;
+            for (int rr = RB - 1; rr >= 0; rr--) {
+                const int64_t i = n - b * RB - (RB - rr);
                 if (i >= 0) {
                     const double t = fma(-S.v[3][rr][lane], xp2, sc * S.v[0][rr][lane] * S.v[1][rr][lane]);
                     const double xi = fma(-S.v[2][rr][lane], xp1, t);
-                    if (keep) __stcg(X + i * ld + j, xi);
+                    if (keep) __stcg(X + i * 32 + lane, xi);
                     xp2 = xp1;
                     xp1 = xi;
                     const double ax = fabs(xi);
@@ -181,35 +174,32 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
                 }
             }
             __syncwarp();
+            if (lane == 0 && b + NS < nblk) issue(b + NS);
         }
-        cp_async_wait<0>();
+        fence_proxy_async_global();
         __syncwarp();
     };
-    // forward elimination of the current iterate (rhs = x, in place): y_i, carried c
+    // forward elimination of the current iterate (rhs = x, in place): y_i, carried c; stage b
+    // holds steps i in [b RB, b RB + RB): l_i, pivot bits, and x_{i+1} (in slot 1)
     auto forward = [&](bool keep) {
-        const double* arrL[1] = {a.fl};
-        double c = __ldcg(X + jj);
+        double c = __ldcg(X + lane);
         const int64_t nf = n - 1;
         const int64_t nb = (nf + RB - 1) / RB;
-        const int half = lane >> 4, chk = lane & 15;
-        auto issue = [&](int64_t blk) {
-            Stage& S = stages[blk % NS];
-            stage_rows(S, 1, arrL, a.fp, ld, j0, nf, blk * RB, 1, lane);
-            for (int rr = half; rr < RB; rr += 2) {          // rhs rows i+1 -> slot 1
-                const int64_t i = blk * RB + rr + 1;
-                if (i < n) cp_async16(&S.v[1][rr][chk * 2], X + i * ld + j0 + chk * 2);
-            }
+        auto issue = [&](int64_t b) {
+            const int64_t lo = b * RB, hi = lo + RB < nf ? lo + RB : nf;
+            Stage& S = stages[b % NS];
+            uint64_t* bar = bars + (b % NS);
+            const uint32_t rows = (uint32_t)(hi - lo);
+            mbar_expect_tx(bar, rows * (256u * 2u + 32u));
+            bulk_g2s(&S.v[0][0][0], FL + lo * 32, rows * 256u, bar);
+            bulk_g2s(&S.pv[0][0], FPv + lo * 32, rows * 32u, bar);
+            bulk_g2s(&S.v[1][0][0], X + (lo + 1) * 32, rows * 256u, bar);
         };
-#pragma unroll
-        for (int s = 0; s < NS - 1; s++) {
-            if (s < nb) issue(s);
-            cp_async_commit();
-        }
+        if (lane == 0)
+            for (int64_t b = 0; b < NS && b < nb; b++) issue(b);
         for (int64_t b = 0; b < nb; b++) {
-            if (b + NS - 1 < nb) issue(b + NS - 1);
-            cp_async_commit();
-            cp_async_wait<NS - 1>();
-            __syncwarp();
+            mbar_wait(bars + (b % NS), (ph >> (b % NS)) & 1u);
+            ph ^= 1u << (b % NS);
             const Stage& S = stages[b % NS];
 #pragma unroll
             for (int rr = 0; rr < RB; rr++) {
@@ -220,20 +210,20 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
                     const bool sw = S.pv[rr][lane] != 0;
                     const double y = sw ? bn : c;
                     c = fma(sw ? 1.0 : -l, c, sw ? -l * bn : bn);
-                    if (keep) __stcg(X + i * ld + j, y);
+                    if (keep) __stcg(X + i * 32 + lane, y);
                 }
             }
             __syncwarp();
+            if (lane == 0 && b + NS < nb) issue(b + NS);
         }
-        cp_async_wait<0>();
-        if (keep) __stcg(X + (n - 1) * ld + j, c);
+        if (keep) __stcg(X + (n - 1) * 32 + lane, c);
+        fence_proxy_async_global();
         __syncwarp();
-        __threadfence_block();
     };
 
     double xinf, x1, x2;
     int64_t imax;
-    back(sfac / b1, live, xinf, x1, x2, imax);
+    back(sfac / b1, true, xinf, x1, x2, imax);
     int its = 1;
     // Vectors with j_c >= 1 hand x^(1) to the compact-WY kernel.  The warp keeps sweeping
     // while any lane still iterates; lanes that are done run the sweeps without storing.
@@ -257,7 +247,7 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     if (p == 0) {
         if (passes < kPasses) atomicAdd(&a.out->nflag, 1);
         // Alg. 4 l.20 normalise; sign rule (reading 15)
-        const double xm = __ldcg(X + imax * ld + j);
+        const double xm = __ldcg(X + imax * 32 + lane);
         a.zscale[j] = (xm < 0.0 ? -1.0 : 1.0) / sqrt(x2);
     }
     a.iters[j] = its;
@@ -282,8 +272,8 @@ __global__ void pack_factors_kernel(PackArgs a) {
     for (int r = ty; r < 32; r += 8) {
         const int64_t i = i0 + r, j = j0 + tx;
         const bool ok = i < a.n && j < a.n;
-        for (int c = 0; c < 5; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + i * a.ldv + j) : 0.0;
-        ptile[r][tx] = ok ? a.fp[i * a.ldv + j] : (int8_t)0;
+        for (int c = 0; c < 5; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + bix(i, j, a.n)) : 0.0;
+        ptile[r][tx] = ok ? a.fp[bix(i, j, a.n)] : (int8_t)0;
     }
     __syncthreads();
     // write: vector j0+r, rows i0..i0+31 -> 32 x 4 doubles contiguous (1 KB)
@@ -309,11 +299,12 @@ void launch_pack(const PackArgs& a, cudaStream_t s) {
 // Tiled transpose + scale of finished iterates into column-major Z (j_c == 0 vectors).
 __global__ void finalize_kernel(FinalizeArgs a) {
     __shared__ double tile[32][33];
+    if (a.out->bad || a.out->tnorm == 0.0) return;   // invalid input / Z = I (host handles)
     const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
     for (int r = ty; r < 32; r += 8) {
         int64_t i = i0 + r, j = j0 + tx;
-        tile[r][tx] = (i < a.n && j < a.n) ? a.X[i * a.ldv + j] : 0.0;
+        tile[r][tx] = (i < a.n && j < a.n) ? a.X[bix(i, j, a.n)] : 0.0;
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
@@ -331,11 +322,13 @@ __global__ void identity_kernel(double* Z, int64_t n, int64_t ldz) {
 void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm) {
     int64_t nb = (a.n + 31) / 32;
     if (nb <= nsm) {
-        const size_t sm = sizeof(Stage) * NS_DEEP;
+        const size_t sm = (sizeof(Stage) + 8) * NS_DEEP;
         cudaFuncSetAttribute(batched_lu_kernel<NS_DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         batched_lu_kernel<NS_DEEP><<<(unsigned)nb, 32, sm, s>>>(a);
     } else {
-        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 32, sizeof(Stage) * NS_SHALLOW, s>>>(a);
+        const size_t sm = (sizeof(Stage) + 8) * NS_SHALLOW;
+        cudaFuncSetAttribute(batched_lu_kernel<NS_SHALLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 32, sm, s>>>(a);
     }
 }
 

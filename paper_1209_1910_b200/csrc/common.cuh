@@ -98,6 +98,14 @@ __device__ __forceinline__ void group_sync(GroupBarrier* b, int G) {
     __syncthreads();
 }
 
+// ---------------------------------------------------------------- batched (per-vector) arrays
+// Factors and iterates of the batched solve: blocks of 32 vectors (one warp), each block
+// row-major [row i][lane] (256 B per row), blocks one after the other: element (i, j) at
+// ((j / 32) n + i) 32 + j % 32.  A warp's rows [a, b) are one contiguous span.
+__host__ __device__ __forceinline__ int64_t bix(int64_t i, int64_t j, int64_t n) {
+    return ((j >> 5) * n + i) * 32 + (j & 31);
+}
+
 // ---------------------------------------------------------------- packed layouts
 // Y (row-major, zero-free "assignment model" of Fig. 1): row i of
 // Y_m holds columns 0..min(i, m-1), padded to an even count (16-byte rows).  Narrow clusters

@@ -79,11 +79,16 @@ struct tinv_s {
     int* h_cstart = nullptr;
     int* h_iters = nullptr;
     int64_t h_cap = 0;
+    // pinned image of the cWY schedule header
+    void* h_hdr = nullptr;
+    size_t h_hdr_bytes = 0;
     // host-buffer path
     double* io = nullptr;
     size_t io_bytes = 0;
     // events for profiling
     cudaEvent_t ev[16] = {};
+    cudaStream_t side = nullptr;      // cluster-table readback overlapped with the batched LU
+    cudaEvent_t ev_prep = nullptr;
     tinv_stats_t stats{};
 };
 
@@ -300,6 +305,8 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     h->nsm = prop.multiProcessorCount;
     CK(cudaMallocHost(&h->h_out, sizeof(PrepOut)));
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
     if (h->nranks > 1) {
         if (!cfg->nccl_id || !g_nccl.load()) { delete h; return TINV_ERR_NCCL; }
         ncclUniqueId id;
@@ -321,7 +328,10 @@ int tinv_destroy(tinv_t h) {
     if (h->h_out) cudaFreeHost(h->h_out);
     if (h->h_cstart) cudaFreeHost(h->h_cstart);
     if (h->h_iters) cudaFreeHost(h->h_iters);
+    if (h->h_hdr) cudaFreeHost(h->h_hdr);
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    if (h->ev_prep) cudaEventDestroy(h->ev_prep);
+    if (h->side) cudaStreamDestroy(h->side);
     delete h;
     return 0;
 }
@@ -356,7 +366,9 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     S.n = n;
     int launches = 0;
 
-    // ---------------- prep
+    // ---------------- prep, then (without waiting for the host) the batched LU, the
+    // finalize of finished vectors and the factor/iterate packing of clustered vectors; the
+    // cluster table is read back on a side stream meanwhile and scheduled on the host.
     ev_record(h, 0);
     CK(cudaMemsetAsync(h->out, 0, sizeof(PrepOut), st));
     PrepArgs pa{n, d, e, w, h->wt, h->cstart, h->cid, h->jc, h->out};
@@ -364,13 +376,35 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     launches++;
     CK(cudaGetLastError());
     ev_record(h, 1);
-    CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h->h_cstart, h->cstart, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaEventRecord(h->ev_prep, st));
+    CK(cudaStreamWaitEvent(h->side, h->ev_prep, 0));
+    CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, h->side));
+    CK(cudaMemcpyAsync(h->h_cstart, h->cstart, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, h->side));
+    ev_record(h, 2);
+    BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
+                   h->X, h->unn, h->zscale, h->iters, h->out};
+    launch_batched(ba, st, h->nsm);
+    launches++;
+    CK(cudaGetLastError());
+    ev_record(h, 3);
+    FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->jc, Z, ldz, h->out};
+    launch_finalize(fa, st);
+    launches++;
+    CK(cudaGetLastError());
+    ev_record(h, 4);
+    PackArgs pk{n, h->ldv, h->jc, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP, h->X, h->X1c};
+    launch_pack(pk, st);
+    launches++;
+    CK(cudaGetLastError());
+    ev_record(h, 8);
+    CK(cudaStreamSynchronize(h->side));
     const PrepOut po = *h->h_out;
-    if (po.bad & 1) return -3;
-    if (po.bad & 2) return -4;
-    if (po.bad & 4) return -5;
+    if (po.bad) {
+        CK(cudaStreamSynchronize(st));
+        if (po.bad & 1) return -3;
+        if (po.bad & 2) return -4;
+        return -5;
+    }
     const double tnorm = po.tnorm;
     const int nclus = po.nclus;
     S.nclusters = nclus;
@@ -386,20 +420,6 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         return 0;
     }
     const int* cs = h->h_cstart;
-
-    // ---------------- batched LU + finalize of finished vectors
-    ev_record(h, 2);
-    BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, tnorm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
-                   h->X, h->unn, h->zscale, h->iters, h->out};
-    launch_batched(ba, st, h->nsm);
-    launches++;
-    CK(cudaGetLastError());
-    ev_record(h, 3);
-    FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->jc, Z, ldz};
-    launch_finalize(fa, st);
-    launches++;
-    CK(cudaGetLastError());
-    ev_record(h, 4);
 
     // ---------------- compact-WY kernel over this rank's clusters
     std::vector<int> rlo, rhi;
@@ -419,22 +439,24 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
     Schedule sc = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
     if (!sc.size.empty()) {
-        PackArgs pk{n, h->ldv, h->jc, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP, h->X, h->X1c};
-        launch_pack(pk, st);
-        launches++;
-        CK(cudaGetLastError());
         const int ng = (int)sc.size.size();
         // workspace: schedule arrays + per-group buffers
         unsigned long long* prof = nullptr;
+        // header (schedule arrays, per-group descriptors, barriers) is one contiguous block
+        // filled on the host and copied with a single H2D transfer
+        size_t hdr_lo = 0, hdr_hi = 0;
         auto layout = [&](char* p, std::vector<GroupWS>& ws, int** arrs, long long** syncs, GroupWS** dws) {
             Carve c{p};
             prof = c.take<unsigned long long>((size_t)ng * 16);
             arrs[0] = c.take<int>(ng);
+            hdr_lo = (size_t)((char*)arrs[0] - p);
             arrs[1] = c.take<int>(ng);
             arrs[2] = c.take<int>(ng + 1);
             arrs[3] = c.take<int>(sc.clist.size());
             *syncs = c.take<long long>(ng);
             *dws = c.take<GroupWS>(ng);
+            GroupBarrier* bars = c.take<GroupBarrier>(ng);
+            hdr_hi = c.off;
             ws.resize(ng);
             for (int g = 0; g < ng; g++) {
                 int64_t mc = sc.mcap[g];
@@ -456,7 +478,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.P = c.take<double>((size_t)G * W.mcap);
                 W.P2 = c.take<double>((size_t)G * W.mcap);
                 W.S = c.take<double>((size_t)G * 16 + 16);
-                W.bar = c.take<GroupBarrier>(1);
+                W.bar = bars + g;
             }
             return c.off;
         };
@@ -474,12 +496,29 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             h->cw_bytes = need;
         }
         layout((char*)h->cw, ws, arrs, &syncs, &dws);
-        CK(cudaMemcpyAsync(arrs[0], sc.cta0.data(), sizeof(int) * ng, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(arrs[1], sc.size.data(), sizeof(int) * ng, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(arrs[2], sc.coff.data(), sizeof(int) * (ng + 1), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(arrs[3], sc.clist.data(), sizeof(int) * sc.clist.size(), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(dws, ws.data(), sizeof(GroupWS) * ng, cudaMemcpyHostToDevice, st));
-        for (int g = 0; g < ng; g++) CK(cudaMemsetAsync(ws[g].bar, 0, sizeof(GroupBarrier), st));
+        const size_t hb = hdr_hi - hdr_lo;
+        if (hb > h->h_hdr_bytes) {
+            if (h->h_hdr) cudaFreeHost(h->h_hdr);
+            h->h_hdr = nullptr;
+            h->h_hdr_bytes = 0;
+            CK(cudaMallocHost(&h->h_hdr, hb));
+            h->h_hdr_bytes = hb;
+        }
+        {
+            char* base = (char*)h->cw;
+            char* img = (char*)h->h_hdr;
+            // the previous call's H2D from this pinned image must have completed
+            memset(img, 0, hb);
+            auto put = [&](const void* dev, const void* src, size_t bytes) {
+                memcpy(img + ((const char*)dev - base - hdr_lo), src, bytes);
+            };
+            put(arrs[0], sc.cta0.data(), sizeof(int) * ng);
+            put(arrs[1], sc.size.data(), sizeof(int) * ng);
+            put(arrs[2], sc.coff.data(), sizeof(int) * (ng + 1));
+            put(arrs[3], sc.clist.data(), sizeof(int) * sc.clist.size());
+            put(dws, ws.data(), sizeof(GroupWS) * ng);
+            CK(cudaMemcpyAsync(base + hdr_lo, img, hb, cudaMemcpyHostToDevice, st));
+        }
         CwyArgs ca{};
         ca.n = n; ca.ldv = h->ldv; ca.d = d; ca.e = e; ca.tnorm = tnorm; ca.seed = seed;
         ca.wt = h->wt; ca.cstart = h->cstart;
@@ -552,9 +591,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]); S.kernel_ms[0] = ms;
         cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); S.kernel_ms[1] = ms;
         cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); S.kernel_ms[2] = ms;
+        cudaEventElapsedTime(&ms, h->ev[4], h->ev[8]); S.kernel_ms[4] = ms;
         if (!sc.size.empty()) { cudaEventElapsedTime(&ms, h->ev[5], h->ev[6]); S.kernel_ms[3] = ms; }
         cudaEventElapsedTime(&ms, h->ev[0], h->ev[7]); S.kernel_ms[5] = ms;
-        S.kernel_launches[0] = 1; S.kernel_launches[1] = 1; S.kernel_launches[2] = 1;
+        S.kernel_launches[0] = 1; S.kernel_launches[1] = 1; S.kernel_launches[2] = 1; S.kernel_launches[4] = 1;
         S.kernel_launches[3] = sc.size.empty() ? 0 : 1;
     }
     const int nflag = h->h_out->nflag;

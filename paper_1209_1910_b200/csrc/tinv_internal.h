@@ -39,9 +39,8 @@ struct BatchedArgs {
     const double* e;
     const double* wt;
     const int* jc;
-    double tnorm;
     uint64_t seed;
-    // factors, [i][j]
+    // factors, block-row layout (common.cuh bix)
     double* fl;         // multipliers l_i (row i < n-1)
     int8_t* fp;         // row swap flags
     double* fr;         // 1/u0_i
@@ -77,6 +76,7 @@ struct FinalizeArgs {
     const int* jc;
     double* Z;
     int64_t ldz;
+    const PrepOut* out;
 };
 
 // Per-group workspace of the persistent compact-WY kernel.
