@@ -71,27 +71,30 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // the gpu-scope fences give the release/acquire ordering (and invalidate L1) so data
 // written by any CTA before the barrier is visible to every CTA after it.
 struct GroupBarrier {
-    unsigned int count;
-    unsigned int gen;
+    unsigned int count;   // monotonic arrival counter (episode e completes at count == e G)
+    unsigned int pad;
 };
 
-__device__ __forceinline__ void group_sync(GroupBarrier* b, int G) {
+// `epoch` is the caller's episode counter (identical in every CTA of the group): arrive with
+// one atomic, then poll until all G CTAs of this episode have arrived.  The gpu-scope fences
+// give the release/acquire ordering (and invalidate L1) so data written by any CTA before the
+// barrier is visible to every CTA after it.  A barrier that never completes traps.
+__device__ __forceinline__ void group_sync(GroupBarrier* b, int G, unsigned int& epoch) {
     if (G == 1) {
         __syncthreads();
         return;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned int* vgen = &b->gen;
-        unsigned int g0 = *vgen;
+        epoch++;
+        const unsigned int target = epoch * (unsigned int)G;
         __threadfence();
-        unsigned int arrived = atomicAdd(&b->count, 1u);
-        if (arrived == (unsigned)G - 1) {
-            b->count = 0;
-            __threadfence();
-            atomicAdd(&b->gen, 1u);
-        } else {
-            while (*vgen == g0) { __nanosleep(20); }
+        unsigned int v = atomicAdd(&b->count, 1u) + 1u;
+        volatile unsigned int* vc = &b->count;
+        uint32_t spins = 0;
+        while ((int)(v - target) < 0) {
+            v = *vc;
+            if (++spins > (1u << 30)) __trap();
         }
         __threadfence();
     }
@@ -156,6 +159,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// add transaction bytes without arriving (several lanes may each announce their own copy)
+__device__ __forceinline__ void mbar_add_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -165,8 +176,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Waits for the phase; a wait that never completes (a pipeline bug) traps after ~10 s
+// instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
+        if (++spins > (1u << 27)) __trap();
     }
 }
 // bytes: multiple of 16; src, dst 16-byte aligned

@@ -33,7 +33,9 @@ constexpr int NW = NT / 32;
 constexpr int CFCH = 2048;   // rows whose coefficients are staged in shared memory at once
 constexpr int CH = 256;                              // back-sweep ring chunk (rows)
 constexpr int kRing = 4;                             // back-sweep ring depth
-constexpr int64_t kSolveDoubles = kRing * 5 * CH;    // ring slots (4 CH factor doubles + CH t) in Smem::vs
+constexpr int64_t kSolveDoubles = kRing * 5 * CH;    // back-sweep ring slots (4 CH factor doubles + CH t)
+constexpr int kVsD = 128;                            // staged vector of the short (P <= 65) passes
+constexpr int kNBar = 32;                            // mbarrier slots (incl. 2 use counters), 16-B multiple
 
 // Global accesses: data produced inside this kernel by other CTAs goes through L2 (.cg,
 // never a stale L1 line); explicit global-space intrinsics also let the compiler hoist
@@ -105,8 +107,13 @@ __device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int
 
 // dynamic shared memory carve-up
 struct Smem {
-    double* vs;      // staged vector (vcap + 2 doubles)
+    double* vs;      // staged vector of the short passes (kVsD doubles)
     double* cf;      // CFCH coefficients
+    double* racc;    // 2 RCH row accumulators of wide row dots
+    double* vblk;    // 2 x 2 PW: column blocks of the wide row-dot vectors (double buffer)
+    uint64_t* vbar;  // 2 mbarriers of the vector double buffer
+    uint32_t* vuse;  // 2 use counters (shared)
+    double* bring;   // back-sweep ring (kSolveDoubles), aliases the pass ring
     double2* acc;    // NT
     double* red;     // NW + 8
     uint64_t* mbar;  // kRing mbarriers (back-sweep ring)
@@ -402,7 +409,7 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
     const double* __restrict__ F = a.F + j * n * 4;
     const double* __restrict__ ts = ws.ysol;
     double* __restrict__ x = ws.x;
-    double* ring = sm.vs;                                    // kRing x (4 CH + CH) doubles
+    double* ring = sm.bring;                                 // kRing x (4 CH + CH) doubles
     const int64_t C = (n + CH - 1) / CH;
     fence_proxy_async_global();
     auto issue = [&](int64_t k) {
@@ -590,7 +597,7 @@ struct Ring {
     double* base;      // kNStg slots of kStgD doubles
     uint64_t* mbar;    // kNStg mbarriers
     uint32_t* ph;      // phase bits (per thread copy)
-    uint64_t* tacc;    // optional timers (wait, body, sync) of the timing thread, or nullptr
+    uint64_t* tacc;    // optional timers (wait, body, sync+issue, block end) of the timing thread, or nullptr
 };
 
 // Stream rows [i0, i1) of Y (and coef[i0, i1) if coef != nullptr) through the ring; for each
@@ -709,29 +716,407 @@ __device__ __forceinline__ void narrow_colacc_finish(const Smem& sm, int CPT, in
     __syncthreads();
 }
 
+// ---------------------------------------------------------------- TMA streaming, wide passes
+// Passes with more than kNarrowM columns (every pass of a cluster with m > kNarrowM once
+// p > kNarrowM, and the T passes) stream their rows in column-block-major order: block kb
+// covers columns [kb PW, kb PW + PW); for each block the rows that reach it are cut into
+// pieces (one TMA bulk copy per row piece), PPS pieces per ring stage.  Warp-specialised:
+// warp 0 only issues the copies (gated by per-slot "empty" mbarriers), warps 1..7 consume
+// (full mbarriers) and release.  Row dots: consumer warp w takes piece w-1, with the current
+// block of the vector(s) in shared memory (TMA double buffer, next block prefetched), and
+// adds its warp sum into a per-row accumulator (fixed block order: deterministic).  Column
+// accumulates: consumer thread t' owns the block's columns 2t', 2t'+1 and adds the pieces'
+// rows in order.  Rows of one pass are processed in chunks of <= RCH rows.
+constexpr int NCW = NW - 1;              // consumer warps
+constexpr int NCT = NCW * 32;            // consumer threads
+constexpr int PW = 2 * NCT;              // column block / piece width (doubles) = 448
+constexpr int PPS = NCW;                 // pieces per stage = consumer warps
+constexpr int RCH = 1024;                // rows per chunk (row accumulators; coefficients in Smem::cf)
+constexpr int kWStgD = PPS * PW;         // doubles per wide ring slot
+constexpr int kWStg = 7;                 // wide ring depth
+constexpr int kPfAhead = 0;              // wide stages prefetched into L2 beyond the ring (0: off;
+                                         // measured slower on B200: the prefetches compete with
+                                         // the ring's own bulk copies)
+constexpr int64_t kRingD = (int64_t)kWStg * kWStgD > (int64_t)kNStg * kStgD ? (int64_t)kWStg * kWStgD
+                                                                            : (int64_t)kNStg * kStgD;
+static_assert(kSolveDoubles <= kRingD, "back-sweep ring aliases the pass ring");
+
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
+
+// Row source of a wide pass: row r has valid columns [cs(r), ce(r)) stored from column 0 at
+// base(r) (16-byte aligned; storage padded to an even column count).  Indices are 32-bit.
+struct SrcY {      // rows of Y_P (packed row-major, zero-free)
+    const double* Y;
+    int m, P;
+    __device__ const double* base(int r) const { return Y + y_row_off(r, m); }
+    __device__ int cs(int) const { return 0; }
+    __device__ int ce(int r) const { return r + 1 < P ? r + 1 : P; }
+    // rows of [r0, r1) that reach block kb: ce(r) > kb PW  <=>  r >= kb PW
+    __device__ void rows(int kb, int r0, int r1, int& a, int& b) const {
+        a = max(r0, kb * PW);
+        b = r1;
+    }
+    __device__ int nblk() const { return (P + PW - 1) / PW; }
+};
+struct SrcTc {     // column-packed T: "row" k = T[0..k, k]
+    const double* Tc;
+    int P;
+    __device__ const double* base(int k) const { return Tc + tcol_off(k); }
+    __device__ int cs(int) const { return 0; }
+    __device__ int ce(int k) const { return k + 1; }
+    __device__ void rows(int kb, int r0, int r1, int& a, int& b) const {
+        a = max(r0, kb * PW);
+        b = r1;
+    }
+    __device__ int nblk() const { return (P + PW - 1) / PW; }
+};
+struct SrcTr {     // row-major T: row l = T[l, l..P)
+    const double* Tr;
+    int m2, P;
+    __device__ const double* base(int l) const { return Tr + (int64_t)l * m2; }
+    __device__ int cs(int l) const { return l; }
+    __device__ int ce(int) const { return P; }
+    __device__ void rows(int kb, int r0, int r1, int& a, int& b) const {
+        a = r0;
+        b = min(r1, (kb + 1) * PW);
+    }
+    __device__ int nblk() const { return (P + PW - 1) / PW; }
+};
+
+// Pipeline state of the wide ring: full[s] completes when stage s's bulk copies land, empty[s]
+// when all NW warps released it.  Global stage counters (issued / consumed) persist across
+// passes, so slot = count % kNStg and the phase parity = (count / kNStg) & 1.
+struct WRing {
+    double* base;
+    uint64_t* full;     // kWStg (count 1 + tx)
+    uint64_t* empty;    // kWStg (count NCW consumer warps)
+    uint32_t* issued;   // producer warp's counter
+    uint32_t* used;     // consumer threads' counter
+    uint64_t* tacc;     // optional timers (wait, body, release, block end) or nullptr
+};
+
+// Walk (chunk of rows, block kb, stage of <= PPS rows) in the order above.  Consumers (warps
+// 1..NCW) call blk_begin(kb, c0, c1) at the first stage of each block, body(kb, ra, rb, slot)
+// per stage (piece q = row ra + q at slot + q PW, columns [kb PW, kb PW + PW), only the valid
+// ones copied) and blk_end(kb) after its last stage; these may use consumer_sync() but not
+// __syncthreads.  chunk_begin / chunk_end run on all threads around each chunk (may
+// __syncthreads).
+template <class Src, class Body, class BlkBegin, class BlkEnd, class ChunkBegin, class ChunkEnd>
+__device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, bool reverse_blocks,
+                            ChunkBegin chunk_begin, BlkBegin blk_begin, Body body, BlkEnd blk_end,
+                            ChunkEnd chunk_end) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int NB = src.nblk();
+    for (int c0 = r0; c0 < r1; c0 += RCH) {
+        const int c1 = min(r1, c0 + RCH);
+        chunk_begin(c0, c1);
+        auto blk_of = [&](int t) { return reverse_blocks ? NB - 1 - t : t; };
+        // stage cursor: block step t, next row; returns false at the end
+        auto next = [&](int& t, int& row, int& ra, int& rb) -> bool {
+            while (t < NB) {
+                int a, b;
+                src.rows(blk_of(t), c0, c1, a, b);
+                row = max(row, a);
+                if (row < b) {
+                    ra = row;
+                    rb = min(b, row + PPS);
+                    row = rb;
+                    return true;
+                }
+                t++;
+                row = -1;
+            }
+            return false;
+        };
+        int t = 0, row = -1, ra = 0, rb = 0;
+        if (warp == 0) {
+            // ---- producer: lane q copies piece q of every stage; a second cursor kPfAhead
+            // stages further on prefetches the same pieces into L2
+            auto piece = [&](int kb, int r, int& a, int& b) {
+                a = max(src.cs(r) & ~1, kb * PW);
+                b = min((src.ce(r) + 1) & ~1, kb * PW + PW);
+            };
+            int ft = 0, frow = -1, fra = 0, frb = 0;
+            bool fmore = true;
+            auto prefetch_next = [&]() {
+                if (kPfAhead == 0) return;
+                if (fmore && (fmore = next(ft, frow, fra, frb))) {
+                    const int r = fra + lane;
+                    if (r < frb) {
+                        int a, b;
+                        piece(blk_of(ft), r, a, b);
+                        if (b > a) l2_prefetch(src.base(r) + a, b - a);
+                    }
+                }
+            };
+            if (lane == 0) fence_proxy_async_global();
+            __syncwarp();
+            for (int k = 0; k < kWStg + kPfAhead; k++) prefetch_next();
+            while (next(t, row, ra, rb)) {
+                const int kb = blk_of(t);
+                const uint32_t g = *rg.issued;
+                const int slot = (int)(g % kWStg);
+                if (g >= (uint32_t)kWStg) mbar_wait(rg.empty + slot, ((g / kWStg) - 1) & 1u);
+                const int r = ra + lane;
+                if (r < rb) {
+                    int a, b;
+                    piece(kb, r, a, b);
+                    if (b > a) {
+                        const uint32_t bytes = (uint32_t)(b - a) * 8u;
+                        mbar_add_tx(rg.full + slot, bytes);
+                        bulk_g2s(rg.base + (int64_t)slot * kWStgD + (r - ra) * PW + (a - kb * PW), src.base(r) + a,
+                                 bytes, rg.full + slot);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(rg.full + slot);
+                *rg.issued = g + 1;
+                prefetch_next();
+            }
+        } else {
+            // ---- consumers
+            int last_kb = -1;
+            while (next(t, row, ra, rb)) {
+                const int kb = blk_of(t);
+                const uint64_t c0t = rg.tacc ? gtime() : 0;
+                if (kb != last_kb) {
+                    if (last_kb >= 0) blk_end(last_kb);
+                    blk_begin(kb, c0, c1);
+                }
+                last_kb = kb;
+                const uint32_t u = *rg.used;
+                const int slot = (int)(u % kWStg);
+                const uint64_t c1t = rg.tacc ? gtime() : 0;
+                mbar_wait(rg.full + slot, (u / kWStg) & 1u);
+                const uint64_t c2t = rg.tacc ? gtime() : 0;
+                body(kb, ra, rb, rg.base + (int64_t)slot * kWStgD);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(rg.empty + slot);
+                *rg.used = u + 1;
+                if (rg.tacc) {
+                    const uint64_t c3t = gtime();
+                    rg.tacc[3] += c1t - c0t;
+                    rg.tacc[0] += c2t - c1t;
+                    rg.tacc[1] += c3t - c2t;
+                }
+            }
+            if (last_kb >= 0) blk_end(last_kb);
+        }
+        __syncthreads();   // ring drained before the next chunk / pass
+        chunk_end(c0, c1);
+    }
+}
+
+// Row dots of a wide pass: dot(r) = sum_{cs(r) <= k < ce(r)} row_r[k] v[k] (and with a second
+// vector w when TWO); epi(r, dot, dot2) after all blocks, one thread per row.
+template <bool TWO, class Src, class Epi>
+__device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, int r0, int r1, const double* v,
+                             const double* w, int P, Epi epi) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* racc = sm.racc;           // RCH (x2 when TWO)
+    int cb = 0;
+    // vector blocks: TMA copies into a double buffer (buffer kb & 1), block kb + 1 prefetched
+    // when block kb starts; one mbarrier per buffer; issued by consumer thread 32
+    auto vfetch = [&](int kb) {
+        const int buf = kb & 1;
+        const int a = kb * PW, b = min(P, kb * PW + PW);
+        const uint32_t bytes = (uint32_t)(((b - a + 1) & ~1) * 8);
+        mbar_expect_tx(sm.vbar + buf, bytes * (TWO ? 2u : 1u));
+        bulk_g2s(sm.vblk + buf * 2 * PW, v + a, bytes, sm.vbar + buf);
+        if (TWO) bulk_g2s(sm.vblk + buf * 2 * PW + PW, w + a, bytes, sm.vbar + buf);
+    };
+    const int NB = src.nblk();
+    int pre = -1;   // block prefetched into its buffer (thread 32)
+    wide_stream(
+        rg, src, r0, r1, false,
+        [&](int c0, int c1) {
+            cb = c0;
+            pre = -1;
+            for (int i = threadIdx.x; i < c1 - c0; i += NT) {
+                racc[i] = 0.0;
+                if (TWO) racc[RCH + i] = 0.0;
+            }
+            __syncthreads();
+        },
+        [&](int kb, int c0, int c1) {
+            consumer_sync();   // all consumers are done with the buffer that kb + 1 will overwrite
+            if (threadIdx.x == 32) {
+                fence_proxy_async_global();
+                if (pre != kb) vfetch(kb);       // not prefetched by the previous block
+                pre = -1;
+                if (kb + 1 < NB) {               // blocks with rows are contiguous in the walk
+                    int a, b;
+                    src.rows(kb + 1, c0, c1, a, b);
+                    if (a < b) {
+                        vfetch(kb + 1);
+                        pre = kb + 1;
+                    }
+                }
+            }
+            const uint32_t u = sm.vuse[kb & 1];
+            mbar_wait(sm.vbar + (kb & 1), u & 1u);
+            consumer_sync();
+            if (threadIdx.x == 32) sm.vuse[kb & 1] = u + 1;
+        },
+        [&](int kb, int ra, int rb, const double* slot) {
+            const int q = warp - 1;
+            const int r = ra + q;
+            if (r < rb) {
+                const int lo = src.cs(r), hi = src.ce(r);
+                const double* vb = sm.vblk + (kb & 1) * 2 * PW;
+                double a1 = 0.0, a2 = 0.0;
+                const double* rowp = slot + q * PW;
+                const int kbase = kb * PW;
+                if (lo <= kbase && hi >= kbase + PW) {   // full piece: no masks
+#pragma unroll
+                    for (int e = 0; e < PW; e += 64) {
+                        const int cl = e + 2 * lane;
+                        const double2 y = *reinterpret_cast<const double2*>(rowp + cl);
+                        const double2 vv = *reinterpret_cast<const double2*>(vb + cl);
+                        a1 = fma(y.x, vv.x, a1);
+                        a1 = fma(y.y, vv.y, a1);
+                        if (TWO) {
+                            const double2 ww = *reinterpret_cast<const double2*>(vb + PW + cl);
+                            a2 = fma(y.x, ww.x, a2);
+                            a2 = fma(y.y, ww.y, a2);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < PW; e += 64) {   // lane: columns e + 2 lane, +1 (conflict-free)
+                        const int cl = e + 2 * lane;
+                        const int k = kbase + cl;
+                        if (k + 1 >= lo && k < hi) {
+                            const double2 y = *reinterpret_cast<const double2*>(rowp + cl);
+                            const double2 vv = *reinterpret_cast<const double2*>(vb + cl);
+                            const double y0 = (k >= lo) ? y.x : 0.0;
+                            const double y1 = (k + 1 < hi) ? y.y : 0.0;
+                            a1 = fma(y0, vv.x, a1);
+                            a1 = fma(y1, vv.y, a1);
+                            if (TWO) {
+                                const double2 ww = *reinterpret_cast<const double2*>(vb + PW + cl);
+                                a2 = fma(y0, ww.x, a2);
+                                a2 = fma(y1, ww.y, a2);
+                            }
+                        }
+                    }
+                }
+                a1 = warp_sum(a1);
+                if (TWO) a2 = warp_sum(a2);
+                if (lane == 0) {
+                    racc[r - cb] += a1;
+                    if (TWO) racc[RCH + r - cb] += a2;
+                }
+            }
+        },
+        [&](int) {},
+        [&](int c0, int c1) {
+            for (int r = c0 + threadIdx.x; r < c1; r += NT) {
+                if (TWO) epi(r, racc[r - c0], racc[RCH + r - c0]);
+                else epi(r, racc[r - c0], 0.0);
+            }
+            __syncthreads();
+        });
+}
+
+// Column accumulate of a wide pass: out[k] = sum_r row_r[k] coef(r) for k < P over rows
+// [r0, r1); coefficients staged per chunk from coef (global).  Returns sum coef^2.
+template <class Src>
+__device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, int r0, int r1, const double* coef,
+                              int P, double* out, bool reverse_blocks) {
+    const int tid = threadIdx.x, tc = tid - 32;   // consumer thread index
+    double c2 = 0.0;
+    double a0 = 0.0, a1 = 0.0;
+    int cb = 0;
+    // The accumulate owns columns 2tc, 2tc+1 of every block.  With one row chunk each block's
+    // sums are final at its end (plain store); with several chunks they are added up (zeroed
+    // first).  Blocks that no row of this CTA reaches are zero.
+    const bool multi = (r1 - r0) > RCH;
+    if (tc >= 0)
+        for (int kb = 0; kb < src.nblk(); kb++) {
+            int a, b;
+            src.rows(kb, r0, r1, a, b);
+            if (a < b && !multi) continue;   // written by blk_end
+            const int k = kb * PW + 2 * tc;
+            if (k < P) st(out + k, 0.0);
+            if (k + 1 < P) st(out + k + 1, 0.0);
+        }
+    if (r1 <= r0) return 0.0;
+    wide_stream(
+        rg, src, r0, r1, reverse_blocks,
+        [&](int c0, int c1) {
+            cb = c0;
+            for (int r = c0 + tid; r < c1; r += NT) {
+                const double c = ld(coef + r);
+                sm.cf[r - c0] = c;
+                c2 = fma(c, c, c2);
+            }
+            __syncthreads();
+            a0 = a1 = 0.0;
+        },
+        [&](int, int, int) {},
+        [&](int kb, int ra, int rb, const double* slot) {
+            const int k = kb * PW + 2 * tc;
+            for (int r = ra; r < rb; r++) {
+                const int lo = src.cs(r), hi = src.ce(r);
+                if (k + 1 >= lo && k < hi) {
+                    const double2 y = *reinterpret_cast<const double2*>(slot + (r - ra) * PW + 2 * tc);
+                    const double c = sm.cf[r - cb];
+                    if (k >= lo) a0 = fma(y.x, c, a0);
+                    if (k + 1 < hi) a1 = fma(y.y, c, a1);
+                }
+            }
+        },
+        [&](int kb) {
+            const int k = kb * PW + 2 * tc;
+            if (k < P) st(out + k, multi ? ld(out + k) + a0 : a0);
+            if (k + 1 < P) st(out + k + 1, multi ? ld(out + k + 1) + a1 : a1);
+            a0 = a1 = 0.0;
+        },
+        [&](int, int) {});
+    return c2;
+}
+
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem sm;
     {
-        const int64_t vdoubles = ((a.vcap + 2 > kSolveDoubles ? a.vcap + 2 : kSolveDoubles) + 1) & ~int64_t(1);
         sm.vs = reinterpret_cast<double*>(smem_raw);
-        sm.cf = sm.vs + vdoubles;
-        sm.acc = reinterpret_cast<double2*>(sm.cf + CFCH);
+        sm.cf = sm.vs + kVsD;
+        sm.racc = sm.cf + CFCH;
+        sm.vblk = sm.racc + 2 * RCH;
+        sm.acc = reinterpret_cast<double2*>(sm.vblk + 4 * PW);
         sm.red = reinterpret_cast<double*>(sm.acc + NT);
         sm.mbar = reinterpret_cast<uint64_t*>(sm.red + NW + 8);
     }
-    double* ring_base = reinterpret_cast<double*>(sm.mbar + kRing + kNStg);   // 16-B aligned (see cwy_smem_bytes)
+    // mbarriers: [0, kRing) back sweep, [kRing, +kNStg) narrow ring, then wide full, wide
+    // empty, vector double buffer; vuse counters after them
+    uint64_t* wfull = sm.mbar + kRing + kNStg;
+    uint64_t* wempty = wfull + kWStg;
+    sm.vbar = wempty + kWStg;
+    sm.vuse = reinterpret_cast<uint32_t*>(sm.vbar + 2);
+    double* ring_base = reinterpret_cast<double*>(sm.mbar + kNBar);   // 16-B aligned (see cwy_smem_bytes)
+    sm.bring = ring_base;   // the back-sweep ring aliases the pass ring (never in use together)
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing + kNStg; k++) mbar_init(sm.mbar + k, 1);
+        for (int k = 0; k < kWStg; k++) {
+            mbar_init(wfull + k, 1);
+            mbar_init(wempty + k, NCW);
+        }
+        mbar_init(sm.vbar, 1);
+        mbar_init(sm.vbar + 1, 1);
+        sm.vuse[0] = sm.vuse[1] = 0;
         fence_mbar_init();
     }
     __syncthreads();
     uint32_t mbph = 0;   // back-sweep ring phase bits (thread 0)
     uint32_t rph = 0;    // pass ring phase bits (every thread)
     const bool timing0 = (a.prof != nullptr) && threadIdx.x == 0 && (int)blockIdx.x == a.g_cta0[0];
-    uint64_t ntim[3] = {0, 0, 0};
+    uint64_t ntim[4] = {0, 0, 0, 0};
     const Ring rg{ring_base, sm.mbar + kRing, &rph, timing0 ? ntim : nullptr};
+    uint32_t wiss = 0, wuse = 0;   // wide ring stage counters (issued: warp 0; used: all)
+    const WRing wr{ring_base, wfull, wempty, &wiss, &wuse, timing0 ? ntim : nullptr};
     const int tid = threadIdx.x;
     int g = 0;
     for (int t = 0; t < a.ngroups; t++)
@@ -741,7 +1126,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     if (r >= G) return;  // CTA not used by any group
     const GroupWS ws = a.ws[g];
     long long nsync = 0;
-    auto gsync = [&]() { group_sync(ws.bar, G); nsync++; };
+    unsigned int bar_epoch = 0;
+    auto gsync = [&]() { group_sync(ws.bar, G, bar_epoch); nsync++; };
     // optional phase timers (thread 0 of each group's first CTA; globaltimer ns)
     const bool timing = (a.prof != nullptr) && r == 0 && tid == 0;
     uint64_t tacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -830,6 +1216,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                 narrow_colacc(ra, rb, (int)m2, Ys, Xs, CPT, [&](int i) -> int { return i + 1 < p ? i + 1 : (int)p; }, a0, a1);
                             });
                             narrow_colacc_finish(sm, CPT, p, a0, a1, P_ + (int64_t)r * mc);
+                        } else if (p > kNarrowM) {
+                            x2 = wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, xcur, p, P_ + (int64_t)r * mc, false);
                         } else {
                             x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)r * mc);
                         }
@@ -860,7 +1248,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t k0, k1;
                     part_tt(p, r, G, k0, k1);
-                    if (k1 > k0) {
+                    if (p > kNarrowM) {
+                        wide_rowdots<false>(sm, wr, SrcTc{Tc, (int)p}, (int)k0, (int)k1, ws.g, nullptr, p,
+                                            [&](int64_t k, double v, double) { st(ws.gp + k, v); });
+                    } else if (k1 > k0) {
                         stage_vec(sm, ws.g, p);
                         rowdots(k0, k1, p, sm.vs,
                                 [&](int64_t k) { return Tc + tcol_off(k); },
@@ -896,6 +1287,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         narrow_colacc_finish(sm, LPR, p, a0, a1, P_ + (int64_t)r * mc);
                         u2 = block_sum<NT>(u2, sm.red);
                         if (tid == 0) st(S + r * SST + SSlots::U2, u2);
+                    } else if (p > kNarrowM) {
+                        wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.gp, nullptr, p,
+                                            [&](int64_t i, double v, double) {
+                                                const double ui = ld(xcur + i) - v;
+                                                st(ws.u + i, ui);
+                                                u2 = fma(ui, ui, u2);
+                                            });
+                        u2 = block_sum<NT>(u2, sm.red);
+                        if (tid == 0) st(S + r * SST + SSlots::U2, u2);
+                        // second read of Yhat, blocks in reverse order (the last ones are in L2)
+                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)r * mc, true);
                     } else {
                         stage_vec(sm, ws.gp, p);
                         rowdots(i0, i1, p, sm.vs,
@@ -954,7 +1356,15 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t l0, l1;
                     part_tn(p, r, G, l0, l1);
-                    if (l1 > l0) {
+                    if (p > kNarrowM) {
+                        wide_rowdots<true>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, yrow, p,
+                                           [&](int64_t l, double a1, double a2) {
+                                               const double that = -tt * a1;
+                                               st(ws.xp + l, a2 + y0 * that);
+                                               st(Tc + tcol_off(p) + l, that);
+                                               st(Tr + l * m2 + p, that);
+                                           });
+                    } else if (l1 > l0) {
                         stage_vec(sm, ws.s, p);
                         const int lane = tid & 31, warp = tid >> 5;
                         constexpr int U = 4;
@@ -1042,6 +1452,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         narrow_stream(rg, Y, (int)m2, (int)i0, (int)i1, nullptr, [&](int ra, int rb, const double* Ys, double*) {
                             narrow_rowdots(ra, rb, (int)m2, Ys, sm.vs, lendn, epiq);
                         });
+                    } else if (p + 1 > kNarrowM) {
+                        wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p + 1}, (int)i0, (int)i1, ws.xp, nullptr, p + 1,
+                                            [&](int64_t i, double v, double) { epiq(i, v); });
                     } else {
                         stage_vec(sm, ws.xp, p + 1);
                         rowdots(i0, i1, p + 1, sm.vs, [&](int64_t i) { return Y + y_row_off(i, m); }, lend, epiq);
@@ -1185,7 +1598,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         const int Gl = (G > 1) ? G - 1 : 1, rl = (G > 1) ? r - 1 : 0;
                         int64_t i0, i1;
                         part_rows_weighted(n, p, rl, Gl, i0, i1);
-                        double x2n = colacc(sm, Y, m, i0, i1, p, a.X1c + (j + 1) * n2v, 1, ws.P2 + (int64_t)r * mc);
+                        double x2n = (p > kNarrowM)
+                                         ? wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, a.X1c + (j + 1) * n2v, p,
+                                                       ws.P2 + (int64_t)r * mc, false)
+                                         : colacc(sm, Y, m, i0, i1, p, a.X1c + (j + 1) * n2v, 1, ws.P2 + (int64_t)r * mc);
                         x2n = block_sum<NT>(x2n, sm.red);
                         if (tid == 0) st(S + r * SST + SSlots::X2N, x2n);
                     }
@@ -1203,7 +1619,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     if (timing)
         for (int k = 0; k < 12; k++) a.prof[g * 16 + k] = tacc[k];
     if (timing0)
-        for (int k = 0; k < 3; k++) a.prof[12 + k] = ntim[k];
+        for (int k = 0; k < 4; k++) a.prof[12 + k] = ntim[k];
 #undef PH
 }
 
@@ -1212,9 +1628,10 @@ int cwy_narrow_max() { return kNarrowM; }
 int cwy_ring_stages() { return kNStg; }
 
 size_t cwy_smem_bytes(int64_t vcap, int nstg) {
-    int64_t vd = ((vcap + 2 > kSolveDoubles ? vcap + 2 : kSolveDoubles) + 1) & ~int64_t(1);
-    return sizeof(double) * (size_t)(vd + CFCH) + sizeof(double2) * NT + sizeof(double) * (NW + 8) +
-           sizeof(uint64_t) * (kRing + kNStg) + (nstg > 0 ? sizeof(double) * (size_t)kNStg * kStgD : 0);
+    (void)vcap;
+    (void)nstg;
+    return sizeof(double) * (size_t)(kVsD + CFCH + 2 * RCH + 4 * PW) + sizeof(double2) * NT + sizeof(double) * (NW + 8) +
+           sizeof(uint64_t) * kNBar + sizeof(double) * (size_t)kRingD;
 }
 
 int cwy_max_ctas_per_sm(size_t smem) {

@@ -18,7 +18,7 @@ EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version")
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
-PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "nw_wait", "nw_body", "nw_sync", "spare")
+PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "st_wait", "st_body", "st_sync", "st_blkend")
 
 
 class TinvConfig(C.Structure):
