@@ -79,6 +79,17 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
 int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
                       double* Z, int64_t ldz, uint64_t seed);
 
+/* Multi-rank partition of the eigenvectors (host only, no device needed): the clusters
+ * (cstart[0..nclus], cstart[0] = 0, cstart[nclus] = n, strictly increasing: the
+ * Peters-Wilkinson clusters of PAPER.md:135-139) are split into nranks contiguous,
+ * cost-balanced column ranges [col_lo[r], col_hi[r]) that never cut a cluster (cost of a
+ * cluster of m >= 2 vectors: m^2 n, the reorthogonalisation's HBM traffic; singletons: 1).
+ * tinv_eigvecs with nranks > 1 computes exactly these columns on rank r.  Deterministic.
+ * Returns 0, or -k for invalid argument k (n < 1; nclus outside [1, n]; cstart NULL or not a
+ * valid cluster table; nranks < 1; col_lo / col_hi NULL).  Arrays are caller-owned host
+ * memory of nclus + 1 and nranks entries. */
+int tinv_partition(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi);
+
 /* Release the handle and its device workspace. */
 int tinv_destroy(tinv_t h);
 

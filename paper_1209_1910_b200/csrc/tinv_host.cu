@@ -266,6 +266,25 @@ extern "C" {
 
 int tinv_abi_version(void) { return 1; }
 
+int tinv_partition(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi) {
+    if (n < 1) return -1;
+    if (nclus < 1 || nclus > n) return -2;
+    if (!cstart) return -3;
+    if (nranks < 1) return -4;
+    if (!col_lo) return -5;
+    if (!col_hi) return -6;
+    if (cstart[0] != 0 || cstart[nclus] != n) return -3;
+    for (int64_t c = 0; c < nclus; c++)
+        if (cstart[c + 1] <= cstart[c]) return -3;
+    std::vector<int> lo, hi;
+    rank_ranges(cstart, (int)nclus, n, nranks, lo, hi);
+    for (int r = 0; r < nranks; r++) {
+        col_lo[r] = cstart[lo[r]];
+        col_hi[r] = cstart[hi[r]];
+    }
+    return 0;
+}
+
 const char* tinv_strerror(int code) {
     if (code == 0) return "success";
     if (code > 0) return "some eigenvectors did not meet the stopping rule within MAXITS";

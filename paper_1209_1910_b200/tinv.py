@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtinv.so")
 
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
-           "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version")
+           "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition")
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
 PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "st_wait", "st_body", "st_sync", "st_blkend")
@@ -79,6 +79,8 @@ def load_library(path: str = LIB_PATH):
     L.tinv_get_stats.argtypes = [P, C.POINTER(TinvStats)]
     L.tinv_get_stats.restype = C.c_int
     L.tinv_abi_version.argtypes = []
+    L.tinv_partition.restype = C.c_int
+    L.tinv_partition.argtypes = [I64, I64, P, C.c_int, P, P]
     L.tinv_abi_version.restype = C.c_int
     _lib = L
     return L
@@ -179,3 +181,20 @@ def eigvecs(d, e, w, seed: int = 1, device: int = 0):
         return Z, rc, h.stats()
     finally:
         h.close()
+
+
+def partition(cstart, nranks: int):
+    """Column ranges [(lo, hi)] per rank computed by the library's multi-rank partitioner
+    (tinv_partition: host-only, no device).  ``cstart`` is the cluster table (length
+    nclus + 1, cstart[0] = 0, cstart[-1] = n)."""
+    import numpy as np
+
+    cs = np.ascontiguousarray(cstart, dtype=np.int32)
+    nclus = cs.shape[0] - 1
+    lo = np.zeros(nranks, dtype=np.int32)
+    hi = np.zeros(nranks, dtype=np.int32)
+    L = load_library()
+    rc = L.tinv_partition(int(cs[-1]), nclus, cs.ctypes.data, int(nranks), lo.ctypes.data, hi.ctypes.data)
+    if rc != 0:
+        raise TinvError(rc, L.tinv_strerror(rc).decode())
+    return list(zip(lo.tolist(), hi.tolist()))
