@@ -74,6 +74,19 @@ int tinv_create(tinv_t* h, const tinv_config_t* cfg);
 int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
                  double* Z, int64_t ldz, uint64_t seed);
 
+/* Eigenvalues of T by Sturm-count bisection (the DSTEBZ step before DSTEIN-cWY,
+ * PAPER.md:753-755): w[k] = k-th smallest eigenvalue to full fp64 accuracy (bisection of the
+ * padded Gershgorin interval until the midpoint equals an endpoint; Sturm count with LDL^T
+ * pivots, a zero pivot replaced by -eps ||T||_1 -- DESIGN.md reading 20).  d (n), e (n-1,
+ * NULL iff n == 1) and w (n, written, ascending) are DEVICE pointers.  Synchronous on the
+ * handle's stream.  Returns 0 or -k for invalid argument k (n < 1, NULL pointers). */
+int tinv_eigvals(tinv_t h, int64_t n, const double* d, const double* e, double* w);
+
+/* tinv_eigvals followed by tinv_eigvecs: all eigenpairs (w, Z) of T from (d, e) alone.
+ * Arguments and return codes as for tinv_eigvecs (w is written instead of read). */
+int tinv_eig(tinv_t h, int64_t n, const double* d, const double* e, double* w, double* Z, int64_t ldz,
+             uint64_t seed);
+
 /* Same operation with HOST buffers (pinned host memory recommended): the library copies
  * d, e, w to the device, runs tinv_eigvecs and copies Z back (end-to-end path). */
 int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, const double* w,

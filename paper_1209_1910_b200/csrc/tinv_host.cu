@@ -79,6 +79,7 @@ struct tinv_s {
     int* h_cstart = nullptr;
     int* h_iters = nullptr;
     int64_t h_cap = 0;
+    double* bnd = nullptr;            // bisection bounds (3 doubles)
     // pinned image of the cWY schedule header
     void* h_hdr = nullptr;
     size_t h_hdr_bytes = 0;
@@ -323,6 +324,7 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     h->stream = (cudaStream_t)cfg->stream;
     h->nsm = prop.multiProcessorCount;
     CK(cudaMallocHost(&h->h_out, sizeof(PrepOut)));
+    CK(cudaMalloc(&h->bnd, 4 * sizeof(double)));
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
@@ -344,6 +346,7 @@ int tinv_destroy(tinv_t h) {
     if (h->base) cudaFree(h->base);
     if (h->cw) cudaFree(h->cw);
     if (h->io) cudaFree(h->io);
+    if (h->bnd) cudaFree(h->bnd);
     if (h->h_out) cudaFreeHost(h->h_out);
     if (h->h_cstart) cudaFreeHost(h->h_cstart);
     if (h->h_iters) cudaFreeHost(h->h_iters);
@@ -619,6 +622,29 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const int nflag = h->h_out->nflag;
     S.nflagged = nflag;
     return nflag;
+}
+
+int tinv_eigvals(tinv_t h, int64_t n, const double* d, const double* e, double* w) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (n < 1) return -2;
+    if (!d) return -3;
+    if (!e && n > 1) return -4;
+    if (!w) return -5;
+    CK(cudaSetDevice(h->device));
+    launch_bisect(n, d, e, w, h->bnd, h->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    return 0;
+}
+
+int tinv_eig(tinv_t h, int64_t n, const double* d, const double* e, double* w, double* Z, int64_t ldz,
+             uint64_t seed) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (!Z) return -6;
+    if (ldz < n) return -7;
+    int rc = tinv_eigvals(h, n, d, e, w);
+    if (rc) return rc;
+    return tinv_eigvecs(h, n, d, e, w, Z, ldz, seed);
 }
 
 int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, const double* w,

@@ -135,6 +135,7 @@ struct CwyArgs {
 };
 
 void launch_prep(const PrepArgs& a, cudaStream_t s);
+void launch_bisect(int64_t n, const double* d, const double* e, double* w, double* bnd, cudaStream_t s);
 void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm);
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 void launch_pack(const PackArgs& a, cudaStream_t s);

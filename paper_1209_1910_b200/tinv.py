@@ -15,7 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtinv.so")
 
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
-           "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition")
+           "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",
+           "tinv_eigvals", "tinv_eig")
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
 PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "st_wait", "st_body", "st_sync", "st_blkend")
@@ -79,6 +80,10 @@ def load_library(path: str = LIB_PATH):
     L.tinv_get_stats.argtypes = [P, C.POINTER(TinvStats)]
     L.tinv_get_stats.restype = C.c_int
     L.tinv_abi_version.argtypes = []
+    L.tinv_eigvals.restype = C.c_int
+    L.tinv_eigvals.argtypes = [P, I64, P, P, P]
+    L.tinv_eig.restype = C.c_int
+    L.tinv_eig.argtypes = [P, I64, P, P, P, P, I64, C.c_uint64]
     L.tinv_partition.restype = C.c_int
     L.tinv_partition.argtypes = [I64, I64, P, C.c_int, P, P]
     L.tinv_abi_version.restype = C.c_int
@@ -153,6 +158,33 @@ class Tinv:
         if rc < 0 and check:
             raise TinvError(f"tinv_eigvecs failed: {rc} ({strerror(rc)})")
         return Zt.t(), rc
+
+    def eigvals(self, d, e, check: bool = True):
+        """Device path: eigenvalues of T (Sturm bisection, tinv_eigvals); d, e float64 CUDA
+        tensors; returns w (CUDA tensor, ascending)."""
+        torch = self._torch
+        n = int(d.shape[0])
+        for name, t in (("d", d),) + ((("e", e),) if n > 1 else ()):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise TinvError(f"{name} must be a contiguous float64 CUDA tensor")
+        w = torch.empty(n, dtype=torch.float64, device=d.device)
+        rc = self._L.tinv_eigvals(self._h, n, C.c_void_p(d.data_ptr()),
+                                  C.c_void_p(e.data_ptr()) if n > 1 else None, C.c_void_p(w.data_ptr()))
+        if rc < 0 and check:
+            raise TinvError(f"tinv_eigvals failed: {rc} ({strerror(rc)})")
+        return w
+
+    def eig(self, d, e, seed: int = 1, check: bool = True):
+        """All eigenpairs from (d, e): (w, Z, info) via tinv_eig."""
+        torch = self._torch
+        n = int(d.shape[0])
+        w = torch.empty(n, dtype=torch.float64, device=d.device)
+        Zt = torch.empty((n, n), dtype=torch.float64, device=d.device)
+        rc = self._L.tinv_eig(self._h, n, C.c_void_p(d.data_ptr()), C.c_void_p(e.data_ptr()) if n > 1 else None,
+                              C.c_void_p(w.data_ptr()), C.c_void_p(Zt.data_ptr()), n, int(seed))
+        if rc < 0 and check:
+            raise TinvError(f"tinv_eig failed: {rc} ({strerror(rc)})")
+        return w, Zt.t(), rc
 
     def eigvecs_host(self, d, e, w, Z=None, seed: int = 1, check: bool = True):
         """End-to-end path with host buffers (numpy or pinned CPU tensors)."""

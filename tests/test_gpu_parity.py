@@ -247,3 +247,57 @@ def test_stats_report_native_launches(handle, torch):
     st = handle.stats()
     assert st["launches"] >= 3 and st["n"] == 400 and st["nclusters"] >= 1
     assert sum(st["iters_hist"]) == 400
+
+
+# ------------------------------------------------------------------ eigenvalues
+
+@pytest.mark.parametrize("cfg,n", [("cfg1", None), ("cfg2", None), ("cfg3", 1050), ("cfg4", 600), ("cfg5", 1500),
+                                   ("type1", 333), ("type2", 257), ("type3", 105)])
+def test_bisection_bit_exact(handle, torch, cfg, n):
+    """Sturm counts are integers decided by floating point: the GPU takes every decision in
+    the oracle's arithmetic (explicit round-to-nearest, no contraction), so the eigenvalues are
+    identical bit for bit."""
+    d, e = W.make(cfg, n)
+    dev = torch.device("cuda:0")
+    w = handle.eigvals(torch.tensor(d, device=dev), torch.tensor(e, device=dev)).cpu().numpy()
+    wo = O.bisect(d, e)
+    assert np.array_equal(w, wo), np.abs(w - wo).max()
+
+
+def test_bisection_edge_cases(handle, torch):
+    dev = torch.device("cuda:0")
+    w = handle.eigvals(torch.tensor([3.5], dtype=torch.float64, device=dev), torch.zeros(0, dtype=torch.float64,
+                                                                                         device=dev))
+    assert w.cpu().numpy().tolist() == O.bisect(np.array([3.5]), np.zeros(0)).tolist()
+    for d, e in ((np.zeros(7), np.zeros(6)), (np.array([1.0, 1.0, 1.0]), np.zeros(2)),
+                 (np.full(40, 2.0), np.full(39, -1.0))):
+        w = handle.eigvals(torch.tensor(d, device=dev), torch.tensor(e, device=dev)).cpu().numpy()
+        assert np.array_equal(w, O.bisect(d, e))
+
+
+def test_bisection_full_size_cfg5(handle, torch):
+    d, e = W.make("cfg5")
+    dev = torch.device("cuda:0")
+    w = handle.eigvals(torch.tensor(d, device=dev), torch.tensor(e, device=dev)).cpu().numpy()
+    assert np.all(np.diff(w) >= 0)
+    # sampled indices: the oracle's Sturm count brackets each w_k within a few ulps
+    tn = O.tnorm(d, e)
+    for k in (0, 1, 777, 8000, 15998, 15999):
+        dx = 8 * np.spacing(max(abs(w[k]), tn * 1e-300))
+        assert O.sturm_count(d, e, w[k] - dx, tn) <= k < O.sturm_count(d, e, w[k] + dx, tn)
+
+
+def test_eig_end_to_end(handle, torch):
+    """T -> (w, Z) entirely on the device: eigenvalues by bisection then DSTEIN-cWY."""
+    d, e = W.make("cfg2", 700)
+    dev = torch.device("cuda:0")
+    w, Z, rc = handle.eig(torch.tensor(d, device=dev), torch.tensor(e, device=dev))
+    torch.cuda.synchronize()
+    assert rc == 0
+    wh = w.cpu().numpy()
+    assert np.array_equal(wh, O.bisect(d, e))
+    res, orth = invariants_gpu(torch, d, e, wh, Z)
+    assert res <= 10.0 and orth <= 10.0
+    Zo, info = O.eigvecs(d, e, wh, seed=1)
+    wv, ws, _, _ = parity_report(wh, O.tnorm(d, e), Z.cpu().numpy(), Zo)
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
