@@ -587,7 +587,7 @@ __device__ void cta_solve(const CwyArgs& a, const GroupWS& ws, int64_t j, int mo
 // so a CTA's rows [i0, i1) are one contiguous span.  Passes A, BC and D stream it through a
 // kNStg-deep shared-memory ring of TMA bulk copies (stage = RPS whole rows + the matching
 // coefficient rows x_i), one mbarrier per slot; thread 0 issues, all threads consume.
-constexpr int SBD = 4096;                    // Y doubles per stage (32 KB)
+constexpr int SBD = 3584;                    // Y doubles per stage (28 KB)
 constexpr int kMaxRPS = 512;                 // rows per stage cap (coefficient slots)
 constexpr int SXD = kMaxRPS + 4;             // coefficient doubles per stage
 constexpr int kStgD = SBD + SXD;             // doubles per ring slot
@@ -603,11 +603,18 @@ struct Ring {
 // Stream rows [i0, i1) of Y (and coef[i0, i1) if coef != nullptr) through the ring; for each
 // stage call body(ra, rb, Ys, Xs) with Ys = the stage's rows (row i at Ys + (i - ra) m2) and
 // Xs = coefficients (x_i at Xs[i - ra]).  All threads call; body may __syncthreads.
-template <class Body>
+// Threads [T0, T0 + TN) run the stream (TN < NT: the look-ahead on warps 1.. while warp 0
+// runs the chained back sweep; stage barriers are then named barrier 2 over those warps).
+template <int T0, int TN>
+__device__ __forceinline__ void sub_sync() {
+    if (TN == NT) __syncthreads();
+    else asm volatile("bar.sync 2, %0;" ::"n"(TN) : "memory");
+}
+template <int T0 = 0, int TN = NT, class Body>
 __device__ void narrow_stream(const Ring& rg, const double* Y, int m2, int i0, int i1, const double* coef,
                               Body body) {
     if (i1 <= i0) return;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x - T0;
     const int RPS = min(kMaxRPS, SBD / m2);
     const int nst = (i1 - i0 + RPS - 1) / RPS;
     int ps = 0;   // stages issued (thread 0)
@@ -638,7 +645,7 @@ __device__ void narrow_stream(const Ring& rg, const double* Y, int m2, int i0, i
         double* Xs = const_cast<double*>(Ys) + SBD + (ra & 1);
         body(ra, rb, Ys, Xs);       // (a body that writes the slot fences the async proxy itself)
         const uint64_t c2 = rg.tacc ? gtime() : 0;
-        __syncthreads();            // slot free
+        sub_sync<T0, TN>();         // slot free
         if (tid == 0 && ps < nst) issue();
         if (rg.tacc) {
             rg.tacc[0] += c1 - c0;
@@ -671,10 +678,11 @@ __device__ __forceinline__ void narrow_rowdots(int ra, int rb, int m2, const dou
 
 // Column accumulate over a stage: thread (cp, rs) adds Y[i][2cp..2cp+1] * c_i for the stage's
 // rows i with (i - ra) % RS == rs into (a0, a1); columns k < len(i) only.
-template <class Len>
+template <int T0 = 0, int TN = NT, class Len>
 __device__ __forceinline__ void narrow_colacc(int ra, int rb, int m2, const double* Ys, const double* Xs, int CPT,
                                               Len len, double& a0, double& a1) {
-    const int RS = NT / CPT, cp = threadIdx.x % CPT, rs = threadIdx.x / CPT;
+    const int t = threadIdx.x - T0;
+    const int RS = TN / CPT, cp = t % CPT, rs = t / CPT;
     const int k = 2 * cp;
     constexpr int U = 4;
     for (int ib = ra + rs; ib < rb; ib += RS * U) {
@@ -697,12 +705,13 @@ __device__ __forceinline__ void narrow_colacc(int ra, int rb, int m2, const doub
 }
 
 // Fixed-order reduction of the row-slice column accumulators; writes out[k] for k < P.
+template <int T0 = 0, int TN = NT>
 __device__ __forceinline__ void narrow_colacc_finish(const Smem& sm, int CPT, int64_t P, double a0, double a1,
                                                      double* out) {
-    const int tid = threadIdx.x, RS = NT / CPT, cp = tid % CPT, rs = tid / CPT;
-    __syncthreads();
+    const int tid = threadIdx.x - T0, RS = TN / CPT, cp = tid % CPT, rs = tid / CPT;
+    sub_sync<T0, TN>();
     sm.acc[tid] = make_double2(a0, a1);
-    __syncthreads();
+    sub_sync<T0, TN>();
     if (rs == 0) {
         for (int q = 1; q < RS; q++) {
             const double2 t = sm.acc[cp + q * CPT];
@@ -713,7 +722,7 @@ __device__ __forceinline__ void narrow_colacc_finish(const Smem& sm, int CPT, in
         if (k < P) st(out + k, a0);
         if (k + 1 < P) st(out + k + 1, a1);
     }
-    __syncthreads();
+    sub_sync<T0, TN>();
 }
 
 // ---------------------------------------------------------------- TMA streaming, wide passes
@@ -739,7 +748,7 @@ constexpr int kPfAhead = 0;              // wide stages prefetched into L2 beyon
                                          // the ring's own bulk copies)
 constexpr int64_t kRingD = (int64_t)kWStg * kWStgD > (int64_t)kNStg * kStgD ? (int64_t)kWStg * kWStgD
                                                                             : (int64_t)kNStg * kStgD;
-static_assert(kSolveDoubles <= kRingD, "back-sweep ring aliases the pass ring");
+static_assert((int64_t)kNStg * kStgD + kSolveDoubles <= kRingD, "back-sweep ring after the narrow ring");
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
 
@@ -1097,7 +1106,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     sm.vbar = wempty + kWStg;
     sm.vuse = reinterpret_cast<uint32_t*>(sm.vbar + 2);
     double* ring_base = reinterpret_cast<double*>(sm.mbar + kNBar);   // 16-B aligned (see cwy_smem_bytes)
-    sm.bring = ring_base;   // the back-sweep ring aliases the pass ring (never in use together)
+    // the back-sweep ring sits after the narrow ring (the single-CTA look-ahead streams the
+    // narrow ring while the back sweep runs) and aliases the wide ring (never in use together)
+    sm.bring = ring_base + (int64_t)kNStg * kStgD;
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing + kNStg; k++) mbar_init(sm.mbar + k, 1);
         for (int k = 0; k < kWStg; k++) {
@@ -1162,6 +1173,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         const int64_t m = a.cstart[cl + 1] - j1;
         const int64_t m2 = (m + 1) & ~int64_t(1);
         const bool narrow = (m <= kNarrowM) && a.nstg > 0;
+        const bool la_ok = (G > 1) || narrow;   // look-ahead can overlap the back sweep
         double* __restrict__ Tc = ws.Tc;
         double* __restrict__ Tr = ws.Tr;
 
@@ -1430,13 +1442,12 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     }
                     // y_p^T x^(1)_{p+1}: the last column of the next vector's first pass A
                     double gpn = 0.0;
-                    if (p + 1 < m && G > 1) {
-                        const double* xn = a.X1c + (j + 1) * n2v;
+                    const bool want_gpn = (p + 1 < m) && la_ok;
+                    const double* xn = a.X1c + (j + 1) * n2v;
+                    if (want_gpn && !narrow) {   // (narrow: fused into the D stream below)
                         for (int64_t i = (i0 > p ? i0 : p) + tid; i < i1; i += NT)
                             gpn = fma(ld(Y + y_row_off(i, m) + p), ld(xn + i), gpn);
                     }
-                    gpn = block_sum<NT>(gpn, sm.red);
-                    if (tid == 0) st(S + r * SST + SSlots::GPN, gpn);
                     auto epiq = [&](int64_t i, double v) {
                         const double qi = (i == p) ? v - 1.0 : v;
                         st(ws.q + i, qi);
@@ -1449,8 +1460,14 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     if (narrow) {
                         stage_vec(sm, ws.xp, p + 1);
                         auto lendn = [&](int i) -> int { return (i + 1 < p + 1) ? i + 1 : (int)p + 1; };
-                        narrow_stream(rg, Y, (int)m2, (int)i0, (int)i1, nullptr, [&](int ra, int rb, const double* Ys, double*) {
-                            narrow_rowdots(ra, rb, (int)m2, Ys, sm.vs, lendn, epiq);
+                        // with the look-ahead, the next vector's x^(1) rides along as the stage's
+                        // coefficient rows: y_p^T x^(1)_{p+1} from the same stage data
+                        narrow_stream(rg, Y, (int)m2, (int)i0, (int)i1, want_gpn ? xn : nullptr,
+                                      [&](int ra, int rb, const double* Ys, double* Xs) {
+                            narrow_rowdots(ra, rb, (int)m2, Ys, sm.vs, lendn, [&](int i, double v) {
+                                epiq(i, v);
+                                if (want_gpn && i >= p) gpn = fma(Ys[(i - ra) * m2 + p], Xs[i - ra], gpn);
+                            });
                         });
                     } else if (p + 1 > kNarrowM) {
                         wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p + 1}, (int)i0, (int)i1, ws.xp, nullptr, p + 1,
@@ -1459,6 +1476,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         stage_vec(sm, ws.xp, p + 1);
                         rowdots(i0, i1, p + 1, sm.vs, [&](int64_t i) { return Y + y_row_off(i, m); }, lend, epiq);
                     }
+                    gpn = block_sum<NT>(gpn, sm.red);
+                    if (tid == 0) st(S + r * SST + SSlots::GPN, gpn);
                     q2 = block_sum<NT>(q2, sm.red);
                     q1 = block_sum<NT>(q1, sm.red);
                     // block argmax (lowest index on ties)
@@ -1545,8 +1564,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     its++;
                     kin++;
                     PH(8);
-                    // look-ahead only when other CTAs can overlap it with the solve
-                    const bool la = !la_done && p + 1 < m && G > 1;
+                    // look-ahead only when it can overlap the back sweep (other CTAs of the
+                    // group, or warps 1.. of a single-CTA narrow group)
+                    const bool la = !la_done && p + 1 < m && la_ok;
                     if (r == 0) {
                         if (la) {   // CTA 0 solves; its look-ahead partial is zero when G > 1
                             for (int64_t k = tid; k < p; k += NT) st(ws.P2 + k, 0.0);
@@ -1590,9 +1610,38 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     }
                     gsync();
                     PH(9);
-                    if (r == 0 && tid == 0) back_sweep(a, ws, j, sm, mbph);
+                    if (G == 1 && la) {
+                        // single-CTA narrow group: warps 1..NW-1 stream the look-ahead pass A
+                        // of vector p+1 while lane 0 of warp 0 runs the chained back sweep
+                        if (tid == 0) back_sweep(a, ws, j, sm, mbph);
+                        if (tid >= 32) {
+                            constexpr int LT = NT - 32;
+                            const int CPT = pow2ceil((int)((p + 1) / 2));
+                            double a0 = 0.0, a1 = 0.0, x2n = 0.0;
+                            narrow_stream<32, LT>(rg, Y, (int)m2, 0, (int)n, a.X1c + (j + 1) * n2v,
+                                                  [&](int ra, int rb, const double* Ys, double* Xs) {
+                                for (int ii = tid - 32; ii < rb - ra; ii += LT) x2n = fma(Xs[ii], Xs[ii], x2n);
+                                narrow_colacc<32, LT>(ra, rb, (int)m2, Ys, Xs, CPT,
+                                                      [&](int i) -> int { return i + 1 < p ? i + 1 : (int)p; }, a0, a1);
+                            });
+                            narrow_colacc_finish<32, LT>(sm, CPT, p, a0, a1, ws.P2);
+                            x2n = warp_sum(x2n);
+                            if ((tid & 31) == 0) sm.red[tid >> 5] = x2n;
+                            sub_sync<32, LT>();
+                            if (tid == 32) {
+                                double t = 0.0;
+                                for (int w = 1; w < NW; w++) t += sm.red[w];
+                                st(S + SSlots::X2N, t);
+                                *reinterpret_cast<uint32_t*>(sm.red + NW + 7) = rph;
+                            }
+                        }
+                        __syncthreads();
+                        rph = *reinterpret_cast<volatile uint32_t*>(sm.red + NW + 7);
+                    } else if (r == 0 && tid == 0) {
+                        back_sweep(a, ws, j, sm, mbph);
+                    }
                     mark(10);
-                    if (la && r > 0) {
+                    if (la && r > 0) {   // G > 1: the other CTAs of the group
                         // look-ahead: Y_{p}^T x^(1)_{p+1} over the accepted columns 0..p-1,
                         // overlapped with the chained solve (PAPER.md:534-535 for vector j+1)
                         const int Gl = (G > 1) ? G - 1 : 1, rl = (G > 1) ? r - 1 : 0;
