@@ -138,6 +138,14 @@ typedef struct {
 } tinv_stats_t;
 
 int tinv_set_profiling(tinv_t h, int enable);
+
+/* Testing aid for the multi-GPU row split on a single device: when the
+ * clustered work of a tinv_eigvecs call is one cluster of more than 64 vectors, split it over
+ * `nranks` virtual ranks -- groups of CTAs of the one launch, each with its own replica of
+ * the workspace, exchanging through mirrored stores, partial sums read from their owner's
+ * replica and the rank-replicated barrier, exactly as real ranks do over NVLink.  1 (the
+ * default) disables it.  Returns 0, -2 for nranks outside [1, 16], TINV_ERR_HANDLE. */
+int tinv_set_virtual_ranks(tinv_t h, int nranks);
 int tinv_get_stats(tinv_t h, tinv_stats_t* out);
 
 /* Number of exported entry points (for the loader test). */

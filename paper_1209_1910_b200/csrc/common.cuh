@@ -75,6 +75,31 @@ struct GroupBarrier {
     unsigned int pad;
 };
 
+// Barrier of a group whose CTAs live on nrk ranks (rank-replicated counters at bar + delta[k]
+// doubles): every CTA adds 1 to every rank's counter (system-scope atomics: the replicas may
+// be peer memory over NVLink), then polls its own rank's counter until all Gt CTAs of the
+// episode arrived.  System-scope fences order the mirrored stores of all ranks.
+__device__ __forceinline__ void group_sync_ranks(GroupBarrier* b, const int64_t* delta, int nrk, int Gt,
+                                                 unsigned int& epoch) {
+    __threadfence_system();   // this thread's mirrored (possibly remote) stores
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        epoch++;
+        const unsigned int target = epoch * (unsigned int)Gt;
+        for (int k = 0; k < nrk; k++) {
+            unsigned int* c = reinterpret_cast<unsigned int*>(reinterpret_cast<double*>(&b->count) + delta[k]);
+            atomicAdd_system(c, 1u);
+        }
+        volatile unsigned int* vc = &b->count;
+        uint32_t spins = 0;
+        while ((int)(*vc - target) < 0) {
+            if (++spins > (1u << 30)) __trap();
+        }
+        __threadfence_system();
+    }
+    __syncthreads();
+}
+
 // `epoch` is the caller's episode counter (identical in every CTA of the group): arrive with
 // one atomic, then poll until all G CTAs of this episode have arrived.  The gpu-scope fences
 // give the release/acquire ordering (and invalidate L1) so data written by any CTA before the

@@ -315,9 +315,15 @@ __device__ __forceinline__ void reduce_argmax(const Smem& sm, const double* S, i
 }
 // out[k] = sum_{t<G} P[t*mc + k] for k in [k0, k1): threads split (k, t-group); the
 // t-groups are combined in a fixed order (deterministic).
+// Slot t of a rank-split group lives in the replica of rank t / Gl (delta in doubles).
+struct Ranks {
+    int nrk, Gl;
+    const int64_t* delta;
+    __device__ __forceinline__ int64_t off(int t) const { return nrk == 1 ? 0 : __ldg(delta + t / Gl); }
+};
 template <class Post>
 __device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P, int64_t mc, int G, int64_t k0,
-                                                int64_t k1, Post post) {
+                                                int64_t k1, Post post, const Ranks& rks = Ranks{1, 1, nullptr}) {
     const int tid = threadIdx.x;
     for (int64_t kb = k0; kb < k1; kb += NT) {
         const int64_t K = (k1 - kb < NT) ? (k1 - kb) : NT;
@@ -328,12 +334,13 @@ __device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P,
         if (tg < TG && kk < K) {
             const double* col = P + kb + kk;
             int t = tg;
+            auto at = [&](int u) { return col + (int64_t)u * mc + rks.off(u); };
             for (; t + 3 * TG < G; t += 4 * TG) {
-                const double v0 = ld(col + (int64_t)t * mc), v1 = ld(col + (int64_t)(t + TG) * mc);
-                const double v2 = ld(col + (int64_t)(t + 2 * TG) * mc), v3 = ld(col + (int64_t)(t + 3 * TG) * mc);
+                const double v0 = ld(at(t)), v1 = ld(at(t + TG));
+                const double v2 = ld(at(t + 2 * TG)), v3 = ld(at(t + 3 * TG));
                 acc += v0; acc += v1; acc += v2; acc += v3;
             }
-            for (; t < G; t += TG) acc += ld(col + (int64_t)t * mc);
+            for (; t < G; t += TG) acc += ld(at(t));
         }
         if (TG > 1) {
             __syncthreads();
@@ -1136,9 +1143,25 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     const int G = a.g_size[g];
     if (r >= G) return;  // CTA not used by any group
     const GroupWS ws = a.ws[g];
+    // row split over ranks: this CTA is cg of Gt = nrk G CTAs; work split
+    // over the group uses (cg, Gt), replicated local work uses (r, G)
+    const int NR = ws.nrk, RK = ws.rk;
+    const int Gt = NR * G, cg = RK * G + r;
+    const Ranks rks{NR, G, ws.delta};
+    const bool own_out = !(ws.vrt && RK != 0);   // virtual ranks share the caller's outputs
     long long nsync = 0;
     unsigned int bar_epoch = 0;
-    auto gsync = [&]() { group_sync(ws.bar, G, bar_epoch); nsync++; };
+    auto gsync = [&]() {
+        if (NR == 1) group_sync(ws.bar, G, bar_epoch);
+        else group_sync_ranks(ws.bar, ws.delta, NR, Gt, bar_epoch);
+        nsync++;
+    };
+    // mirrored store: every rank's replica of the group workspace
+    auto mst = [&](double* ptr, double v) {
+        if (NR == 1) st(ptr, v);
+        else
+            for (int k = 0; k < NR; k++) st(ptr + __ldg(ws.delta + k), v);
+    };
     // optional phase timers (thread 0 of each group's first CTA; globaltimer ns)
     const bool timing = (a.prof != nullptr) && r == 0 && tid == 0;
     uint64_t tacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -1189,9 +1212,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 u2 = fma(zi, zi, u2);
             }
             u2 = block_sum<NT>(u2, sm.red);
-            if (tid == 0) st(S + r * SST + SSlots::U2, u2);
+            if (tid == 0) st(S + cg * SST + SSlots::U2, u2);   // this rank's slots only (replicated work)
             gsync();
-            const double un = sqrt(reduce_slot(sm, S, G, SSlots::U2));
+            const double un = sqrt(reduce_slot(sm, S + RK * G * SST, G, SSlots::U2));
             const double u0 = ld(ws.u);
             const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
             const double tt = 1.0 / (c * c - u0 * c);
@@ -1218,7 +1241,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     // ---------------- A: partial g = Y_p^T x, ||x||^2
                     {
                         int64_t i0, i1;
-                        part_rows_weighted(n, p, r, G, i0, i1);
+                        part_rows_weighted(n, p, cg, Gt, i0, i1);
                         double x2 = 0.0;
                         if (narrow) {
                             const int CPT = pow2ceil((int)((p + 1) / 2));
@@ -1227,14 +1250,14 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                 for (int ii = tid; ii < rb - ra; ii += NT) x2 = fma(Xs[ii], Xs[ii], x2);
                                 narrow_colacc(ra, rb, (int)m2, Ys, Xs, CPT, [&](int i) -> int { return i + 1 < p ? i + 1 : (int)p; }, a0, a1);
                             });
-                            narrow_colacc_finish(sm, CPT, p, a0, a1, P_ + (int64_t)r * mc);
+                            narrow_colacc_finish(sm, CPT, p, a0, a1, P_ + (int64_t)cg * mc);
                         } else if (p > kNarrowM) {
-                            x2 = wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, xcur, p, P_ + (int64_t)r * mc, false);
+                            x2 = wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, xcur, p, P_ + (int64_t)cg * mc, false);
                         } else {
-                            x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)r * mc);
+                            x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)cg * mc);
                         }
                         x2 = block_sum<NT>(x2, sm.red);
-                        if (tid == 0) st(S + r * SST + SSlots::X2, x2);
+                        if (tid == 0) mst(S + cg * SST + SSlots::X2, x2);
                     }
                     gsync();
                     PH(1);
@@ -1245,13 +1268,13 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t k0, k1;
                     if (use_la) {
-                        part_uniform(0, p - 1, r, G, k0, k1);
-                        reduce_partials(sm, ws.P2, mc, G, k0, k1, [&](int64_t k, double v) { st(ws.g + k, v); });
-                        const double gl = reduce_slot(sm, S, G, SSlots::GPN);
-                        if (r == 0 && tid == 0) st(ws.g + p - 1, gl);
+                        part_uniform(0, p - 1, cg, Gt, k0, k1);
+                        reduce_partials(sm, ws.P2, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
+                        const double gl = reduce_slot(sm, S, Gt, SSlots::GPN);
+                        if (r == 0 && tid == 0) st(ws.g + p - 1, gl);   // every rank, its own replica
                     } else {
-                        part_uniform(0, p, r, G, k0, k1);
-                        reduce_partials(sm, P_, mc, G, k0, k1, [&](int64_t k, double v) { st(ws.g + k, v); });
+                        part_uniform(0, p, cg, Gt, k0, k1);
+                        reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
                     }
                 }
                 gsync();
@@ -1259,16 +1282,16 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // ---------------- TT: g' = T_p^T g
                 {
                     int64_t k0, k1;
-                    part_tt(p, r, G, k0, k1);
+                    part_tt(p, cg, Gt, k0, k1);
                     if (p > kNarrowM) {
                         wide_rowdots<false>(sm, wr, SrcTc{Tc, (int)p}, (int)k0, (int)k1, ws.g, nullptr, p,
-                                            [&](int64_t k, double v, double) { st(ws.gp + k, v); });
+                                            [&](int64_t k, double v, double) { mst(ws.gp + k, v); });
                     } else if (k1 > k0) {
                         stage_vec(sm, ws.g, p);
                         rowdots(k0, k1, p, sm.vs,
                                 [&](int64_t k) { return Tc + tcol_off(k); },
                                 [&](int64_t k) -> int64_t { return k + 1; },
-                                [&](int64_t k, double v) { st(ws.gp + k, v); });
+                                [&](int64_t k, double v) { mst(ws.gp + k, v); });
                     }
                 }
                 gsync();
@@ -1276,7 +1299,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // ---------------- BC: u^ = x^ - Yhat g' (rows p..n-1), s' partials, ||u^||^2
                 {
                     int64_t i0, i1;
-                    part_uniform(p, n, r, G, i0, i1);
+                    part_uniform(p, n, cg, Gt, i0, i1);
                     double u2 = 0.0;
                     if (narrow) {
                         // one read of Yhat per stage: row dots -> uhat (into the stage's
@@ -1289,27 +1312,27 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                             narrow_rowdots(ra, rb, (int)m2, Ys, sm.vs, lenp, [&](int i, double v) {
                                 const double ui = Xs[i - ra] - v;
                                 Xs[i - ra] = ui;
-                                st(ws.u + i, ui);
+                                mst(ws.u + i, ui);
                                 u2 = fma(ui, ui, u2);
                             });
                             __syncthreads();
                             narrow_colacc(ra, rb, (int)m2, Ys, Xs, LPR, lenp, a0, a1);
                             fence_proxy_async_smem();   // uhat written into the slot before its next bulk fill
                         });
-                        narrow_colacc_finish(sm, LPR, p, a0, a1, P_ + (int64_t)r * mc);
+                        narrow_colacc_finish(sm, LPR, p, a0, a1, P_ + (int64_t)cg * mc);
                         u2 = block_sum<NT>(u2, sm.red);
-                        if (tid == 0) st(S + r * SST + SSlots::U2, u2);
+                        if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
                     } else if (p > kNarrowM) {
                         wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.gp, nullptr, p,
                                             [&](int64_t i, double v, double) {
                                                 const double ui = ld(xcur + i) - v;
-                                                st(ws.u + i, ui);
+                                                mst(ws.u + i, ui);
                                                 u2 = fma(ui, ui, u2);
                                             });
                         u2 = block_sum<NT>(u2, sm.red);
-                        if (tid == 0) st(S + r * SST + SSlots::U2, u2);
+                        if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
                         // second read of Yhat, blocks in reverse order (the last ones are in L2)
-                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)r * mc, true);
+                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)cg * mc, true);
                     } else {
                         stage_vec(sm, ws.gp, p);
                         rowdots(i0, i1, p, sm.vs,
@@ -1317,19 +1340,19 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                 [&](int64_t i) -> int64_t { return p; },
                                 [&](int64_t i, double v) {
                                     const double ui = ld(xcur + i * xs) - v;
-                                    st(ws.u + i, ui);
+                                    mst(ws.u + i, ui);
                                     u2 = fma(ui, ui, u2);
                                 });
                         u2 = block_sum<NT>(u2, sm.red);
-                        if (tid == 0) st(S + r * SST + SSlots::U2, u2);
-                        colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)r * mc);
+                        if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
+                        colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)cg * mc);
                     }
                 }
                 gsync();
                 PH(4);
                 // ---------------- R2: scalars (every CTA, identical), s = s' - c Y[p,:]
-                double un = sqrt(reduce_slot(sm, S, G, SSlots::U2));
-                const double x2 = reduce_slot(sm, S, G, use_la ? SSlots::X2N : SSlots::X2);
+                double un = sqrt(reduce_slot(sm, S, Gt, SSlots::U2));
+                const double x2 = reduce_slot(sm, S, Gt, use_la ? SSlots::X2N : SSlots::X2);
                 use_la = false;
                 double u0 = ld(ws.u + p);
                 const bool zero_u = (un == 0.0);   // reading: exactly-zero uhat -> e_1
@@ -1354,12 +1377,12 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 const double* yrow = Y + y_row_off(p, m);
                 {
                     int64_t k0, k1;
-                    part_uniform(0, p, r, G, k0, k1);
+                    part_uniform(0, p, cg, Gt, k0, k1);
                     if (zero_u) {
-                        for (int64_t k = k0 + tid; k < k1; k += NT) st(ws.s + k, ld(yrow + k) - c * ld(yrow + k));
+                        for (int64_t k = k0 + tid; k < k1; k += NT) mst(ws.s + k, ld(yrow + k) - c * ld(yrow + k));
                     } else {
-                        reduce_partials(sm, P_, mc, G, k0, k1,
-                                        [&](int64_t k, double v) { st(ws.s + k, v - c * ld(yrow + k)); });
+                        reduce_partials(sm, P_, mc, Gt, k0, k1,
+                                        [&](int64_t k, double v) { mst(ws.s + k, v - c * ld(yrow + k)); }, rks);
                     }
                 }
                 gsync();
@@ -1367,14 +1390,14 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // ---------------- TN: [Ts, h] = T_p [s, yrow]; column p of T and Y; x'
                 {
                     int64_t l0, l1;
-                    part_tn(p, r, G, l0, l1);
+                    part_tn(p, cg, Gt, l0, l1);
                     if (p > kNarrowM) {
                         wide_rowdots<true>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, yrow, p,
                                            [&](int64_t l, double a1, double a2) {
                                                const double that = -tt * a1;
-                                               st(ws.xp + l, a2 + y0 * that);
-                                               st(Tc + tcol_off(p) + l, that);
-                                               st(Tr + l * m2 + p, that);
+                                               mst(ws.xp + l, a2 + y0 * that);
+                                               mst(Tc + tcol_off(p) + l, that);
+                                               mst(Tr + l * m2 + p, that);
                                            });
                     } else if (l1 > l0) {
                         stage_vec(sm, ws.s, p);
@@ -1409,9 +1432,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                             a2 = warp_sum(a2);
                             if (lane == 0) {
                                 const double that = -tt * a1;
-                                st(ws.xp + l, a2 + y0 * that);
-                                st(Tc + tcol_off(p) + l, that);
-                                st(Tr + l * m2 + p, that);
+                                mst(ws.xp + l, a2 + y0 * that);
+                                mst(Tc + tcol_off(p) + l, that);
+                                mst(Tr + l * m2 + p, that);
                             }
                         }
                     }
@@ -1433,7 +1456,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 bool flast = false;
                 {
                     int64_t i0, i1;
-                    part_rows_weighted(n, p + 1, r, G, i0, i1);
+                    part_rows_weighted(n, p + 1, cg, Gt, i0, i1);
                     double q2 = 0.0, q1 = 0.0, qinf = -1.0;
                     int64_t qarg = 0;
                     if (tid == 0) {   // this CTA's factor rows (forward sweep below, back sweep)
@@ -1450,7 +1473,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     }
                     auto epiq = [&](int64_t i, double v) {
                         const double qi = (i == p) ? v - 1.0 : v;
-                        st(ws.q + i, qi);
+                        mst(ws.q + i, qi);
                         q2 = fma(qi, qi, q2);
                         const double aq = fabs(qi);
                         q1 += aq;
@@ -1477,7 +1500,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         rowdots(i0, i1, p + 1, sm.vs, [&](int64_t i) { return Y + y_row_off(i, m); }, lend, epiq);
                     }
                     gpn = block_sum<NT>(gpn, sm.red);
-                    if (tid == 0) st(S + r * SST + SSlots::GPN, gpn);
+                    if (tid == 0) mst(S + cg * SST + SSlots::GPN, gpn);
                     q2 = block_sum<NT>(q2, sm.red);
                     q1 = block_sum<NT>(q1, sm.red);
                     // block argmax (lowest index on ties)
@@ -1493,10 +1516,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                             double2 t = sm.acc[w];
                             if (t.x > qinf || (t.x == qinf && (int64_t)t.y < qarg)) { qinf = t.x; qarg = (int64_t)t.y; }
                         }
-                        st(S + r * SST + SSlots::Q2, q2);
-                        st(S + r * SST + SSlots::QINF, qinf);
-                        st(S + r * SST + SSlots::QARG, (double)qarg);
-                        st(S + r * SST + SSlots::Q1, q1);
+                        mst(S + cg * SST + SSlots::Q2, q2);
+                        mst(S + cg * SST + SSlots::QINF, qinf);
+                        mst(S + cg * SST + SSlots::QARG, (double)qarg);
+                        mst(S + cg * SST + SSlots::Q1, q1);
                     }
                     // forward sweep of the chained solve with rhs q, pass 1: steps s in
                     // [i0-1, i1-1) use q_{s+1} from this CTA's rows (reduced to one map per
@@ -1533,17 +1556,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     Aff1 tot;
                     fex = block_scan_excl(f, reinterpret_cast<Aff1*>(sm.acc), tot);
                     if (tid == 0) {
-                        st(S + r * SST + SSlots::FA, tot.a);
-                        st(S + r * SST + SSlots::FB, tot.b);
+                        mst(S + cg * SST + SSlots::FA, tot.a);
+                        mst(S + cg * SST + SSlots::FB, tot.b);
                     }
                 }
                 gsync();
                 PH(7);
                 // ---------------- TEST
-                const double q2 = reduce_slot(sm, S, G, SSlots::Q2);
+                const double q2 = reduce_slot(sm, S, Gt, SSlots::Q2);
                 double qinf;
                 int64_t qarg;
-                reduce_argmax(sm, S, G, qinf, qarg);
+                reduce_argmax(sm, S, Gt, qinf, qarg);
                 if (fabs(c) * qinf >= thr) passes++;
                 if (passes >= kPasses) done = true;
                 else if (kin >= kMaxIts) { done = true; flagged = true; }
@@ -1553,10 +1576,12 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     int64_t i0, i1;
                     part_uniform(0, n, r, G, i0, i1);
                     double* zj = a.Z + j * a.ldz;
-                    for (int64_t i = i0 + tid; i < i1; i += NT) zj[i] = ld(ws.q + i) * scl;
-                    if (r == 0 && tid == 0) {
-                        a.iters[j] = its;
-                        if (flagged) atomicAdd(&a.out->nflag, 1);
+                    if (own_out) {   // q is complete in every rank's replica: local rows, local Z
+                        for (int64_t i = i0 + tid; i < i1; i += NT) zj[i] = ld(ws.q + i) * scl;
+                        if (r == 0 && tid == 0) {
+                            a.iters[j] = its;
+                            if (flagged) atomicAdd(&a.out->nflag, 1);
+                        }
                     }
                     la_have = la_done;
                     PH(8);
@@ -1568,18 +1593,18 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     // group, or warps 1.. of a single-CTA narrow group)
                     const bool la = !la_done && p + 1 < m && la_ok;
                     if (r == 0) {
-                        if (la) {   // CTA 0 solves; its look-ahead partial is zero when G > 1
-                            for (int64_t k = tid; k < p; k += NT) st(ws.P2 + k, 0.0);
-                            if (tid == 0) st(S + SSlots::X2N, 0.0);
+                        if (la) {   // CTA 0 of every rank solves; its look-ahead partial is zero
+                            for (int64_t k = tid; k < p; k += NT) st(ws.P2 + (int64_t)cg * mc + k, 0.0);
+                            if (tid == 0) mst(S + cg * SST + SSlots::X2N, 0.0);
                         }
                     }
                     {   // forward sweep, pass 2: exact carries from the CTA maps -> t_s = sc y_s / u0_s
                         const double* Fj = a.F + j * n * 4;
                         const int8_t* FPj = a.FP + j * n;
-                        const Aff1 pre = compose_ctas(S, r, reinterpret_cast<Aff1*>(sm.acc));
+                        const Aff1 pre = compose_ctas(S, cg, reinterpret_cast<Aff1*>(sm.acc));
                         const double q0 = ld(ws.q);
                         double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
-                        const double q1 = reduce_slot(sm, S, G, SSlots::Q1);
+                        const double q1 = reduce_slot(sm, S, Gt, SSlots::Q1);
                         const double sc = (double)n * a.tnorm * fmax(kEps, ldro(a.unn + j)) / q1;
                         double* ts = ws.ysol;
                         for (int64_t s0 = fta; s0 < ftb; s0 += 8) {
@@ -1599,13 +1624,13 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                     double y;
                                     if (sw[u]) { y = bn[u]; cc = fma(-l[u], bn[u], cc); }
                                     else { y = cc; cc = fma(-l[u], cc, bn[u]); }
-                                    st(ts + s0 + u, sc * y * rr[u]);
+                                    mst(ts + s0 + u, sc * y * rr[u]);
                                 }
                             }
                         }
                         if (flast) {
-                            st(ts + n - 1, sc * cc * ldro(Fj + (n - 1) * 4 + 1));
-                            st(ts + n, 0.0);
+                            mst(ts + n - 1, sc * cc * ldro(Fj + (n - 1) * 4 + 1));
+                            mst(ts + n, 0.0);
                         }
                     }
                     gsync();
@@ -1644,15 +1669,16 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     if (la && r > 0) {   // G > 1: the other CTAs of the group
                         // look-ahead: Y_{p}^T x^(1)_{p+1} over the accepted columns 0..p-1,
                         // overlapped with the chained solve (PAPER.md:534-535 for vector j+1)
-                        const int Gl = (G > 1) ? G - 1 : 1, rl = (G > 1) ? r - 1 : 0;
+                        // (every rank's CTA 0 solves; the others split the rows over all ranks)
+                        const int Gl = Gt - NR, rl = RK * (G - 1) + (r - 1);
                         int64_t i0, i1;
                         part_rows_weighted(n, p, rl, Gl, i0, i1);
                         double x2n = (p > kNarrowM)
                                          ? wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, a.X1c + (j + 1) * n2v, p,
-                                                       ws.P2 + (int64_t)r * mc, false)
-                                         : colacc(sm, Y, m, i0, i1, p, a.X1c + (j + 1) * n2v, 1, ws.P2 + (int64_t)r * mc);
+                                                       ws.P2 + (int64_t)cg * mc, false)
+                                         : colacc(sm, Y, m, i0, i1, p, a.X1c + (j + 1) * n2v, 1, ws.P2 + (int64_t)cg * mc);
                         x2n = block_sum<NT>(x2n, sm.red);
-                        if (tid == 0) st(S + r * SST + SSlots::X2N, x2n);
+                        if (tid == 0) mst(S + cg * SST + SSlots::X2N, x2n);
                     }
                     if (la) la_done = true;
                     gsync();

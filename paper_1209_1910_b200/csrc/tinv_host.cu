@@ -37,6 +37,8 @@ struct Nccl {
     ncclResult_t (*broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*groupStart)() = nullptr;
     ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     bool load() {
         if (lib) return true;
         lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
@@ -47,11 +49,15 @@ struct Nccl {
         broadcast = (decltype(broadcast))dlsym(lib, "ncclBroadcast");
         groupStart = (decltype(groupStart))dlsym(lib, "ncclGroupStart");
         groupEnd = (decltype(groupEnd))dlsym(lib, "ncclGroupEnd");
-        return commInitRank && commDestroy && broadcast && groupStart && groupEnd;
+        allGather = (decltype(allGather))dlsym(lib, "ncclAllGather");
+        allReduce = (decltype(allReduce))dlsym(lib, "ncclAllReduce");
+        return commInitRank && commDestroy && broadcast && groupStart && groupEnd && allGather && allReduce;
     }
 };
 Nccl g_nccl;
 constexpr int ncclFloat64 = 8;
+constexpr int ncclUint8 = 1;
+constexpr int ncclSum = 0;
 
 }  // namespace
 
@@ -80,6 +86,11 @@ struct tinv_s {
     int* h_iters = nullptr;
     int64_t h_cap = 0;
     double* bnd = nullptr;            // bisection bounds (3 doubles)
+    int vranks = 1;                   // virtual ranks for the row split (testing on one device)
+    // row split over real ranks: peers' cWY workspaces mapped through CUDA IPC
+    std::vector<void*> peer_cw;       // per rank (nullptr for self)
+    std::vector<char> peer_hdl;       // the IPC handles the mappings were opened from
+    void* ipc_buf = nullptr;          // device staging for the handle allgather / barrier
     // pinned image of the cWY schedule header
     void* h_hdr = nullptr;
     size_t h_hdr_bytes = 0;
@@ -260,6 +271,36 @@ void ev_record(tinv_s* h, int k) {
     if (h->profiling) cudaEventRecord(h->ev[k], h->stream);
 }
 
+// Map every peer rank's cWY workspace (same layout as ours) into this process with CUDA IPC;
+// the 64-byte handles are exchanged with an NCCL allgather on every call (collective on all
+// ranks), and a mapping is reopened only when that peer's allocation changed.
+int map_peers(tinv_s* h, cudaStream_t st) {
+    if (h->peer_cw.size() != (size_t)h->nranks) {
+        h->peer_cw.assign(h->nranks, nullptr);
+        h->peer_hdl.assign(64 * (size_t)h->nranks, 0);
+    }
+    if (!h->ipc_buf) CK(cudaMalloc(&h->ipc_buf, 64 * (size_t)h->nranks + 64));
+    cudaIpcMemHandle_t mine;
+    CK(cudaIpcGetMemHandle(&mine, h->cw));
+    char* buf = (char*)h->ipc_buf;
+    CK(cudaMemcpyAsync(buf + 64 * h->rank, &mine, 64, cudaMemcpyHostToDevice, st));
+    if (g_nccl.allGather(buf + 64 * h->rank, buf, 64, ncclUint8, h->comm, st)) return TINV_ERR_NCCL;
+    std::vector<char> all(64 * (size_t)h->nranks);
+    CK(cudaMemcpyAsync(all.data(), buf, all.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int k = 0; k < h->nranks; k++) {
+        if (k == h->rank) continue;
+        if (h->peer_cw[k] && !memcmp(h->peer_hdl.data() + 64 * k, all.data() + 64 * k, 64)) continue;
+        if (h->peer_cw[k]) cudaIpcCloseMemHandle(h->peer_cw[k]);
+        h->peer_cw[k] = nullptr;
+        cudaIpcMemHandle_t hk;
+        memcpy(&hk, all.data() + 64 * k, 64);
+        CK(cudaIpcOpenMemHandle(&h->peer_cw[k], hk, cudaIpcMemLazyEnablePeerAccess));
+        memcpy(h->peer_hdl.data() + 64 * k, all.data() + 64 * k, 64);
+    }
+    return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -347,6 +388,8 @@ int tinv_destroy(tinv_t h) {
     if (h->cw) cudaFree(h->cw);
     if (h->io) cudaFree(h->io);
     if (h->bnd) cudaFree(h->bnd);
+    for (void* pp : h->peer_cw) if (pp) cudaIpcCloseMemHandle(pp);
+    if (h->ipc_buf) cudaFree(h->ipc_buf);
     if (h->h_out) cudaFreeHost(h->h_out);
     if (h->h_cstart) cudaFreeHost(h->h_cstart);
     if (h->h_iters) cudaFreeHost(h->h_iters);
@@ -355,6 +398,13 @@ int tinv_destroy(tinv_t h) {
     if (h->ev_prep) cudaEventDestroy(h->ev_prep);
     if (h->side) cudaStreamDestroy(h->side);
     delete h;
+    return 0;
+}
+
+int tinv_set_virtual_ranks(tinv_t h, int nranks) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (nranks < 1 || nranks > 16) return -2;
+    h->vranks = nranks;
     return 0;
 }
 
@@ -459,7 +509,36 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         return TINV_ERR_DEVICE;
     }
     const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
-    Schedule sc = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
+    // Row split: when the clustered work is one wide cluster (cfg4/cfg5), all
+    // ranks share it -- every rank keeps a replica of the group workspace, the rows of every
+    // pass are split over all ranks' CTAs, small results are mirrored into every replica and
+    // the per-CTA partial sums are read from their owner's replica.  Virtual ranks run the
+    // same scheme as groups of one launch on one device (tinv_set_virtual_ranks, tests).
+    int nbig = 0;
+    for (int c = 0; c < nclus; c++)
+        if (cs[c + 1] - cs[c] >= 2) nbig++;
+    const bool wide1 = nbig == 1 && po.max_cluster > cwy_narrow_max();
+    const bool rs_real = h->nranks > 1 && wide1;
+    const int NRK = rs_real ? h->nranks : ((h->nranks == 1 && h->vranks > 1 && wide1) ? h->vranks : 1);
+    const bool rs_virtual = !rs_real && NRK > 1;
+    Schedule sc = rs_real ? make_schedule(cs, 0, nclus, n, nctas_max)
+                          : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
+    if (rs_virtual && sc.size.size() == 1) {   // split the group into NRK equal virtual ranks
+        const int Gv = sc.size[0] / NRK;
+        const int cl = sc.clist[0];
+        const int64_t mc = sc.mcap[0];
+        sc = Schedule{};
+        sc.coff.push_back(0);
+        for (int k = 0; k < NRK; k++) {
+            sc.cta0.push_back(k * Gv);
+            sc.size.push_back(Gv);
+            sc.clist.push_back(cl);
+            sc.coff.push_back(k + 1);
+            sc.mcap.push_back(mc);
+        }
+        sc.nctas = NRK * Gv;
+    }
+    const int RG = (rs_real || rs_virtual) ? NRK : 1;   // ranks per group
     if (!sc.size.empty()) {
         const int ng = (int)sc.size.size();
         // workspace: schedule arrays + per-group buffers
@@ -478,12 +557,13 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             *syncs = c.take<long long>(ng);
             *dws = c.take<GroupWS>(ng);
             GroupBarrier* bars = c.take<GroupBarrier>(ng);
+            int64_t* dl = c.take<int64_t>((size_t)ng * RG);
             hdr_hi = c.off;
             ws.resize(ng);
             for (int g = 0; g < ng; g++) {
                 int64_t mc = sc.mcap[g];
                 int64_t m2 = (mc + 1) & ~int64_t(1);
-                int G = sc.size[g];
+                int G = sc.size[g] * RG;   // partial / scalar slots for the CTAs of all ranks
                 GroupWS& W = ws[g];
                 W.mcap = m2 + 2;
                 W.Y = c.take<double>(y_row_off(n, mc) + 2);
@@ -501,6 +581,17 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.P2 = c.take<double>((size_t)G * W.mcap);
                 W.S = c.take<double>((size_t)G * 16 + 16);
                 W.bar = bars + g;
+                W.nrk = 1;
+                W.rk = 0;
+                W.vrt = 0;
+                W.delta = nullptr;
+                if (RG > 1) {   // replicated layout: the barrier lives inside the replica
+                    W.bar = c.take<GroupBarrier>(2);
+                    W.nrk = RG;
+                    W.rk = rs_real ? h->rank : g;
+                    W.vrt = rs_virtual ? 1 : 0;
+                    W.delta = dl + (size_t)g * RG;
+                }
             }
             return c.off;
         };
@@ -539,7 +630,26 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             put(arrs[2], sc.coff.data(), sizeof(int) * (ng + 1));
             put(arrs[3], sc.clist.data(), sizeof(int) * sc.clist.size());
             put(dws, ws.data(), sizeof(GroupWS) * ng);
+            if (RG > 1) {
+                std::vector<int64_t> dv((size_t)ng * RG, 0);
+                if (rs_virtual) {
+                    for (int g = 0; g < ng; g++)
+                        for (int k = 0; k < RG; k++) dv[(size_t)g * RG + k] = ws[k].Y - ws[g].Y;
+                } else {
+                    if (int rc = map_peers(h, st)) return rc;
+                    for (int k = 0; k < RG; k++)
+                        dv[k] = (k == h->rank) ? 0 : ((char*)h->peer_cw[k] - (char*)h->cw) / 8;
+                }
+                put(ws[0].delta, dv.data(), sizeof(int64_t) * dv.size());
+            }
             CK(cudaMemcpyAsync(base + hdr_lo, img, hb, cudaMemcpyHostToDevice, st));
+            if (RG > 1) {
+                for (int g = 0; g < ng; g++) CK(cudaMemsetAsync(ws[g].bar, 0, 2 * sizeof(GroupBarrier), st));
+                if (rs_real) {   // every rank's counters are zero before any kernel adds to them
+                    if (g_nccl.allReduce(h->ipc_buf, h->ipc_buf, 1, ncclUint8, ncclSum, h->comm, st))
+                        return TINV_ERR_NCCL;
+                }
+            }
         }
         CwyArgs ca{};
         ca.n = n; ca.ldv = h->ldv; ca.d = d; ca.e = e; ca.tnorm = tnorm; ca.seed = seed;
@@ -570,7 +680,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     S.solve_bytes = 144.0 * (double)n * (double)n;  // factor 32n + 2 x 56n per vector
 
     // ---------------- multi-rank: broadcast each rank's cluster columns
-    if (h->nranks > 1) {
+    if (h->nranks > 1 && !rs_real) {
         if (g_nccl.groupStart()) return TINV_ERR_NCCL;
         for (int r = 0; r < h->nranks; r++) {
             int64_t c0 = cs[rlo[r]], c1 = cs[rhi[r]];
@@ -599,7 +709,8 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     // every iteration of a clustered vector runs one step.
     {
         double rb = 0.0;
-        for (int c = rlo[h->rank]; c < rhi[h->rank]; c++) {
+        const int c_lo = rs_real ? 0 : rlo[h->rank], c_hi = rs_real ? nclus : rhi[h->rank];
+        for (int c = c_lo; c < c_hi; c++) {
             for (int64_t j = cs[c] + 1; j < cs[c + 1]; j++) {
                 double p = (double)(j - cs[c]);
                 rb += (double)h->h_iters[j] * 8.0 * (4.0 * p * (double)n - 1.5 * p * p);

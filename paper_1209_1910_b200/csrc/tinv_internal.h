@@ -91,12 +91,21 @@ struct GroupWS {
     double* gp;         // T^T g               (mcap)
     double* s;          // Yhat^T yhat          (mcap)
     double* xp;         // T_{p+1} y_row        (mcap + 1)
-    double* P;          // partial sums [G][mcap]
-    double* S;          // scalar partials [G][8]
-    double* P2;         // look-ahead partial sums [G][mcap]
+    double* P;          // partial sums [Gt][mcap] (a rank writes only its own CTAs' slots)
+    double* S;          // scalar partials [Gt][16] (Gt = CTAs of the group over all ranks)
+    double* P2;         // look-ahead partial sums [Gt][mcap]
     double* ysol;       // forward-sweep workspace of the chained solve (n)
     GroupBarrier* bar;
     int64_t mcap;
+    // Row split of one cluster over `nrk` ranks: every rank holds a full
+    // replica of this workspace with the same layout; `delta[k]` (doubles) moves a pointer
+    // into this replica to the same place in rank k's replica (delta[rk] = 0).  nrk == 1:
+    // plain single-GPU group.  `vrt`: the ranks are virtual (groups of one launch on one
+    // device sharing the caller's outputs; only rank 0 writes them).
+    int nrk;
+    int rk;
+    int vrt;
+    const int64_t* delta;
 };
 
 struct CwyArgs {

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libtinv.so")
 
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",
-           "tinv_eigvals", "tinv_eig")
+           "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks")
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
 PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "st_wait", "st_body", "st_sync", "st_blkend")
@@ -80,6 +80,8 @@ def load_library(path: str = LIB_PATH):
     L.tinv_get_stats.argtypes = [P, C.POINTER(TinvStats)]
     L.tinv_get_stats.restype = C.c_int
     L.tinv_abi_version.argtypes = []
+    L.tinv_set_virtual_ranks.restype = C.c_int
+    L.tinv_set_virtual_ranks.argtypes = [P, C.c_int]
     L.tinv_eigvals.restype = C.c_int
     L.tinv_eigvals.argtypes = [P, I64, P, P, P]
     L.tinv_eig.restype = C.c_int
@@ -158,6 +160,11 @@ class Tinv:
         if rc < 0 and check:
             raise TinvError(f"tinv_eigvecs failed: {rc} ({strerror(rc)})")
         return Zt.t(), rc
+
+    def set_virtual_ranks(self, nranks: int):
+        rc = self._L.tinv_set_virtual_ranks(self._h, int(nranks))
+        if rc:
+            raise TinvError(f"tinv_set_virtual_ranks failed: {rc}")
 
     def eigvals(self, d, e, check: bool = True):
         """Device path: eigenvalues of T (Sturm bisection, tinv_eigvals); d, e float64 CUDA
