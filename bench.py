@@ -249,8 +249,16 @@ def main():
     else:
         alg_bytes = st["solve_bytes"]
     achieved = alg_bytes / (avg[dom] * 1e-3) / 1e9 if avg.get(dom, 0) > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(args.config)
+        if tr and tr.get("kernel") == dom:
+            traffic = float(tr["bytes"])
+    except Exception:
+        traffic = None
     roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": src,
+            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": src,
             "alg_bytes_per_launch": alg_bytes, "kernel_ms": avg[dom],
             "share_of_step": avg[dom] / ms_per_step if ms_per_step > 0 else None}
 
@@ -272,12 +280,16 @@ def main():
     e2e = {"value": n / (e_ms * 1e-3), "unit": "eigenvectors/s", "ms_per_step": e_ms,
            "h2d_bytes_per_step": 8 * (3 * n - 1), "d2h_bytes_per_step": 8 * n * n}
 
+    # one wide cluster holds all the clustered vectors -> the library row-splits it over the
+    # ranks; otherwise clusters are sharded by columns
+    row_split = st["max_cluster"] > 64 and st["n_clustered"] == st["max_cluster"] - 1
+    parallelism = "single GPU" if ws == 1 else (f"row-split x{ws}" if row_split else f"cluster-shard x{ws}")
     line = {
         "metric": "eigenvectors/s (all n, fp64)", "value": value, "unit": "eigenvectors/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC[args.config], "name": args.config, "n": n,
-                   "parallelism": f"cluster-shard x{ws}" if ws > 1 else "single GPU",
+                   "parallelism": parallelism,
                    "l2": "flushed between timed steps (256 MB write)", "seed": args.seed},
         "roofline": roof,
         "e2e": e2e,
