@@ -125,6 +125,7 @@ typedef struct {
     int64_t group_syncs;        /* group barrier episodes in the cWY kernel (per group max) */
     int64_t ngroups;            /* CTA groups used by the cWY kernel                  */
     int64_t cwy_ctas;           /* CTAs of the cWY kernel                             */
+    int64_t resident_groups;    /* launches of the resident (DSMEM) cWY kernel        */
     double  reorth_bytes;       /* algorithmic bytes of the cWY passes    */
     double  solve_bytes;        /* algorithmic bytes of the batched LU kernel         */
     double  kernel_ms[TINV_NKERNELS];     /* prep, batched_lu, finalize, cwy, misc, total */
@@ -146,6 +147,12 @@ int tinv_set_profiling(tinv_t h, int enable);
  * replica and the rank-replicated barrier, exactly as real ranks do over NVLink.  1 (the
  * default) disables it.  Returns 0, -2 for nranks outside [1, 16], TINV_ERR_HANDLE. */
 int tinv_set_virtual_ranks(tinv_t h, int nranks);
+
+/* Narrow clusters (m <= 64, n <= 4096) normally run in the resident kernel (one thread-block
+ * cluster per eigen-cluster, Y kept in distributed shared memory); enable = 0 routes them
+ * through the streaming persistent kernel instead (same results up to rounding; used to
+ * compare the two paths).  Returns 0 or TINV_ERR_HANDLE. */
+int tinv_set_resident(tinv_t h, int enable);
 int tinv_get_stats(tinv_t h, tinv_stats_t* out);
 
 /* Number of exported entry points (for the loader test). */

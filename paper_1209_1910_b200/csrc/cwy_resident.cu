@@ -1,0 +1,715 @@
+// cwy_resident.cu -- compact-WY inverse iteration for narrow clusters with Y resident in
+// distributed shared memory (Alg. 4, §3.3.2 lines
+// 439-633).
+//
+// The clustered work of small-n problems (cfg1/cfg2: hundreds of clusters of m <= 64) is
+// latency-bound: the critical path is the 2 (m-1) dependent iterations of the largest
+// cluster, each a handful of passes over its Y (n x m).  Streaming Y from L2 every pass costs
+// ~15 us per pass; here every eigen-cluster is owned by one thread-block cluster of CS CTAs
+// (CS in {1, 2, 4, 8}, chosen by the host so that the cluster's rows fit): CTA c keeps rows
+// [c RL, (c+1) RL) of Y (built column by column, never leaving shared memory), of the iterate
+// and of uhat / q.  Every phase works on local rows; the few cross-CTA reductions (Y^T x,
+// Yhat^T uhat, norms, the chained solve's forward maps) go through a double-buffered exchange
+// area read over DSMEM in fixed CTA order (deterministic), separated by hardware cluster
+// barriers.  T (m x m), g, g', s, x' are small and replicated in every CTA.
+//
+// Per iteration of vector p (the same algebra as cwy.cu; formulas cited there):
+//   A   g = Y_p^T x                       (or the look-ahead partials for the first iteration)
+//   TT  g' = T_p^T g                      (replicated)
+//   BC  uhat = xhat - Yhat g', s' = Yhat^T uhat, ||uhat||^2
+//   R2  c, t, y0 (reflector), s = s' - c Y[p,:]
+//   TN  that = -t T_p s, x' = T_p Y[p,:]^T + y0 that (the T_j erratum fix), column p of T, Y
+//   D   q = Y_{p+1} x' - e_p, norms/argmax, forward-sweep chunk maps
+//   TEST, then either z_j = q/||q|| or the chained solve: exact forward carries from the
+//   composed maps -> t rows (gathered in CTA 0), serial back sweep by one thread of CTA 0
+//   (factor records streamed by TMA) in place over t, then every CTA copies its x rows, while
+//   every other warp computes the look-ahead pass A of vector p+1.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "tinv_internal.h"
+
+namespace cgr = cooperative_groups;
+
+namespace tinv {
+namespace res {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int CH = 256;          // back-sweep ring chunk (rows)
+constexpr int kRing = 4;         // back-sweep ring depth
+constexpr int kXS = 16;          // scalar slots of the exchange area
+enum { U2 = 0, X2 = 1, U0 = 2, Q2 = 3, QINF = 4, QARG = 5, Q1 = 6, FA = 7, FB = 8, X2N = 9, GPN = 10 };
+
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+// bulk L2 prefetch (16-byte aligned, size rounded up to 16 bytes)
+__device__ __forceinline__ void l2_prefetch_(const double* p, int64_t nd) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)(((nd * 8) + 15) & ~int64_t(15)))
+                 : "memory");
+}
+__device__ __forceinline__ int pow2ceil(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+struct Aff {
+    double a, b;   // c -> a c + b
+};
+__device__ __forceinline__ Aff comp(const Aff& f, const Aff& g) { return Aff{f.a * g.a, fma(f.a, g.b, f.b)}; }
+
+struct L {        // shared-memory carve-up (doubles unless noted)
+    double* Y;    // RL x M2, local rows
+    double* xl;   // RL: current iterate
+    double* ul;   // RL: uhat
+    double* ql;   // RL: q
+    double* x1l;  // RL: x^(1) of the next vector (look-ahead)
+    double* T;    // M2 x M2 row-major, T[l][k]
+    double* g;    // M2 + 2
+    double* gp;
+    double* s;
+    double* xp;
+    double* yrow;
+    double* PX;   // 2 x (M2 + kXS): exchange (double-buffered)
+    double* PXL;  // M2 + kXS: look-ahead exchange
+    double* tf;   // n + 2: t rows gathered for the back sweep (CTA 0)
+    double* ring; // kRing x 4 CH: factor records of the back sweep
+    double* red;  // NW + 8
+    double2* acc; // NT
+    uint64_t* mbar;
+};
+
+__host__ __device__ inline size_t smem_doubles(int64_t n, int RL, int M2) {
+    return (size_t)RL * (M2 + 4) + (size_t)M2 * M2 + 5 * (size_t)(M2 + 2) + 3 * (size_t)(M2 + kXS) + (n + 2) +
+           (size_t)kRing * 4 * CH + (NW + 8) + 2 * NT + kRing + 8;
+}
+
+// block-wide exclusive scan of affine maps (thread order), total returned
+__device__ __forceinline__ Aff scan_excl(Aff f, Aff* buf, Aff& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    Aff inc = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const Aff g{__shfl_up_sync(0xffffffffu, inc.a, o), __shfl_up_sync(0xffffffffu, inc.b, o)};
+        if (lane >= o) inc = comp(inc, g);
+    }
+    Aff ex{__shfl_up_sync(0xffffffffu, inc.a, 1), __shfl_up_sync(0xffffffffu, inc.b, 1)};
+    if (lane == 0) ex = Aff{1.0, 0.0};
+    __syncthreads();
+    if (lane == 31) buf[w] = inc;
+    __syncthreads();
+    Aff pre{1.0, 0.0};
+    for (int k = 0; k < w; k++) pre = comp(buf[k], pre);
+    total = pre;
+    for (int k = w; k < NW; k++) total = comp(buf[k], total);
+    __syncthreads();
+    return comp(ex, pre);
+}
+
+// Column accumulate over local rows [a, b) (local indices): out[k] = sum Y[i][k] c_i for
+// k < min(gi + 1, P) (gi = global row); threads [t0, t0 + nth); fixed-order slice reduction.
+template <class Coef, class Sync>
+__device__ void colacc_local(const L& sm, int M2, int r0, int a, int b, int P, Coef coef, double* out, int t0,
+                             int nth, Sync sync) {
+    const int t = threadIdx.x - t0;
+    const int CPT = min(32, pow2ceil((P + 1) / 2 > 0 ? (P + 1) / 2 : 1));
+    const int RS = nth / CPT, cp = t % CPT, rs = t / CPT;
+    const int k = 2 * cp;
+    double a0 = 0.0, a1 = 0.0;
+    for (int i = a + rs; i < b; i += RS) {
+        const int gi = r0 + i;
+        const int le = min(gi + 1, P);
+        if (k < le) {
+            const double2 y = *reinterpret_cast<const double2*>(sm.Y + (size_t)i * M2 + k);
+            const double c = coef(i);
+            a0 = fma(y.x, c, a0);
+            if (k + 1 < le) a1 = fma(y.y, c, a1);
+        }
+    }
+    sync();
+    sm.acc[t] = make_double2(a0, a1);
+    sync();
+    if (rs == 0 && t < CPT) {
+        for (int q = 1; q < RS; q++) {
+            const double2 v = sm.acc[cp + q * CPT];
+            a0 += v.x;
+            a1 += v.y;
+        }
+        if (k < P) out[k] = a0;
+        if (k + 1 < P) out[k + 1] = a1;
+    }
+    // columns beyond 2 CPT (P <= 64 always here)
+    sync();
+}
+
+// Chained back substitution x_i = t_i - b_i x_{i+1} - c_i x_{i+2} (rows n-1 .. 0) by the
+// calling thread, in place over t (shared memory): t_i is read before x_i overwrites it.
+// Factor records (l, 1/u0, b, c) stream through a kRing-deep TMA ring; the loop keeps the
+// next 8 rows' shared-memory loads ahead of the dependent chain (13 cycles/row on B200,
+// tools/micro/chain.cu).
+__device__ void back_sweep_inplace(const double* __restrict__ F, double* tf, int64_t n, double* ring, uint64_t* mbar,
+                                   uint32_t& mbph) {
+    const int64_t C = (n + CH - 1) / CH;
+    fence_proxy_async_global();
+    auto issue = [&](int64_t k) {
+        const int slot = (int)(k % kRing);
+        const int64_t c = C - 1 - k;
+        const int64_t lo = c * CH, hi = min64(lo + CH, n);
+        mbar_expect_tx(mbar + slot, (uint32_t)((hi - lo) * 32));
+        bulk_g2s(ring + (int64_t)slot * 4 * CH, F + lo * 4, (uint32_t)((hi - lo) * 32), mbar + slot);
+    };
+    for (int64_t k = 0; k < C && k < kRing; k++) issue(k);
+    double x1 = 0.0, x2 = 0.0;
+    for (int64_t k = 0; k < C; k++) {
+        const int slot = (int)(k % kRing);
+        mbar_wait(mbar + slot, (mbph >> slot) & 1u);
+        mbph ^= 1u << slot;
+        const double* Fs = ring + (int64_t)slot * 4 * CH;
+        const int64_t lo = (C - 1 - k) * CH, hi = min64(lo + CH, n);
+        double* Ts = tf + lo;
+        const int cnt = (int)(hi - lo);
+        const int top = cnt & ~7;
+        for (int u = cnt - 1; u >= top; u--) {
+            const double2 bc = *reinterpret_cast<const double2*>(Fs + u * 4 + 2);
+            const double xi = fma(-bc.x, x1, fma(-bc.y, x2, Ts[u]));
+            Ts[u] = xi;
+            x2 = x1;
+            x1 = xi;
+        }
+        if (top > 0) {
+            double b[8], c[8], t[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const double2 bc = *reinterpret_cast<const double2*>(Fs + (top - 8 + u) * 4 + 2);
+                b[u] = bc.x; c[u] = bc.y; t[u] = Ts[top - 8 + u];
+            }
+            for (int u0 = top - 8; u0 >= 0; u0 -= 8) {
+                double bn[8], cn[8], tn[8], xv[8];
+                const int nx = u0 >= 8 ? u0 - 8 : 0;
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const double2 bc = *reinterpret_cast<const double2*>(Fs + (nx + u) * 4 + 2);
+                    bn[u] = bc.x; cn[u] = bc.y; tn[u] = Ts[nx + u];
+                }
+#pragma unroll
+                for (int u = 7; u >= 0; u--) {
+                    xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u]));
+                    x2 = x1;
+                    x1 = xv[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u += 2)
+                    *reinterpret_cast<double2*>(Ts + u0 + u) = make_double2(xv[u], xv[u + 1]);
+#pragma unroll
+                for (int u = 0; u < 8; u++) { b[u] = bn[u]; c[u] = cn[u]; t[u] = tn[u]; }
+            }
+        }
+        if (k + kRing < C) issue(k + kRing);
+    }
+}
+
+__device__ __forceinline__ double block_sum_(double v, double* red) { return block_sum<NT>(v, red); }
+
+__global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cgr::cluster_group cl = cgr::this_cluster();
+    const int CS = (int)cl.num_blocks();
+    const int crank = (int)cl.block_rank();
+    const int unit = blockIdx.x / CS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = a.n;
+    const int RL = a.RL, M2 = a.M2;
+    L sm;
+    {
+        double* p = reinterpret_cast<double*>(smem_raw);
+        sm.Y = p; p += (size_t)RL * M2;
+        sm.xl = p; p += RL;
+        sm.ul = p; p += RL;
+        sm.ql = p; p += RL;
+        sm.x1l = p; p += RL;
+        sm.T = p; p += (size_t)M2 * M2;
+        sm.g = p; p += M2 + 2;
+        sm.gp = p; p += M2 + 2;
+        sm.s = p; p += M2 + 2;
+        sm.xp = p; p += M2 + 2;
+        sm.yrow = p; p += M2 + 2;
+        sm.PX = p; p += 2 * (M2 + kXS);
+        sm.PXL = p; p += M2 + kXS;
+        sm.tf = p; p += n + 2;
+        p += (reinterpret_cast<uintptr_t>(p) & 15) ? 1 : 0;
+        sm.ring = p; p += kRing * 4 * CH;
+        sm.red = p; p += NW + 8;
+        sm.acc = reinterpret_cast<double2*>(p); p += 2 * NT;
+        sm.mbar = reinterpret_cast<uint64_t*>(p);
+    }
+    if (tid == 0) {
+        for (int k = 0; k < kRing; k++) mbar_init(sm.mbar + k, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t mbph = 0;
+    const double thr = sqrt(0.1 / (double)n);
+    // optional phase timers (unit 0, CTA 0, thread 0; globaltimer ns)
+    const bool timing = a.prof && unit == 0 && crank == 0 && tid == 0;
+    uint64_t tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint64_t tmark = 0;
+    auto now = []() { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+    if (timing) tmark = now();
+    auto PH = [&](int k) {
+        if (timing) { const uint64_t t = now(); tacc[k] += t - tmark; tmark = t; }
+    };
+    const int64_t n2v = (n + 1) & ~int64_t(1);
+    const int r0 = crank * RL, r1 = (int)min64(n, (int64_t)r0 + RL);
+    const int nl = max(0, r1 - r0);
+    int pxb = 0;   // exchange buffer parity
+    auto PXo = [&](int c, int b) -> double* { return cl.map_shared_rank(sm.PX, c) + b * (M2 + kXS); };
+    auto csum = [&](int b, int slot) {   // sum over CTAs of a scalar slot, fixed order
+        double v = 0.0;
+        for (int c = 0; c < CS; c++) v += PXo(c, b)[M2 + slot];
+        return v;
+    };
+    auto csumL = [&](int slot) {
+        double v = 0.0;
+        for (int c = 0; c < CS; c++) v += cl.map_shared_rank(sm.PXL, c)[M2 + slot];
+        return v;
+    };
+    auto bsync = []() { __syncthreads(); };
+
+    for (int ci = a.u_off[unit]; ci < a.u_off[unit + 1]; ci++) {
+        const int clid = a.u_list[ci];
+        const int64_t j1 = a.cstart[clid];
+        const int m = (int)(a.cstart[clid + 1] - j1);
+
+        // ================= first reflector from z_{j1}
+        {
+            const double* z = a.Z + j1 * a.ldz;
+            double u2 = 0.0;
+            for (int i = tid; i < nl; i += NT) {
+                const double zi = __ldcg(z + r0 + i);
+                sm.ul[i] = zi;
+                u2 = fma(zi, zi, u2);
+            }
+            u2 = block_sum_(u2, sm.red);
+            double* px = sm.PX + pxb * (M2 + kXS);
+            if (tid == 0) px[M2 + U2] = u2;
+            cl.sync();
+            const double un = sqrt(csum(pxb, U2));
+            const double u0 = cl.map_shared_rank(sm.ul, 0)[0];
+            const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
+            const double tt = 1.0 / (c * c - u0 * c);
+            for (int i = tid; i < nl; i += NT) sm.Y[(size_t)i * M2] = (r0 + i == 0) ? (u0 - c) : sm.ul[i];
+            if (tid == 0) sm.T[0] = tt;
+            pxb ^= 1;
+            cl.sync();
+        }
+
+        bool la_have = false;
+        for (int p = 1; p < m; p++) {
+            const int64_t j = j1 + p;
+            int its = 1, kin = 1, passes = 0, restart = 0;
+            bool done = false, flagged = false;
+            bool use_la = la_have;
+            bool la_done = false;
+            la_have = false;
+            bool first = true;
+            if (crank == 0 && tid == 0) {   // this vector's factor records for the chained solve
+                const double* Fj = a.F + j * n * 4;
+                for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
+            }
+            // x^(1)_j into xl (the look-ahead already loaded it into x1l)
+            if (use_la) {
+                for (int i = tid; i < nl; i += NT) sm.xl[i] = sm.x1l[i];
+            } else {
+                const double* x1 = a.X1c + j * n2v;
+                for (int i = tid; i < nl; i += NT) sm.xl[i] = __ldcg(x1 + r0 + i);
+            }
+            __syncthreads();
+            while (!done) {
+                double x2;
+                // ---------------- A / R1: g = Y_p^T x
+                if (first && use_la) {
+                    for (int k = tid; k < p - 1; k += NT) {
+                        double v = 0.0;
+                        for (int c = 0; c < CS; c++) v += cl.map_shared_rank(sm.PXL, c)[k];
+                        sm.g[k] = v;
+                    }
+                    if (tid == 0) sm.g[p - 1] = csumL(GPN);
+                    x2 = csumL(X2N);
+                    __syncthreads();
+                } else {
+                    double* px = sm.PX + pxb * (M2 + kXS);
+                    colacc_local(sm, M2, r0, 0, nl, p, [&](int i) { return sm.xl[i]; }, px, 0, NT, bsync);
+                    double v = 0.0;
+                    for (int i = tid; i < nl; i += NT) v = fma(sm.xl[i], sm.xl[i], v);
+                    v = block_sum_(v, sm.red);
+                    if (tid == 0) px[M2 + X2] = v;
+                    cl.sync();
+                    for (int k = tid; k < p; k += NT) {
+                        double s = 0.0;
+                        for (int c = 0; c < CS; c++) s += PXo(c, pxb)[k];
+                        sm.g[k] = s;
+                    }
+                    x2 = csum(pxb, X2);
+                    pxb ^= 1;
+                    __syncthreads();
+                }
+                first = false;
+                use_la = false;
+                PH(0);
+                // ---------------- TT: g' = T_p^T g (replicated)
+                for (int k = tid; k < p; k += NT) {
+                    double v = 0.0;
+                    for (int l = 0; l <= k; l++) v = fma(sm.T[l * M2 + k], sm.g[l], v);
+                    sm.gp[k] = v;
+                }
+                __syncthreads();
+                // ---------------- BC: uhat (local rows >= p), s' partial, ||uhat||^2, uhat_p
+                {
+                    double* px = sm.PX + pxb * (M2 + kXS);
+                    const int ia = max(0, p - r0);
+                    double u2 = 0.0;
+                    for (int i = ia + tid; i < nl; i += NT) {
+                        const double* yr = sm.Y + (size_t)i * M2;
+                        double d0 = 0.0, d1 = 0.0;
+                        int k = 0;
+                        for (; k + 1 < p; k += 2) {
+                            const double2 y = *reinterpret_cast<const double2*>(yr + k);
+                            d0 = fma(y.x, sm.gp[k], d0);
+                            d1 = fma(y.y, sm.gp[k + 1], d1);
+                        }
+                        if (k < p) d0 = fma(yr[k], sm.gp[k], d0);
+                        const double ui = sm.xl[i] - (d0 + d1);
+                        sm.ul[i] = ui;
+                        u2 = fma(ui, ui, u2);
+                    }
+                    __syncthreads();
+                    colacc_local(sm, M2, r0, ia, nl, p, [&](int i) { return sm.ul[i]; }, px, 0, NT, bsync);
+                    u2 = block_sum_(u2, sm.red);
+                    if (tid == 0) {
+                        px[M2 + U2] = u2;
+                        px[M2 + U0] = (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0;
+                    }
+                    cl.sync();
+                }
+                PH(1);
+                // ---------------- R2: scalars; s = s' - c Y[p,:]
+                double un = sqrt(csum(pxb, U2));
+                double u0 = csum(pxb, U0);
+                const bool zero_u = (un == 0.0);
+                if (zero_u) { u0 = 1.0; un = 1.0; }
+                {
+                    const int own = p / RL;
+                    const double* yrp = cl.map_shared_rank(sm.Y, own) + (size_t)(p - own * RL) * M2;
+                    for (int k = tid; k < p; k += NT) sm.yrow[k] = yrp[k];
+                }
+                if (un <= (double)n * kEps * sqrt(x2) && restart < kMaxRestart && !zero_u) {
+                    // degenerate iterate (reading 16): restart from a fresh start vector
+                    restart++;
+                    its++;
+                    kin = 1;
+                    passes = 0;
+                    // forward maps of the start vector over this CTA's steps
+                    double* px = sm.PX + (pxb ^ 1) * (M2 + kXS);
+                    const double* Fj = a.F + j * n * 4;
+                    const int8_t* FPj = a.FP + j * n;
+                    const int s0 = max(0, r0 - 1), s1 = (int)min64(r1 - 1, n - 1);
+                    const int FL = s1 > s0 ? (s1 - s0 + NT - 1) / NT : 0;
+                    const int fta = s0 + min(max(s1 - s0, 0), tid * FL), ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FL);
+                    auto rhs = [&](int64_t i) { return start_entry(a.seed, n, j, restart, i); };
+                    Aff f{1.0, 0.0};
+                    double q1 = 0.0;
+                    for (int i = tid; i < nl; i += NT) q1 += fabs(rhs(r0 + i));
+                    for (int s = fta; s < ftb; s++) {
+                        const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1);
+                        if (FPj[s]) f.b = fma(-l, bn, f.b);
+                        else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
+                    }
+                    Aff tot;
+                    const Aff ex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
+                    q1 = block_sum_(q1, sm.red);
+                    if (tid == 0) { px[M2 + FA] = tot.a; px[M2 + FB] = tot.b; px[M2 + Q1] = q1; }
+                    cl.sync();
+                    Aff pre{1.0, 0.0};
+                    for (int c = 0; c < crank; c++) pre = comp(Aff{PXo(c, pxb ^ 1)[M2 + FA], PXo(c, pxb ^ 1)[M2 + FB]}, pre);
+                    const double q1t = csum(pxb ^ 1, Q1);
+                    const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / q1t;
+                    double cc = fma(ex.a, fma(pre.a, rhs(0), pre.b), ex.b);
+                    double* tf0 = cl.map_shared_rank(sm.tf, 0);
+                    for (int s = fta; s < ftb; s++) {
+                        const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1), rr = __ldg(Fj + (int64_t)s * 4 + 1);
+                        double y;
+                        if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
+                        else { y = cc; cc = fma(-l, cc, bn); }
+                        tf0[s] = sc * y * rr;
+                    }
+                    if (ftb == n - 1 && fta < ftb) {
+                        tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
+                        tf0[n] = 0.0;
+                    } else if (n == 1 && tid == 0) {
+                        tf0[0] = sc * cc * __ldg(Fj + 1);
+                        tf0[1] = 0.0;
+                    }
+                    pxb ^= 1;   // the buffer used above is now the "previous" one
+                    cl.sync();
+                    if (crank == 0 && tid == 0) back_sweep_inplace(a.F + j * n * 4, sm.tf, n, sm.ring, sm.mbar, mbph);
+                    cl.sync();
+                    {   // every CTA takes its rows of x from CTA 0
+                        const double* x0 = cl.map_shared_rank(sm.tf, 0);
+                        for (int i = tid; i < nl; i += NT) sm.xl[i] = x0[r0 + i];
+                    }
+                    cl.sync();
+                    first = false;
+                    continue;
+                }
+                if (un <= (double)n * kEps * sqrt(x2)) flagged = true;
+                const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
+                const double tt = 1.0 / (c * c - u0 * c);
+                const double y0 = u0 - c;
+                for (int k = tid; k < p; k += NT) {
+                    double v = 0.0;
+                    if (!zero_u)
+                        for (int cc = 0; cc < CS; cc++) v += PXo(cc, pxb)[k];
+                    sm.s[k] = v - c * sm.yrow[k];
+                }
+                pxb ^= 1;
+                __syncthreads();
+                // ---------------- TN (replicated): that, x', column p of T; column p of local Y
+                for (int l = tid; l < p; l += NT) {
+                    double a1 = 0.0, a2 = 0.0;
+                    const double* tr = sm.T + (size_t)l * M2;
+                    for (int k = l; k < p; k++) {
+                        a1 = fma(tr[k], sm.s[k], a1);
+                        a2 = fma(tr[k], sm.yrow[k], a2);
+                    }
+                    const double that = -tt * a1;
+                    sm.xp[l] = a2 + y0 * that;
+                    sm.T[(size_t)l * M2 + p] = that;
+                }
+                if (tid == 0) {
+                    sm.xp[p] = tt * y0;
+                    sm.T[(size_t)p * M2 + p] = tt;
+                }
+                for (int i = max(0, p - r0) + tid; i < nl; i += NT)
+                    sm.Y[(size_t)i * M2 + p] = (r0 + i == p) ? y0 : (zero_u ? 0.0 : sm.ul[i]);
+                __syncthreads();
+                PH(2);
+                // ---------------- D: q = Y_{p+1} x' - e_p, norms, argmax, look-ahead column,
+                // forward-sweep chunk maps over this CTA's steps
+                Aff fex{1.0, 0.0};
+                int fta = 0, ftb = 0;
+                {
+                    double* px = sm.PX + pxb * (M2 + kXS);
+                    double q2 = 0.0, q1 = 0.0, qinf = -1.0, gpn = 0.0;
+                    int64_t qarg = 0;
+                    for (int i = tid; i < nl; i += NT) {
+                        const int gi = r0 + i;
+                        const int le = min(gi + 1, p + 1);
+                        const double* yr = sm.Y + (size_t)i * M2;
+                        double d0 = 0.0, d1 = 0.0;
+                        int k = 0;
+                        for (; k + 1 < le; k += 2) {
+                            const double2 y = *reinterpret_cast<const double2*>(yr + k);
+                            d0 = fma(y.x, sm.xp[k], d0);
+                            d1 = fma(y.y, sm.xp[k + 1], d1);
+                        }
+                        if (k < le) d0 = fma(yr[k], sm.xp[k], d0);
+                        const double qi = (gi == p) ? (d0 + d1) - 1.0 : (d0 + d1);
+                        sm.ql[i] = qi;
+                        q2 = fma(qi, qi, q2);
+                        const double aq = fabs(qi);
+                        q1 += aq;
+                        if (aq > qinf) { qinf = aq; qarg = gi; }
+                        if (la_done && gi >= p) gpn = fma(yr[p], sm.x1l[i], gpn);
+                    }
+                    q2 = block_sum_(q2, sm.red);
+                    q1 = block_sum_(q1, sm.red);
+                    gpn = block_sum_(gpn, sm.red);
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double oq = __shfl_xor_sync(0xffffffffu, qinf, o);
+                        const long long oa = __shfl_xor_sync(0xffffffffu, (long long)qarg, o);
+                        if (oq > qinf || (oq == qinf && oa < qarg)) { qinf = oq; qarg = oa; }
+                    }
+                    if (lane == 0) sm.acc[warp] = make_double2(qinf, (double)qarg);
+                    __syncthreads();
+                    if (tid == 0) {
+                        for (int w = 1; w < NW; w++) {
+                            const double2 t = sm.acc[w];
+                            if (t.x > qinf || (t.x == qinf && (int64_t)t.y < qarg)) { qinf = t.x; qarg = (int64_t)t.y; }
+                        }
+                        px[M2 + Q2] = q2;
+                        px[M2 + Q1] = q1;
+                        px[M2 + QINF] = qinf;
+                        px[M2 + QARG] = (double)qarg;
+                        sm.PXL[M2 + GPN] = gpn;
+                    }
+                    // forward sweep pass 1: steps [max(0, r0-1), min(r1-1, n-1)) use this CTA's q
+                    const double* Fj = a.F + j * n * 4;
+                    const int8_t* FPj = a.FP + j * n;
+                    const int s0 = max(0, r0 - 1), s1 = (int)min64(r1 - 1, n - 1);
+                    const int FL = s1 > s0 ? (s1 - s0 + NT - 1) / NT : 0;
+                    fta = s0 + min(max(s1 - s0, 0), tid * FL);
+                    ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FL);
+                    Aff f{1.0, 0.0};
+                    __syncthreads();
+                    for (int s = fta; s < ftb; s++) {
+                        const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
+                        if (FPj[s]) f.b = fma(-l, bn, f.b);
+                        else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
+                    }
+                    Aff tot;
+                    fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
+                    if (tid == 0) { px[M2 + FA] = tot.a; px[M2 + FB] = tot.b; }
+                    cl.sync();
+                }
+                PH(3);
+                // ---------------- TEST (replicated)
+                const double q2 = csum(pxb, Q2);
+                double qinf = -1.0;
+                int64_t qarg = 0;
+                for (int c2 = 0; c2 < CS; c2++) {
+                    const double v = PXo(c2, pxb)[M2 + QINF];
+                    const int64_t ia = (int64_t)PXo(c2, pxb)[M2 + QARG];
+                    if (v > qinf || (v == qinf && ia < qarg)) { qinf = v; qarg = ia; }
+                }
+                if (fabs(c) * qinf >= thr) passes++;
+                if (passes >= kPasses) done = true;
+                else if (kin >= kMaxIts) { done = true; flagged = true; }
+                if (done) {
+                    const int own = (int)(qarg / RL);
+                    const double sgn = (cl.map_shared_rank(sm.ql, own)[qarg - (int64_t)own * RL] < 0.0) ? -1.0 : 1.0;
+                    const double scl = sgn / sqrt(q2);
+                    double* zj = a.Z + j * a.ldz;
+                    for (int i = tid; i < nl; i += NT) zj[r0 + i] = sm.ql[i] * scl;
+                    if (crank == 0 && tid == 0) {
+                        a.iters[j] = its;
+                        if (flagged) atomicAdd(&a.out->nflag, 1);
+                    }
+                    la_have = la_done;
+                    pxb ^= 1;
+                    cl.sync();   // exchange buffer and ql reads done before the next vector
+                    PH(4);
+                } else {
+                    its++;
+                    kin++;
+                    // forward pass 2: exact carries -> t rows, gathered into CTA 0
+                    {
+                        const double* Fj = a.F + j * n * 4;
+                        const int8_t* FPj = a.FP + j * n;
+                        Aff pre{1.0, 0.0};
+                        for (int c2 = 0; c2 < crank; c2++)
+                            pre = comp(Aff{PXo(c2, pxb)[M2 + FA], PXo(c2, pxb)[M2 + FB]}, pre);
+                        const double q0 = cl.map_shared_rank(sm.ql, 0)[0];
+                        double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
+                        const double q1 = csum(pxb, Q1);
+                        const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / q1;
+                        double* tf0 = cl.map_shared_rank(sm.tf, 0);
+                        for (int s = fta; s < ftb; s++) {
+                            const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
+                            const double rr = __ldg(Fj + (int64_t)s * 4 + 1);
+                            double y;
+                            if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
+                            else { y = cc; cc = fma(-l, cc, bn); }
+                            tf0[s] = sc * y * rr;
+                        }
+                        if (ftb == n - 1 && fta < ftb) {
+                            tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
+                            tf0[n] = 0.0;
+                        }
+                    }
+                    pxb ^= 1;
+                    cl.sync();
+                    PH(5);
+                    const bool la = !la_done && p + 1 < m;
+                    if (crank == 0 && tid == 0) back_sweep_inplace(a.F + j * n * 4, sm.tf, n, sm.ring, sm.mbar, mbph);
+                    if (la) {
+                        // look-ahead pass A of vector p+1 (every warp except CTA 0's warp 0):
+                        // columns 0..p-1 of Y_{p+1} are final
+                        const bool solver = (crank == 0);
+                        if (!solver || warp > 0) {
+                            const int t0 = solver ? 32 : 0, nth = solver ? NT - 32 : NT;
+                            auto ssync = [&]() {
+                                if (solver) asm volatile("bar.sync 1, %0;" ::"n"(NT - 32) : "memory");
+                                else __syncthreads();
+                            };
+                            const double* x1 = a.X1c + (j + 1) * n2v;
+                            double x2n = 0.0;
+                            for (int i = tid - t0; i < nl; i += nth) {
+                                const double v = __ldcg(x1 + r0 + i);
+                                sm.x1l[i] = v;
+                                x2n = fma(v, v, x2n);
+                            }
+                            ssync();
+                            colacc_local(sm, M2, r0, 0, nl, p, [&](int i) { return sm.x1l[i]; }, sm.PXL, t0, nth, ssync);
+                            x2n = warp_sum(x2n);
+                            if (lane == 0) sm.red[warp] = x2n;
+                            ssync();
+                            if (tid == t0) {
+                                double v = 0.0;
+                                for (int w = t0 / 32; w < NW; w++) v += sm.red[w];
+                                sm.PXL[M2 + X2N] = v;
+                            }
+                        }
+                        la_done = true;
+                    }
+                    if (timing) PH(6);
+                    cl.sync();   // x complete in CTA 0, look-ahead partials published
+                    {   // every CTA takes its rows of x from CTA 0
+                        const double* x0 = cl.map_shared_rank(sm.tf, 0);
+                        for (int i = tid; i < nl; i += NT) sm.xl[i] = x0[r0 + i];
+                    }
+                    cl.sync();   // CTA 0's t/x buffer is free again
+                    PH(7);
+                }
+            }
+        }
+        cl.sync();   // shared workspace reuse by the unit's next cluster
+    }
+    if (timing)
+        for (int k = 0; k < 8; k++) a.prof[k] = tacc[k];
+}
+
+}  // namespace res
+
+size_t resident_smem_bytes(int64_t n, int RL, int M2) { return sizeof(double) * res::smem_doubles(n, RL, M2); }
+
+cudaError_t launch_resident(const ResArgs& a, int cs, int nunits, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(res::cwy_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (cs > 8) {
+        e = cudaFuncSetAttribute(res::cwy_resident_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nunits * cs));
+    cfg.blockDim = dim3(res::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, res::cwy_resident_kernel, a);
+}
+
+int resident_max_clusters(int cs, size_t smem) {
+    cudaFuncSetAttribute(res::cwy_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cs);
+    cfg.blockDim = dim3(res::NT);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, res::cwy_resident_kernel, &cfg) != cudaSuccess) return 0;
+    return nc;
+}
+
+}  // namespace tinv

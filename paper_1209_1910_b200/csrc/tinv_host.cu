@@ -87,7 +87,12 @@ struct tinv_s {
     int64_t h_cap = 0;
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
+    int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
     // row split over real ranks: peers' cWY workspaces mapped through CUDA IPC
+    int* res_buf = nullptr;           // resident kernel unit lists (device)
+    size_t res_cap = 0;
+    int* h_res = nullptr;             // pinned staging
+    size_t h_res_cap = 0;
     std::vector<void*> peer_cw;       // per rank (nullptr for self)
     std::vector<char> peer_hdl;       // the IPC handles the mappings were opened from
     void* ipc_buf = nullptr;          // device staging for the handle allgather / barrier
@@ -100,6 +105,8 @@ struct tinv_s {
     // events for profiling
     cudaEvent_t ev[16] = {};
     cudaStream_t side = nullptr;      // cluster-table readback overlapped with the batched LU
+    cudaStream_t rs[4] = {};          // resident-kernel launches (one per cluster size) run concurrently
+    cudaEvent_t rev[5] = {};
     cudaEvent_t ev_prep = nullptr;
     tinv_stats_t stats{};
 };
@@ -186,11 +193,11 @@ struct Schedule {
 // Clusters [c_lo, c_hi) with m >= 2 -> CTA groups.  Many clusters: one CTA per group and
 // LPT over groups by cost m^2 n.  Few clusters: one group per cluster, CTAs shared in
 // proportion to cost, capped so a CTA keeps >= 256 KB of Y per pass.
-Schedule make_schedule(const int* cs, int c_lo, int c_hi, int64_t n, int nctas) {
+Schedule make_schedule(const int* cs, int c_lo, int c_hi, int64_t n, int nctas, const std::vector<char>* skip = nullptr) {
     Schedule s;
     std::vector<int> cl;
     for (int c = c_lo; c < c_hi; c++)
-        if (cs[c + 1] - cs[c] >= 2) cl.push_back(c);
+        if (cs[c + 1] - cs[c] >= 2 && !(skip && (*skip)[c])) cl.push_back(c);
     if (cl.empty()) return s;
     auto cost = [&](int c) { double m = cs[c + 1] - cs[c]; return m * m * (double)n + 64.0 * m * (double)n; };
     std::stable_sort(cl.begin(), cl.end(), [&](int a, int b) { return cost(a) > cost(b); });
@@ -365,9 +372,11 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     h->stream = (cudaStream_t)cfg->stream;
     h->nsm = prop.multiProcessorCount;
     CK(cudaMallocHost(&h->h_out, sizeof(PrepOut)));
-    CK(cudaMalloc(&h->bnd, 4 * sizeof(double)));
+    CK(cudaMalloc(&h->bnd, 32 * sizeof(double)));   // [0,4) bisection bounds, [8,16) resident timers
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    for (auto& q : h->rs) CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+    for (auto& q : h->rev) CK(cudaEventCreateWithFlags(&q, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
     if (h->nranks > 1) {
         if (!cfg->nccl_id || !g_nccl.load()) { delete h; return TINV_ERR_NCCL; }
@@ -388,6 +397,8 @@ int tinv_destroy(tinv_t h) {
     if (h->cw) cudaFree(h->cw);
     if (h->io) cudaFree(h->io);
     if (h->bnd) cudaFree(h->bnd);
+    if (h->res_buf) cudaFree(h->res_buf);
+    if (h->h_res) cudaFreeHost(h->h_res);
     for (void* pp : h->peer_cw) if (pp) cudaIpcCloseMemHandle(pp);
     if (h->ipc_buf) cudaFree(h->ipc_buf);
     if (h->h_out) cudaFreeHost(h->h_out);
@@ -397,6 +408,8 @@ int tinv_destroy(tinv_t h) {
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
     if (h->ev_prep) cudaEventDestroy(h->ev_prep);
     if (h->side) cudaStreamDestroy(h->side);
+    for (auto& q : h->rs) if (q) cudaStreamDestroy(q);
+    for (auto& q : h->rev) if (q) cudaEventDestroy(q);
     delete h;
     return 0;
 }
@@ -405,6 +418,12 @@ int tinv_set_virtual_ranks(tinv_t h, int nranks) {
     if (!h) return TINV_ERR_HANDLE;
     if (nranks < 1 || nranks > 16) return -2;
     h->vranks = nranks;
+    return 0;
+}
+
+int tinv_set_resident(tinv_t h, int enable) {
+    if (!h) return TINV_ERR_HANDLE;
+    h->resident = enable != 0;
     return 0;
 }
 
@@ -521,8 +540,41 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const bool rs_real = h->nranks > 1 && wide1;
     const int NRK = rs_real ? h->nranks : ((h->nranks == 1 && h->vranks > 1 && wide1) ? h->vranks : 1);
     const bool rs_virtual = !rs_real && NRK > 1;
+    // Narrow clusters whose rows fit in the shared memory of 1..8 CTAs run in the resident
+    // kernel (one thread-block cluster per eigen-cluster, Y in distributed shared memory);
+    // the rest in the persistent kernel.
+    std::vector<char> resident(nclus, 0);
+    struct ResGroup { int cs, RL, M2; size_t smem; std::vector<int> cl; };
+    std::vector<ResGroup> rgroups;
+    if (!rs_real && NRK == 1 && n <= 4096 && h->resident) {
+        const int css[4] = {1, 2, 4, 8};
+        for (int c = rlo[h->rank]; c < rhi[h->rank]; c++) {
+            const int m = cs[c + 1] - cs[c];
+            if (m < 2 || m > cwy_narrow_max()) continue;
+            const int m2 = (m + 1) & ~1;
+            for (int q = 0; q < 4; q++) {
+                const int RL = (int)(((n + css[q] - 1) / css[q] + 1) & ~int64_t(1));
+                if (resident_smem_bytes(n, RL, m2) <= 232448) {
+                    int gi = -1;
+                    for (int k = 0; k < (int)rgroups.size(); k++)
+                        if (rgroups[k].cs == css[q]) gi = k;
+                    if (gi < 0) {
+                        rgroups.push_back(ResGroup{css[q], RL, 0, 0, {}});
+                        gi = (int)rgroups.size() - 1;
+                    }
+                    rgroups[gi].cl.push_back(c);
+                    rgroups[gi].M2 = std::max(rgroups[gi].M2, m2);
+                    resident[c] = 1;
+                    break;
+                }
+            }
+        }
+        for (auto& rg : rgroups) rg.smem = resident_smem_bytes(n, rg.RL, rg.M2);
+        // the largest clusters first (longest dependent chains)
+        std::sort(rgroups.begin(), rgroups.end(), [](const ResGroup& a, const ResGroup& b) { return a.cs > b.cs; });
+    }
     Schedule sc = rs_real ? make_schedule(cs, 0, nclus, n, nctas_max)
-                          : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max);
+                          : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max, &resident);
     if (rs_virtual && sc.size.size() == 1) {   // split the group into NRK equal virtual ranks
         const int Gv = sc.size[0] / NRK;
         const int cl = sc.clist[0];
@@ -539,6 +591,77 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         sc.nctas = NRK * Gv;
     }
     const int RG = (rs_real || rs_virtual) ? NRK : 1;   // ranks per group
+    ev_record(h, 5);
+    if (!rgroups.empty()) {
+        // unit lists (LPT by the cluster's work m (m-1)) for every group, one H2D copy
+        std::vector<int> img;
+        std::vector<int> units(rgroups.size()), offs(rgroups.size());
+        // SMs shared between the concurrent groups in proportion to their work (vectors x
+        // CTAs), so all units are co-resident (no second wave)
+        double wtot = 0.0;
+        std::vector<double> wg(rgroups.size(), 0.0);
+        for (size_t q = 0; q < rgroups.size(); q++) {
+            for (int c : rgroups[q].cl) wg[q] += (double)(cs[c + 1] - cs[c] - 1) * rgroups[q].cs;
+            wtot += wg[q];
+        }
+        for (size_t q = 0; q < rgroups.size(); q++) {
+            ResGroup& rg = rgroups[q];
+            const int maxc = std::max(1, resident_max_clusters(rg.cs, rg.smem));
+            const int share = std::max(1, (int)((double)h->nsm * wg[q] / std::max(wtot, 1.0) / rg.cs));
+            const int nu = std::max(1, std::min<int>({(int)rg.cl.size(), maxc, share}));
+            std::vector<int> order = rg.cl;
+            std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+                return (cs[x + 1] - cs[x]) > (cs[y + 1] - cs[y]);
+            });
+            std::vector<std::vector<int>> lists(nu);
+            std::vector<double> load(nu, 0.0);
+            for (int c : order) {
+                const double m = cs[c + 1] - cs[c];
+                const int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+                lists[b].push_back(c);
+                load[b] += m * (m - 1);
+            }
+            units[q] = nu;
+            offs[q] = (int)img.size();
+            int acc = 0;
+            img.push_back(0);
+            for (int u = 0; u < nu; u++) { acc += (int)lists[u].size(); img.push_back(acc); }
+            for (int u = 0; u < nu; u++) for (int c : lists[u]) img.push_back(c);
+        }
+        if (img.size() > h->res_cap) {
+            if (h->res_buf) cudaFree(h->res_buf);
+            h->res_buf = nullptr;
+            CK(cudaMalloc(&h->res_buf, sizeof(int) * img.size()));
+            h->res_cap = img.size();
+        }
+        if (img.size() > h->h_res_cap) {
+            if (h->h_res) cudaFreeHost(h->h_res);
+            h->h_res = nullptr;
+            CK(cudaMallocHost(&h->h_res, sizeof(int) * img.size()));
+            h->h_res_cap = img.size();
+        }
+        memcpy(h->h_res, img.data(), sizeof(int) * img.size());
+        CK(cudaMemcpyAsync(h->res_buf, h->h_res, sizeof(int) * img.size(), cudaMemcpyHostToDevice, st));
+        // fork: every cluster size on its own stream (independent eigen-clusters), join below
+        CK(cudaEventRecord(h->rev[4], st));
+        for (size_t q = 0; q < rgroups.size(); q++) {
+            ResGroup& rg = rgroups[q];
+            cudaStream_t sq = h->rs[q];
+            CK(cudaStreamWaitEvent(sq, h->rev[4], 0));
+            ResArgs ra{};
+            ra.n = n; ra.RL = rg.RL; ra.M2 = rg.M2; ra.tnorm = tnorm; ra.seed = seed; ra.cstart = h->cstart;
+            ra.u_off = h->res_buf + offs[q];
+            ra.u_list = h->res_buf + offs[q] + units[q] + 1;
+            ra.X1c = h->X1c; ra.F = h->F; ra.FP = h->FP; ra.unn = h->unn; ra.Z = Z; ra.ldz = ldz;
+            ra.iters = h->iters; ra.out = h->out;
+            ra.prof = (h->profiling && q == 0) ? reinterpret_cast<unsigned long long*>(h->bnd + 8) : nullptr;
+            CK(launch_resident(ra, rg.cs, units[q], rg.smem, sq));
+            launches++;
+            CK(cudaEventRecord(h->rev[q], sq));
+        }
+        for (size_t q = 0; q < rgroups.size(); q++) CK(cudaStreamWaitEvent(st, h->rev[q], 0));
+        S.ngroups += 0;
+    }
     if (!sc.size.empty()) {
         const int ng = (int)sc.size.size();
         // workspace: schedule arrays + per-group buffers
@@ -658,12 +781,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.X1c = h->X1c; ca.Z = Z; ca.ldz = ldz; ca.iters = h->iters; ca.out = h->out;
         ca.ngroups = ng; ca.g_cta0 = arrs[0]; ca.g_size = arrs[1]; ca.g_coff = arrs[2]; ca.g_clist = arrs[3];
         ca.ws = dws; ca.syncs = syncs; ca.prof = h->profiling ? prof : nullptr;
-        ev_record(h, 5);
         ca.vcap = vcap;
         ca.nstg = nstg;
         CK(launch_cwy(ca, sc.nctas, smem, st));
         launches++;
-        ev_record(h, 6);
         S.ngroups = ng;
         S.cwy_ctas = sc.nctas;
         // algorithmic bytes: computed after the iteration counts are known (below)
@@ -676,6 +797,14 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         CK(cudaStreamSynchronize(st));
         for (int k = 0; k < 16; k++) S.cwy_phase_ms[k] = (double)hp[k] * 1e-6;
         for (auto v : hs) S.group_syncs = std::max<int64_t>(S.group_syncs, v);
+    }
+    ev_record(h, 6);
+    S.resident_groups = (int64_t)rgroups.size();
+    if (h->profiling && !rgroups.empty()) {   // resident phase timers -> the last 8 phase slots
+        unsigned long long hp[8];
+        CK(cudaMemcpyAsync(hp, h->bnd + 8, sizeof(hp), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int k = 0; k < 8; k++) S.cwy_phase_ms[8 + k] = (double)hp[k] * 1e-6;
     }
     S.solve_bytes = 144.0 * (double)n * (double)n;  // factor 32n + 2 x 56n per vector
 
@@ -725,10 +854,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); S.kernel_ms[1] = ms;
         cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); S.kernel_ms[2] = ms;
         cudaEventElapsedTime(&ms, h->ev[4], h->ev[8]); S.kernel_ms[4] = ms;
-        if (!sc.size.empty()) { cudaEventElapsedTime(&ms, h->ev[5], h->ev[6]); S.kernel_ms[3] = ms; }
+        cudaEventElapsedTime(&ms, h->ev[5], h->ev[6]); S.kernel_ms[3] = ms;
         cudaEventElapsedTime(&ms, h->ev[0], h->ev[7]); S.kernel_ms[5] = ms;
         S.kernel_launches[0] = 1; S.kernel_launches[1] = 1; S.kernel_launches[2] = 1; S.kernel_launches[4] = 1;
-        S.kernel_launches[3] = sc.size.empty() ? 0 : 1;
+        S.kernel_launches[3] = (sc.size.empty() ? 0 : 1) + (int64_t)rgroups.size();
     }
     const int nflag = h->h_out->nflag;
     S.nflagged = nflag;

@@ -143,6 +143,31 @@ struct CwyArgs {
     int nstg;                // TMA ring stages for narrow clusters (0 = ring not allocated)
 };
 
+// Resident compact-WY kernel for narrow clusters (cwy_resident.cu): one thread-block cluster
+// of CS CTAs per eigen-cluster, Y kept in distributed shared memory.
+struct ResArgs {
+    int64_t n;
+    int RL;                 // rows per CTA (even)
+    int M2;                 // Y / T row stride (>= every cluster's roundup(m, 2))
+    double tnorm;
+    uint64_t seed;
+    const int* cstart;
+    const int* u_off;       // per unit: offsets into u_list
+    const int* u_list;      // cluster ids
+    const double* X1c;      // x^(1), [j][i], vector stride roundup(n, 2)
+    const double* F;        // packed factors [j][i][4]
+    const int8_t* FP;       // pivot bytes [j][i]
+    const double* unn;
+    double* Z;
+    int64_t ldz;
+    int* iters;
+    PrepOut* out;
+    unsigned long long* prof;   // optional 8 phase timers of unit 0 (ns), or NULL
+};
+size_t resident_smem_bytes(int64_t n, int RL, int M2);
+cudaError_t launch_resident(const ResArgs& a, int cs, int nunits, size_t smem, cudaStream_t s);
+int resident_max_clusters(int cs, size_t smem);
+
 void launch_prep(const PrepArgs& a, cudaStream_t s);
 void launch_bisect(int64_t n, const double* d, const double* e, double* w, double* bnd, cudaStream_t s);
 void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm);

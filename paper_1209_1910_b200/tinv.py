@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libtinv.so")
 
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",
-           "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks")
+           "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks", "tinv_set_resident")
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
 PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "st_wait", "st_body", "st_sync", "st_blkend")
@@ -31,7 +31,7 @@ class TinvStats(C.Structure):
     _fields_ = [("n", C.c_int64), ("nclusters", C.c_int64), ("max_cluster", C.c_int64),
                 ("n_clustered", C.c_int64), ("nflagged", C.c_int64), ("iters_hist", C.c_int64 * 8),
                 ("launches", C.c_int64), ("group_syncs", C.c_int64), ("ngroups", C.c_int64),
-                ("cwy_ctas", C.c_int64), ("reorth_bytes", C.c_double), ("solve_bytes", C.c_double),
+                ("cwy_ctas", C.c_int64), ("resident_groups", C.c_int64), ("reorth_bytes", C.c_double), ("solve_bytes", C.c_double),
                 ("kernel_ms", C.c_double * 6), ("kernel_launches", C.c_int64 * 6),
                 ("cwy_phase_ms", C.c_double * 16)]
 
@@ -41,6 +41,7 @@ class TinvStats(C.Structure):
             "n_clustered": self.n_clustered, "nflagged": self.nflagged,
             "iters_hist": list(self.iters_hist), "launches": self.launches,
             "group_syncs": self.group_syncs, "ngroups": self.ngroups, "cwy_ctas": self.cwy_ctas,
+            "resident_groups": self.resident_groups,
             "reorth_bytes": self.reorth_bytes, "solve_bytes": self.solve_bytes,
             "kernel_ms": dict(zip(KERNEL_NAMES, list(self.kernel_ms))),
             "kernel_launches": dict(zip(KERNEL_NAMES, list(self.kernel_launches))),
@@ -80,6 +81,8 @@ def load_library(path: str = LIB_PATH):
     L.tinv_get_stats.argtypes = [P, C.POINTER(TinvStats)]
     L.tinv_get_stats.restype = C.c_int
     L.tinv_abi_version.argtypes = []
+    L.tinv_set_resident.restype = C.c_int
+    L.tinv_set_resident.argtypes = [P, C.c_int]
     L.tinv_set_virtual_ranks.restype = C.c_int
     L.tinv_set_virtual_ranks.argtypes = [P, C.c_int]
     L.tinv_eigvals.restype = C.c_int
@@ -160,6 +163,11 @@ class Tinv:
         if rc < 0 and check:
             raise TinvError(f"tinv_eigvecs failed: {rc} ({strerror(rc)})")
         return Zt.t(), rc
+
+    def set_resident(self, enable: bool):
+        rc = self._L.tinv_set_resident(self._h, int(bool(enable)))
+        if rc:
+            raise TinvError(f"tinv_set_resident failed: {rc}")
 
     def set_virtual_ranks(self, nranks: int):
         rc = self._L.tinv_set_virtual_ranks(self._h, int(nranks))
