@@ -79,6 +79,14 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     }
     __syncwarp();
     uint32_t ph = 0;
+    // optional sweep timers (warp 0, lane 0; globaltimer ns): factor+fwd, back 1, fwd 2, back 2
+    const bool timing = a.prof && blockIdx.x == 0 && lane == 0;
+    auto now = []() { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+    uint64_t t_mark = timing ? now() : 0;
+    int t_slot = 0;
+    auto tick = [&]() {
+        if (timing) { const uint64_t t = now(); if (t_slot < 8) a.prof[t_slot++] = t - t_mark; t_mark = t; }
+    };
 
     // ---------------- iteration 1: factor + forward elimination of the random start
     double pv_last;
@@ -134,6 +142,7 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
         __stcg(FC + o, 0.0);
         __stcg(X + o, c);
     }
+    tick();
     const double unn = fabs(pv_last);
     if (live) a.unn[j] = unn;
     const double sfac = (double)n * tnorm * fmax(kEps, unn);
@@ -158,20 +167,25 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
             mbar_wait(bars + (b % NS), (ph >> (b % NS)) & 1u);
             ph ^= 1u << (b % NS);
             const Stage& S = stages[b % NS];
+            // branch-free rows (rows below 0 only occur after row 0: their values are
+            // never used, only the statistics and stores are predicated), so the compiler
+            // can hoist the shared-memory loads of later rows above the dependent chain
+            const int64_t ib = n - b * RB - RB;
 #pragma unroll
             for (int rr = RB - 1; rr >= 0; rr--) {
-                const int64_t i = n - b * RB - (RB - rr);
-                if (i >= 0) {
-                    const double t = fma(-S.v[3][rr][lane], xp2, sc * S.v[0][rr][lane] * S.v[1][rr][lane]);
-                    const double xi = fma(-S.v[2][rr][lane], xp1, t);
-                    if (keep) __stcg(X + i * 32 + lane, xi);
-                    xp2 = xp1;
-                    xp1 = xi;
-                    const double ax = fabs(xi);
-                    if (ax >= xinf) { xinf = ax; imax = i; }   // lowest index on ties (descending)
-                    x1 += ax;
-                    x2 = fma(xi, xi, x2);
-                }
+                const int64_t i = ib + rr;
+                const bool valid = i >= 0;
+                const double t = fma(-S.v[3][rr][lane], xp2, sc * S.v[0][rr][lane] * S.v[1][rr][lane]);
+                const double xi = fma(-S.v[2][rr][lane], xp1, t);
+                if (keep && valid) __stcg(X + i * 32 + lane, xi);
+                xp2 = xp1;
+                xp1 = xi;
+                const double ax = valid ? fabs(xi) : -1.0;
+                const bool better = ax >= xinf;   // lowest index on ties (descending rows)
+                xinf = better ? ax : xinf;
+                imax = better ? i : imax;
+                x1 += valid ? ax : 0.0;
+                x2 = fma(valid ? xi : 0.0, valid ? xi : 0.0, x2);
             }
             __syncwarp();
             if (lane == 0 && b + NS < nblk) issue(b + NS);
@@ -202,16 +216,16 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
             ph ^= 1u << (b % NS);
             const Stage& S = stages[b % NS];
 #pragma unroll
-            for (int rr = 0; rr < RB; rr++) {
+            for (int rr = 0; rr < RB; rr++) {   // branch-free: steps past nf keep c unchanged
                 const int64_t i = b * RB + rr;
-                if (i < nf) {
-                    const double l = S.v[0][rr][lane];
-                    const double bn = S.v[1][rr][lane];
-                    const bool sw = S.pv[rr][lane] != 0;
-                    const double y = sw ? bn : c;
-                    c = fma(sw ? 1.0 : -l, c, sw ? -l * bn : bn);
-                    if (keep) __stcg(X + i * 32 + lane, y);
-                }
+                const bool valid = i < nf;
+                const double l = S.v[0][rr][lane];
+                const double bn = S.v[1][rr][lane];
+                const bool sw = S.pv[rr][lane] != 0;
+                const double y = sw ? bn : c;
+                const double cn = fma(sw ? 1.0 : -l, c, sw ? -l * bn : bn);
+                c = valid ? cn : c;
+                if (keep && valid) __stcg(X + i * 32 + lane, y);
             }
             __syncwarp();
             if (lane == 0 && b + NS < nb) issue(b + NS);
@@ -224,6 +238,7 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     double xinf, x1, x2;
     int64_t imax;
     back(sfac / b1, true, xinf, x1, x2, imax);
+    tick();
     int its = 1;
     // Vectors with j_c >= 1 hand x^(1) to the compact-WY kernel.  The warp keeps sweeping
     // while any lane still iterates; lanes that are done run the sweeps without storing.
@@ -233,9 +248,11 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     while (__any_sync(0xffffffffu, want)) {
         const double sc = sfac / x1;
         forward(want);
+        tick();
         double xi_inf, xi1, xi2;
         int64_t im;
         back(sc, want, xi_inf, xi1, xi2, im);
+        tick();
         if (want) {
             its++;
             xinf = xi_inf; x1 = xi1; x2 = xi2; imax = im;

@@ -473,7 +473,8 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     CK(cudaMemcpyAsync(h->h_cstart, h->cstart, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, h->side));
     ev_record(h, 2);
     BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
-                   h->X, h->unn, h->zscale, h->iters, h->out};
+                   h->X, h->unn, h->zscale, h->iters, h->out,
+                   h->profiling ? reinterpret_cast<unsigned long long*>(h->bnd + 16) : nullptr};
     launch_batched(ba, st, h->nsm);
     launches++;
     CK(cudaGetLastError());
@@ -800,6 +801,13 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     }
     ev_record(h, 6);
     S.resident_groups = (int64_t)rgroups.size();
+    if (h->profiling) {   // batched-LU sweep timers (warp 0) -> phase slots 0..5
+        unsigned long long hb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        CK(cudaMemcpyAsync(hb, h->bnd + 16, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (sc.size.empty())
+            for (int k = 0; k < 6; k++) S.cwy_phase_ms[k] = (double)hb[k] * 1e-6;
+    }
     if (h->profiling && !rgroups.empty()) {   // resident phase timers -> the last 8 phase slots
         unsigned long long hp[8];
         CK(cudaMemcpyAsync(hp, h->bnd + 8, sizeof(hp), cudaMemcpyDeviceToHost, st));

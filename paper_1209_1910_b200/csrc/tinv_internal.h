@@ -51,6 +51,7 @@ struct BatchedArgs {
     double* zscale;     // sign/||x||_2 of finished (j_c == 0) vectors
     int* iters;         // iteration count per vector
     PrepOut* out;
+    unsigned long long* prof;   // optional sweep timers of warp 0 (ns), or NULL
 };
 
 struct PackArgs {
