@@ -773,6 +773,7 @@ struct SrcY {      // rows of Y_P (packed row-major, zero-free)
         b = r1;
     }
     __device__ int nblk() const { return (P + PW - 1) / PW; }
+    __device__ int width() const { return P; }
 };
 struct SrcTc {     // column-packed T: "row" k = T[0..k, k]
     const double* Tc;
@@ -785,6 +786,7 @@ struct SrcTc {     // column-packed T: "row" k = T[0..k, k]
         b = r1;
     }
     __device__ int nblk() const { return (P + PW - 1) / PW; }
+    __device__ int width() const { return P; }
 };
 struct SrcTr {     // row-major T: row l = T[l, l..P)
     const double* Tr;
@@ -797,6 +799,7 @@ struct SrcTr {     // row-major T: row l = T[l, l..P)
         b = min(r1, (kb + 1) * PW);
     }
     __device__ int nblk() const { return (P + PW - 1) / PW; }
+    __device__ int width() const { return P; }
 };
 
 // Pipeline state of the wide ring: full[s] completes when stage s's bulk copies land, empty[s]
@@ -811,7 +814,15 @@ struct WRing {
     uint64_t* tacc;     // optional timers (wait, body, release, block end) or nullptr
 };
 
-// Walk (chunk of rows, block kb, stage of <= PPS rows) in the order above.  Consumers (warps
+// Piece stride of a pass: PW for multi-block passes, else the (even) row width; rows per
+// stage: as many pieces as fit a slot, at most two per consumer warp.
+template <class Src>
+__device__ __forceinline__ int wide_pst(const Src& src) {
+    return src.nblk() > 1 ? PW : ((src.width() + 1) & ~1);
+}
+__device__ __forceinline__ int wide_rps(int pst) { return min(2 * NCW, kWStgD / max(pst, 2)); }
+
+// Walk (chunk of rows, block kb, stage of <= RPS rows) in the order above.  Consumers (warps
 // 1..NCW) call blk_begin(kb, c0, c1) at the first stage of each block, body(kb, ra, rb, slot)
 // per stage (piece q = row ra + q at slot + q PW, columns [kb PW, kb PW + PW), only the valid
 // ones copied) and blk_end(kb) after its last stage; these may use consumer_sync() but not
@@ -823,6 +834,9 @@ __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, boo
                             ChunkEnd chunk_end) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NB = src.nblk();
+    // piece stride / rows per stage: a single narrow block packs up to 32 rows per stage
+    const int PST = wide_pst(src);
+    const int RPS = wide_rps(PST);
     for (int c0 = r0; c0 < r1; c0 += RCH) {
         const int c1 = min(r1, c0 + RCH);
         chunk_begin(c0, c1);
@@ -835,7 +849,7 @@ __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, boo
                 row = max(row, a);
                 if (row < b) {
                     ra = row;
-                    rb = min(b, row + PPS);
+                    rb = min(b, row + RPS);
                     row = rb;
                     return true;
                 }
@@ -880,7 +894,7 @@ __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, boo
                     if (b > a) {
                         const uint32_t bytes = (uint32_t)(b - a) * 8u;
                         mbar_add_tx(rg.full + slot, bytes);
-                        bulk_g2s(rg.base + (int64_t)slot * kWStgD + (r - ra) * PW + (a - kb * PW), src.base(r) + a,
+                        bulk_g2s(rg.base + (int64_t)slot * kWStgD + (r - ra) * PST + (a - kb * PW), src.base(r) + a,
                                  bytes, rg.full + slot);
                     }
                 }
@@ -975,13 +989,13 @@ __device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, in
             if (threadIdx.x == 32) sm.vuse[kb & 1] = u + 1;
         },
         [&](int kb, int ra, int rb, const double* slot) {
-            const int q = warp - 1;
-            const int r = ra + q;
-            if (r < rb) {
+            const int PST = wide_pst(src);
+            for (int q = warp - 1; ra + q < rb; q += NCW) {
+                const int r = ra + q;
                 const int lo = src.cs(r), hi = src.ce(r);
                 const double* vb = sm.vblk + (kb & 1) * 2 * PW;
                 double a1 = 0.0, a2 = 0.0;
-                const double* rowp = slot + q * PW;
+                const double* rowp = slot + q * PST;
                 const int kbase = kb * PW;
                 if (lo <= kbase && hi >= kbase + PW) {   // full piece: no masks
 #pragma unroll
@@ -1002,7 +1016,7 @@ __device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, in
                     for (int e = 0; e < PW; e += 64) {   // lane: columns e + 2 lane, +1 (conflict-free)
                         const int cl = e + 2 * lane;
                         const int k = kbase + cl;
-                        if (k + 1 >= lo && k < hi) {
+                        if (cl < PST && k + 1 >= lo && k < hi) {
                             const double2 y = *reinterpret_cast<const double2*>(rowp + cl);
                             const double2 vv = *reinterpret_cast<const double2*>(vb + cl);
                             const double y0 = (k >= lo) ? y.x : 0.0;
@@ -1073,10 +1087,11 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
         [&](int, int, int) {},
         [&](int kb, int ra, int rb, const double* slot) {
             const int k = kb * PW + 2 * tc;
+            const int PST = wide_pst(src);
             for (int r = ra; r < rb; r++) {
                 const int lo = src.cs(r), hi = src.ce(r);
                 if (k + 1 >= lo && k < hi) {
-                    const double2 y = *reinterpret_cast<const double2*>(slot + (r - ra) * PW + 2 * tc);
+                    const double2 y = *reinterpret_cast<const double2*>(slot + (r - ra) * PST + 2 * tc);
                     const double c = sm.cf[r - cb];
                     if (k >= lo) a0 = fma(y.x, c, a0);
                     if (k + 1 < hi) a1 = fma(y.y, c, a1);
