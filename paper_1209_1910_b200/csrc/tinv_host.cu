@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <dlfcn.h>
 #include <numeric>
@@ -88,6 +89,7 @@ struct tinv_s {
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
+    int res_cs2 = 1000, res_cs4 = 1000;   // m from which a cluster gets >= 2 / 4 CTAs
     // row split over real ranks: peers' cWY workspaces mapped through CUDA IPC
     int* res_buf = nullptr;           // resident kernel unit lists (device)
     size_t res_cap = 0;
@@ -372,6 +374,8 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     h->stream = (cudaStream_t)cfg->stream;
     h->nsm = prop.multiProcessorCount;
     CK(cudaMallocHost(&h->h_out, sizeof(PrepOut)));
+    if (const char* v = getenv("TINV_RES_CS2")) h->res_cs2 = atoi(v);
+    if (const char* v = getenv("TINV_RES_CS4")) h->res_cs4 = atoi(v);
     CK(cudaMalloc(&h->bnd, 32 * sizeof(double)));   // [0,4) bisection bounds, [8,16) resident timers
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -553,9 +557,11 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             const int m = cs[c + 1] - cs[c];
             if (m < 2 || m > cwy_narrow_max()) continue;
             const int m2 = (m + 1) & ~1;
+            // the longest chains get more CTAs (shorter passes) beyond what their rows need
+            const int want = (m >= h->res_cs4) ? 4 : (m >= h->res_cs2 ? 2 : 1);
             for (int q = 0; q < 4; q++) {
                 const int RL = (int)(((n + css[q] - 1) / css[q] + 1) & ~int64_t(1));
-                if (resident_smem_bytes(n, RL, m2) <= 232448) {
+                if (css[q] >= want && resident_smem_bytes(n, RL, m2) <= 232448) {
                     int gi = -1;
                     for (int k = 0; k < (int)rgroups.size(); k++)
                         if (rgroups[k].cs == css[q]) gi = k;
