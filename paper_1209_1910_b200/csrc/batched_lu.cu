@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     extern __shared__ __align__(128) unsigned char bl_smem[];
     Stage* stages = reinterpret_cast<Stage*>(bl_smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(bl_smem + sizeof(Stage) * NS);
+    // small n: d and e staged in shared memory (every warp walks them once per factor sweep;
+    // from a cold L1 each 128-byte line would be an L2 round trip next to the dependent chain)
+    double* sde = reinterpret_cast<double*>(bl_smem + sizeof(Stage) * NS + 8 * (NS + 2));
     const int lane = threadIdx.x;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
     const int64_t j = j0 + lane;
@@ -71,13 +74,21 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     double* __restrict__ FB = a.fb + boff;
     double* __restrict__ FC = a.fc + boff;
     int8_t* __restrict__ FPv = a.fp + boff;
-    const double* __restrict__ dd = a.d;
-    const double* __restrict__ ee = a.e;
+    const bool stage_de = a.stage_de != 0;
     if (lane == 0) {
-        for (int s = 0; s < NS; s++) mbar_init(bars + s, 1);
+        for (int s = 0; s < NS + 1; s++) mbar_init(bars + s, 1);
         fence_mbar_init();
+        if (stage_de) {
+            const uint32_t bd = (uint32_t)(((n + 1) & ~int64_t(1)) * 8), be = (uint32_t)((n & ~int64_t(1)) * 8);
+            mbar_expect_tx(bars + NS, bd + be);
+            bulk_g2s(sde, a.d, bd, bars + NS);
+            if (be) bulk_g2s(sde + ((n + 1) & ~int64_t(1)), a.e, be, bars + NS);
+        }
     }
     __syncwarp();
+    if (stage_de) mbar_wait(bars + NS, 0);
+    const double* __restrict__ dd = stage_de ? sde : a.d;
+    const double* __restrict__ ee = stage_de ? sde + ((n + 1) & ~int64_t(1)) : a.e;
     uint32_t ph = 0;
     // optional sweep timers (warp 0, lane 0; globaltimer ns): factor+fwd, back 1, fwd 2, back 2
     const bool timing = a.prof && blockIdx.x == 0 && lane == 0;
@@ -92,15 +103,15 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     double pv_last;
     double b1 = 0.0;  // ||b||_1
     {
-        double pp = __ldg(dd) - shift;
-        double qq = (n > 1) ? __ldg(ee) : 0.0;
+        double pp = dd[0] - shift;
+        double qq = (n > 1) ? ee[0] : 0.0;
         double c = start_entry(a.seed, n, jj, 0, 0);
         b1 = fabs(c);
 #pragma unroll 4
         for (int64_t i = 0; i < n - 1; i++) {
-            const double sub = __ldg(ee + i);
-            const double anext = __ldg(dd + i + 1) - shift;
-            const double enext = (i + 1 < n - 1) ? __ldg(ee + i + 1) : 0.0;
+            const double sub = ee[i];
+            const double anext = dd[i + 1] - shift;
+            const double enext = (i + 1 < n - 1) ? ee[i + 1] : 0.0;
             const double bn = start_entry(a.seed, n, jj, 0, i + 1);
             b1 += fabs(bn);
             double u0, u1, u2, l, y;
@@ -169,23 +180,50 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
             const Stage& S = stages[b % NS];
             // branch-free rows (rows below 0 only occur after row 0: their values are
             // never used, only the statistics and stores are predicated), so the compiler
-            // can hoist the shared-memory loads of later rows above the dependent chain
+            // can hoist the shared-memory loads of later rows above the dependent chain; the
+            // statistics (||x||_1, ||x||_2^2, argmax) are reduced per stage with fixed trees
+            // instead of one dependent chain per row
             const int64_t ib = n - b * RB - RB;
+            double xv[RB];
 #pragma unroll
             for (int rr = RB - 1; rr >= 0; rr--) {
-                const int64_t i = ib + rr;
-                const bool valid = i >= 0;
                 const double t = fma(-S.v[3][rr][lane], xp2, sc * S.v[0][rr][lane] * S.v[1][rr][lane]);
                 const double xi = fma(-S.v[2][rr][lane], xp1, t);
-                if (keep && valid) __stcg(X + i * 32 + lane, xi);
+                xv[rr] = xi;
                 xp2 = xp1;
                 xp1 = xi;
-                const double ax = valid ? fabs(xi) : -1.0;
-                const bool better = ax >= xinf;   // lowest index on ties (descending rows)
-                xinf = better ? ax : xinf;
-                imax = better ? i : imax;
-                x1 += valid ? ax : 0.0;
-                x2 = fma(valid ? xi : 0.0, valid ? xi : 0.0, x2);
+            }
+            double sa[RB], sq[RB];
+            int ia[RB];
+#pragma unroll
+            for (int rr = 0; rr < RB; rr++) {
+                const bool valid = ib + rr >= 0;
+                if (keep && valid) __stcg(X + (ib + rr) * 32 + lane, xv[rr]);
+                sa[rr] = valid ? fabs(xv[rr]) : 0.0;
+                sq[rr] = valid ? xv[rr] * xv[rr] : 0.0;
+                ia[rr] = rr;
+            }
+            double mx[RB];
+#pragma unroll
+            for (int rr = 0; rr < RB; rr++) mx[rr] = (ib + rr >= 0) ? sa[rr] : -1.0;
+#pragma unroll
+            for (int w = 1; w < RB; w <<= 1) {
+#pragma unroll
+                for (int rr = 0; rr + w < RB; rr += 2 * w) {
+                    sa[rr] += sa[rr + w];
+                    sq[rr] += sq[rr + w];
+                    // larger value wins; on ties the lower row index
+                    const bool tk = mx[rr + w] > mx[rr];
+                    mx[rr] = tk ? mx[rr + w] : mx[rr];
+                    ia[rr] = tk ? ia[rr + w] : ia[rr];
+                }
+            }
+            x1 += sa[0];
+            x2 += sq[0];
+            // this stage's rows are lower than every earlier stage's: ties go to this stage
+            if (mx[0] >= xinf && mx[0] >= 0.0) {
+                xinf = mx[0];
+                imax = ib + ia[0];
             }
             __syncwarp();
             if (lane == 0 && b + NS < nblk) issue(b + NS);
@@ -338,14 +376,19 @@ __global__ void identity_kernel(double* Z, int64_t n, int64_t ldz) {
 
 void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm) {
     int64_t nb = (a.n + 31) / 32;
+    BatchedArgs b = a;
     if (nb <= nsm) {
-        const size_t sm = (sizeof(Stage) + 8) * NS_DEEP;
+        const size_t de = (size_t)(((a.n + 1) & ~int64_t(1)) + (a.n & ~int64_t(1))) * 8;
+        size_t sm = sizeof(Stage) * NS_DEEP + 8 * (NS_DEEP + 2);
+        b.stage_de = (sm + de <= 200 * 1024) ? 1 : 0;
+        if (b.stage_de) sm += de;
         cudaFuncSetAttribute(batched_lu_kernel<NS_DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        batched_lu_kernel<NS_DEEP><<<(unsigned)nb, 32, sm, s>>>(a);
+        batched_lu_kernel<NS_DEEP><<<(unsigned)nb, 32, sm, s>>>(b);
     } else {
-        const size_t sm = (sizeof(Stage) + 8) * NS_SHALLOW;
+        b.stage_de = 0;
+        const size_t sm = sizeof(Stage) * NS_SHALLOW + 8 * (NS_SHALLOW + 2);
         cudaFuncSetAttribute(batched_lu_kernel<NS_SHALLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 32, sm, s>>>(a);
+        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 32, sm, s>>>(b);
     }
 }
 

@@ -52,6 +52,7 @@ struct BatchedArgs {
     int* iters;         // iteration count per vector
     PrepOut* out;
     unsigned long long* prof;   // optional sweep timers of warp 0 (ns), or NULL
+    int stage_de;               // set by the launcher: d, e staged in shared memory
 };
 
 struct PackArgs {
