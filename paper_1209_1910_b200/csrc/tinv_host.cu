@@ -600,21 +600,35 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const int RG = (rs_real || rs_virtual) ? NRK : 1;   // ranks per group
     ev_record(h, 5);
     if (!rgroups.empty()) {
-        // unit lists (LPT by the cluster's work m (m-1)) for every group, one H2D copy
+        // unit lists (LPT by the cluster's work ~ its vectors) for every group, one H2D copy
         std::vector<int> img;
         std::vector<int> units(rgroups.size()), offs(rgroups.size());
-        // SMs shared between the concurrent groups in proportion to their work (vectors x
-        // CTAs), so all units are co-resident (no second wave)
-        double wtot = 0.0;
-        std::vector<double> wg(rgroups.size(), 0.0);
-        for (size_t q = 0; q < rgroups.size(); q++) {
-            for (int c : rgroups[q].cl) wg[q] += (double)(cs[c + 1] - cs[c] - 1) * rgroups[q].cs;
-            wtot += wg[q];
+        // SMs shared between the concurrent groups so that all units are co-resident (no
+        // second wave): the group with the largest CTA clusters (the longest chains) gets one
+        // unit per eigen-cluster, the rest of the SMs go to the other groups in proportion to
+        // their SM-time (vectors x CTAs)
+        std::vector<int> want_units(rgroups.size(), 1);
+        {
+            std::vector<double> wg(rgroups.size(), 0.0);
+            double wrest = 0.0;
+            for (size_t q = 0; q < rgroups.size(); q++) {
+                double vec = 0.0;
+                for (int c : rgroups[q].cl) vec += (double)(cs[c + 1] - cs[c] - 1);
+                // measured: a unit spends about the same time per vector whatever its CTA
+                // count (fewer rows per CTA but more exchange), so SM-time ~ vectors x CTAs
+                wg[q] = vec;
+                if (q > 0) wrest += vec * rgroups[q].cs;
+            }
+            int budget = h->nsm;
+            want_units[0] = std::max(1, std::min<int>((int)rgroups[0].cl.size(), budget / rgroups[0].cs));
+            budget -= want_units[0] * rgroups[0].cs;
+            for (size_t q = 1; q < rgroups.size(); q++)
+                want_units[q] = std::max(1, (int)((double)std::max(budget, 0) * wg[q] / std::max(wrest, 1.0)));
         }
         for (size_t q = 0; q < rgroups.size(); q++) {
             ResGroup& rg = rgroups[q];
             const int maxc = std::max(1, resident_max_clusters(rg.cs, rg.smem));
-            const int share = std::max(1, (int)((double)h->nsm * wg[q] / std::max(wtot, 1.0) / rg.cs));
+            const int share = want_units[q];
             const int nu = std::max(1, std::min<int>({(int)rg.cl.size(), maxc, share}));
             std::vector<int> order = rg.cl;
             std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
@@ -626,9 +640,17 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 const double m = cs[c + 1] - cs[c];
                 const int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
                 lists[b].push_back(c);
-                load[b] += m * (m - 1);
+                // per-vector cost is dominated by the m-independent chained solve: weight by
+                // the number of vectors (m - 1), with a small m term for the passes
+                load[b] += (m - 1) * (1.0 + m / 32.0);
             }
             units[q] = nu;
+            if (getenv("TINV_DEBUG")) {
+                double mx = 0.0;
+                for (double v : load) mx = std::max(mx, v);
+                fprintf(stderr, "[tinv] resident group cs=%d clusters=%zu units=%d (maxc %d share %d) M2=%d smem=%zu max-load %.0f\n",
+                        rg.cs, rg.cl.size(), nu, maxc, share, rg.M2, rg.smem, mx);
+            }
             offs[q] = (int)img.size();
             int acc = 0;
             img.push_back(0);
