@@ -336,3 +336,56 @@ def test_row_split_virtual_ranks_full_size_cfg4(handle, torch):
     assert rc == 0 and st["ngroups"] == 2
     res, orth = invariants_gpu(torch, d, e, w, Zg)
     assert res <= 10.0 and orth <= 10.0
+
+
+# ------------------------------------------------------------------ resident (DSMEM) compact-WY path
+
+def _clustered(n, sizes, seed=3):
+    """Tridiagonal with planted Peters-Wilkinson clusters of the given sizes; the remaining
+    vectors form clusters of 3 or 6 (with n > 1000 every spectrum has clusters under the
+    1e-3 ||T||_1 rule).  Groups sit 1 apart, their members within 1e-7; e is tiny."""
+    rng = np.random.default_rng(seed)
+    groups = list(sizes)
+    rest = n - sum(sizes)
+    f = 3 if n <= 2500 else 6   # fewer than ~900 groups keep them 1e-3 ||T||_1 apart
+    groups += [f] * (rest // f) + ([rest % f] if rest % f else [])
+    rng.shuffle(groups)
+    d = np.concatenate([g + 1e-7 * rng.uniform(-1, 1, m) for g, m in enumerate(groups)])
+    e = 1e-9 * rng.uniform(-1, 1, n - 1)
+    return d, e, W.eigenvalues(d, e)
+
+
+@pytest.mark.parametrize("n,sizes", [(2000, [60, 33, 17, 9, 2]), (1999, [64, 5, 3]), (1501, [40, 12, 7]),
+                                     (4096, [48, 24, 2])])
+def test_resident_cluster_sizes(handle, torch, n, sizes):
+    """Clusters needing 1, 2, 4 and 8 CTAs of a thread-block cluster (m up to 64), odd n."""
+    d, e, w = _clustered(n, sizes)
+    cs = O.clusters(w, O.tnorm(d, e))
+    assert max(np.diff(cs)) == max(sizes)
+    Zg, Zo, rep = full_parity(handle, torch, d, e, w)
+    assert handle.stats()["resident_groups"] >= 1
+
+
+def test_resident_equals_streaming_path(handle, torch):
+    """The resident kernel and the streaming persistent kernel compute the same vectors (up to
+    rounding) on the many-small-clusters workload."""
+    d, e, w = W.problem("cfg2", 1200)
+    dev = torch.device("cuda:0")
+    Zr, rc = run_gpu(handle, torch, d, e, w)
+    assert handle.stats()["resident_groups"] >= 1
+    handle.set_resident(False)
+    try:
+        Zs, rc2 = run_gpu(handle, torch, d, e, w)
+        assert handle.stats()["resident_groups"] == 0
+    finally:
+        handle.set_resident(True)
+    assert rc == 0 and rc2 == 0
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zr.cpu().numpy(), Zs.cpu().numpy())
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+
+
+def test_resident_deterministic(handle, torch):
+    d, e, w = W.problem("cfg2")
+    Z1, _ = run_gpu(handle, torch, d, e, w)
+    Z2, _ = run_gpu(handle, torch, d, e, w)
+    assert torch.equal(Z1, Z2)
