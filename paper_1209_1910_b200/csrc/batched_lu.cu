@@ -22,6 +22,9 @@
 namespace tinv {
 
 constexpr int RB = 16;   // rows per stage
+// start-vector ring of the factor sweep (producer warp -> solver warp), aliased onto the
+// stage buffers (unused until the first back substitution): kRG slots of RR rows x 32 lanes
+constexpr int RR = 32, kRG = 4;
 // pipeline stages: deep when the grid has at most one warp per SM (small n, latency-bound),
 // shallow when several warps share an SM
 constexpr int NS_DEEP = 8, NS_SHALLOW = 2;
@@ -45,28 +48,56 @@ __device__ __forceinline__ void stage_bulk(Stage& S, uint64_t* bar, int na, cons
     if (pbase) bulk_g2s(&S.pv[dst_row0][0], pbase + lo * 32, rows * 32u, bar);
 }
 
+// barriers: NS stage slots, d/e staging, kRG full + kRG empty ring slots, producer done
 template <int NS>
-__global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
+constexpr int kBars = NS + 1 + 2 * kRG + 1;
+template <int NS>
+constexpr size_t smem_fixed() { return sizeof(Stage) * NS + ((8 * kBars<NS> + 15) & ~size_t(15)); }
+
+// Reciprocal of a pivot (|u| in [eps ||T||_1, ~||T||_1], never subnormal or infinite): the
+// hardware approximation refined by two Newton steps (error far below one ulp of the
+// factorisation's own rounding), without the IEEE division's slow-path branch.
+__device__ __forceinline__ double rcp_pivot(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+template <int NS>
+__global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
     extern __shared__ __align__(128) unsigned char bl_smem[];
+    static_assert(sizeof(Stage) * NS >= sizeof(double) * (RR * kRG + 1) * 32, "start-vector ring exceeds the stages");
     Stage* stages = reinterpret_cast<Stage*>(bl_smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(bl_smem + sizeof(Stage) * NS);
+    uint64_t* rfull = bars + NS + 1;
+    uint64_t* rempty = rfull + kRG;
+    uint64_t* rdone = rempty + kRG;
+    double* ring = reinterpret_cast<double*>(bl_smem);
     // small n: d and e staged in shared memory (every warp walks them once per factor sweep;
     // from a cold L1 each 128-byte line would be an L2 round trip next to the dependent chain)
-    double* sde = reinterpret_cast<double*>(bl_smem + sizeof(Stage) * NS + 8 * (NS + 2));
-    const int lane = threadIdx.x;
-    const int64_t j0 = (int64_t)blockIdx.x * 32;
-    const int64_t j = j0 + lane;
+    double* sde = reinterpret_cast<double*>(bl_smem + smem_fixed<NS>());
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;   // 0: solver; 1: start-vector producer (factor sweep only)
     const int64_t n = a.n;
-    const bool live = j < n;
-    const int64_t jj = live ? j : n - 1;          // dead lanes shadow a live vector (no stores)
+    // this warp's class (prep.cu slot permutation): slots < nc_pad iterate to convergence
+    const int64_t ncp = __ldcg(&a.out->nc_pad);
+    const bool iter_warp = (int64_t)blockIdx.x * 32 < ncp;
+    if ((a.mode == 1 && iter_warp) || (a.mode == 2 && !iter_warp)) return;
+    const int64_t j = a.perm[(int64_t)blockIdx.x * 32 + lane];
+    const bool live = j >= 0;
+    if (!__any_sync(0xffffffffu, live)) return;
+    const int64_t jj = live ? j : 0;              // dead lanes shadow vector 0 (no stores)
     const double shift = a.wt[jj];
-    const int p = a.jc[jj];
+    const int p = iter_warp ? 0 : 1;              // 0: iterate; 1: hand x^(1) on
     const double tnorm = __ldcg(&a.out->tnorm);   // written by the prep kernel (same stream)
     if (a.out->bad) return;                       // invalid input: nothing is computed
     double tiny = kEps * tnorm;
     if (tiny == 0.0) tiny = 2.2250738585072014e-308;
     const double thr = sqrt(0.1 / (double)n);
-    // this warp's block of rows (block-row layout, common.cuh bix)
+    // this warp's block of rows (block-row layout over slots, common.cuh bix)
     const int64_t boff = (int64_t)blockIdx.x * n * 32;
     double* __restrict__ X = a.X + boff;
     double* __restrict__ FL = a.fl + boff;
@@ -75,20 +106,59 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     double* __restrict__ FC = a.fc + boff;
     int8_t* __restrict__ FPv = a.fp + boff;
     const bool stage_de = a.stage_de != 0;
-    if (lane == 0) {
+    // d staged at sde[0, n2), e at sde[n2, n2 + n) with e[n-1] = 0 (the factor sweep's
+    // enext past the last row); the bulk copies move whole 16-byte pairs inside the arrays
+    const int64_t n2 = (n + 1) & ~int64_t(1);
+    const int64_t dpairs = n & ~int64_t(1), epairs = (n - 1) & ~int64_t(1);
+    if (threadIdx.x == 0) {
         for (int s = 0; s < NS + 1; s++) mbar_init(bars + s, 1);
+        for (int s = 0; s < kRG; s++) {
+            mbar_init(rfull + s, 32);
+            mbar_init(rempty + s, 1);
+        }
+        mbar_init(rdone, 32);
         fence_mbar_init();
         if (stage_de) {
-            const uint32_t bd = (uint32_t)(((n + 1) & ~int64_t(1)) * 8), be = (uint32_t)((n & ~int64_t(1)) * 8);
-            mbar_expect_tx(bars + NS, bd + be);
-            bulk_g2s(sde, a.d, bd, bars + NS);
-            if (be) bulk_g2s(sde + ((n + 1) & ~int64_t(1)), a.e, be, bars + NS);
+            mbar_expect_tx(bars + NS, (uint32_t)((dpairs + epairs) * 8));
+            if (dpairs) bulk_g2s(sde, a.d, (uint32_t)(dpairs * 8), bars + NS);
+            if (epairs) bulk_g2s(sde + n2, a.e, (uint32_t)(epairs * 8), bars + NS);
         }
     }
-    __syncwarp();
-    if (stage_de) mbar_wait(bars + NS, 0);
+    __syncthreads();
+
+    // ---------------- start-vector producer (warp 1): b_i = U(-1,1)(seed, j, i) for rows
+    // 1..n-1 of the factor sweep into the ring, and ||b||_1 over those rows
+    const int64_t nrow = n - 1;
+    if (wid == 1) {
+        double bsum = 0.0;
+        int64_t k = 0;
+        for (int64_t i0 = 0; i0 < nrow; i0 += RR, k++) {
+            const int slot = (int)(k % kRG);
+            if (k >= kRG) mbar_wait(rempty + slot, (uint32_t)((k / kRG - 1) & 1));
+            double* rb = ring + (size_t)slot * RR * 32;
+            const int cnt = (int)(nrow - i0 < RR ? nrow - i0 : RR);
+            for (int r = 0; r < cnt; r++) {
+                const double v = start_entry(a.seed, n, jj, 0, i0 + r + 1);
+                rb[r * 32 + lane] = v;
+                bsum += fabs(v);
+            }
+            mbar_arrive(rfull + slot);
+        }
+        ring[(size_t)kRG * RR * 32 + lane] = bsum;   // just past the ring (inside the stages)
+        mbar_arrive(rdone);
+        return;
+    }
+    if (stage_de) {
+        mbar_wait(bars + NS, 0);
+        if (lane == 0) {   // odd tails and the zero pad
+            if (dpairs < n) sde[n - 1] = a.d[n - 1];
+            if (epairs < n - 1) sde[n2 + n - 2] = a.e[n - 2];
+            sde[n2 + n - 1] = 0.0;
+        }
+        __syncwarp();
+    }
     const double* __restrict__ dd = stage_de ? sde : a.d;
-    const double* __restrict__ ee = stage_de ? sde + ((n + 1) & ~int64_t(1)) : a.e;
+    const double* __restrict__ ee = stage_de ? sde + n2 : a.e;
     uint32_t ph = 0;
     // optional sweep timers (warp 0, lane 0; globaltimer ns): factor+fwd, back 1, fwd 2, back 2
     const bool timing = a.prof && blockIdx.x == 0 && lane == 0;
@@ -107,19 +177,25 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
         double qq = (n > 1) ? ee[0] : 0.0;
         double c = start_entry(a.seed, n, jj, 0, 0);
         b1 = fabs(c);
+        int64_t k = 0;
+        for (int64_t i0 = 0; i0 < nrow; i0 += RR, k++) {
+          const int slot = (int)(k % kRG);
+          mbar_wait(rfull + slot, (uint32_t)((k / kRG) & 1));
+          const double* rb = ring + (size_t)slot * RR * 32;
+          const int cnt = (int)(nrow - i0 < RR ? nrow - i0 : RR);
 #pragma unroll 4
-        for (int64_t i = 0; i < n - 1; i++) {
+          for (int rr = 0; rr < cnt; rr++) {
+            const int64_t i = i0 + rr;
             const double sub = ee[i];
             const double anext = dd[i + 1] - shift;
-            const double enext = (i + 1 < n - 1) ? ee[i + 1] : 0.0;
-            const double bn = start_entry(a.seed, n, jj, 0, i + 1);
-            b1 += fabs(bn);
+            const double enext = stage_de ? ee[i + 1] : ((i + 1 < n - 1) ? ee[i + 1] : 0.0);
+            const double bn = rb[rr * 32 + lane];
             double u0, u1, u2, l, y;
             int8_t sw;
             // one reciprocal per row on the dependent chain (l = other * (1/pivot))
             const bool swp = fabs(sub) > fabs(pp);
             u0 = pivot_floor(swp ? sub : pp, tiny);
-            const double r = 1.0 / u0;
+            const double r = rcp_pivot(u0);
             l = (swp ? pp : sub) * r;
             if (swp) {
                 u1 = anext;
@@ -138,14 +214,19 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
                 c = bn - l * c;
                 sw = 0;
             }
-            const int64_t o = i * 32 + lane;
+            const int64_t o = i * 32 + lane;   // dead lanes store too: their slots are unused
             __stcg(FL + o, l);
             FPv[o] = sw;
             __stcg(FR + o, r);
             __stcg(FB + o, u1 * r);
             __stcg(FC + o, u2 * r);
             __stcg(X + o, y);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(rempty + slot);
         }
+        mbar_wait(rdone, 0);
+        b1 += ring[(size_t)kRG * RR * 32 + lane];
         pv_last = pivot_floor(pp, tiny);
         const int64_t o = (n - 1) * 32 + lane;
         __stcg(FR + o, 1.0 / pv_last);
@@ -157,8 +238,10 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     const double unn = fabs(pv_last);
     if (live) a.unn[j] = unn;
     const double sfac = (double)n * tnorm * fmax(kEps, unn);
-    // generic writes above -> bulk (async proxy) reads below
+    // generic writes above -> bulk (async proxy) reads below; the ring's shared memory is
+    // reused by the stages (async-proxy writes after generic accesses)
     fence_proxy_async_global();
+    fence_proxy_async_smem();
     __syncwarp();
 
     // back substitution, in place: x_i = s y_i r_i - b_i x_{i+1} - c_i x_{i+2}; stage b holds
@@ -278,8 +361,9 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     back(sfac / b1, true, xinf, x1, x2, imax);
     tick();
     int its = 1;
-    // Vectors with j_c >= 1 hand x^(1) to the compact-WY kernel.  The warp keeps sweeping
-    // while any lane still iterates; lanes that are done run the sweeps without storing.
+    // Vectors with j_c >= 1 (and, with handover, the leaders of resident clusters) hand x^(1)
+    // to the compact-WY kernels: their warps stop here.  Iterating warps keep sweeping while
+    // any lane still iterates; lanes that are done run the sweeps without storing.
     const bool active = live && p == 0;
     int passes = (xinf >= thr) ? 1 : 0;
     bool want = active && passes < kPasses && its < kMaxIts;
@@ -308,33 +392,33 @@ __global__ void __launch_bounds__(32) batched_lu_kernel(BatchedArgs a) {
     a.iters[j] = its;
 }
 
-// Per-vector contiguous copy of the factors of clustered vectors (j_c >= 1) for the chained
-// solves of the compact-WY kernel: F[j][i] = (l_i, 1/u0_i, u1_i/u0_i, u2_i/u0_i), the pivot
-// byte, and the first iterate x^(1) (contiguous per vector, so the compact-WY passes can
-// bulk-copy it), via 32x32 shared-memory tiles (coalesced on both sides).
+// Per-vector contiguous copy of the factors of the first-solve vectors (slots >= nc_pad: j_c >= 1
+// and handed-over leaders) for the chained solves of the compact-WY kernels:
+// F[j][i] = (l_i, 1/u0_i, u1_i/u0_i, u2_i/u0_i), the pivot byte, and the first iterate x^(1)
+// (contiguous per vector, so the compact-WY passes can bulk-copy it), via 32x32 shared-memory
+// tiles (coalesced on both sides).
 __global__ void pack_factors_kernel(PackArgs a) {
     __shared__ double tile[5][32][33];
     __shared__ int8_t ptile[32][33];
-    __shared__ int any;
-    const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+    __shared__ int vec[32];
+    const int64_t s0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+    if (s0 < __ldcg(&a.out->nc_pad)) return;   // iterating warp: nothing to pack
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-    if (tx == 0 && ty == 0) any = 0;
+    if (ty == 0) vec[tx] = a.perm[s0 + tx];
     __syncthreads();
-    if (ty == 0 && j0 + tx < a.n && a.jc[j0 + tx] != 0) any = 1;
-    __syncthreads();
-    if (!any) return;
+    if (vec[0] < 0 && !__syncthreads_or(vec[tx] >= 0)) return;
     const double* src[5] = {a.fl, a.fr, a.fb, a.fc, a.X};
     for (int r = ty; r < 32; r += 8) {
-        const int64_t i = i0 + r, j = j0 + tx;
-        const bool ok = i < a.n && j < a.n;
-        for (int c = 0; c < 5; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + bix(i, j, a.n)) : 0.0;
-        ptile[r][tx] = ok ? a.fp[bix(i, j, a.n)] : (int8_t)0;
+        const int64_t i = i0 + r;
+        const bool ok = i < a.n;
+        for (int c = 0; c < 5; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + bix(i, s0 + tx, a.n)) : 0.0;
+        ptile[r][tx] = ok ? a.fp[bix(i, s0 + tx, a.n)] : (int8_t)0;
     }
     __syncthreads();
-    // write: vector j0+r, rows i0..i0+31 -> 32 x 4 doubles contiguous (1 KB)
+    // write: vector of slot s0+r, rows i0..i0+31 -> 32 x 4 doubles contiguous (1 KB)
     for (int r = ty; r < 32; r += 8) {
-        const int64_t j = j0 + r;
-        if (j >= a.n || a.jc[j] == 0) continue;
+        const int64_t j = vec[r];
+        if (j < 0) continue;
         const int64_t i = i0 + tx;
         if (i < a.n) {
             double* dst = a.F + (j * a.n + i) * 4;
@@ -347,24 +431,27 @@ __global__ void pack_factors_kernel(PackArgs a) {
 }
 
 void launch_pack(const PackArgs& a, cudaStream_t s) {
-    dim3 grid((unsigned)((a.n + 31) / 32), (unsigned)((a.n + 31) / 32));
+    dim3 grid((unsigned)(batched_slot_cap(a.n) / 32), (unsigned)((a.n + 31) / 32));
     pack_factors_kernel<<<grid, dim3(32, 8), 0, s>>>(a);
 }
 
-// Tiled transpose + scale of finished iterates into column-major Z (j_c == 0 vectors).
+// Tiled transpose + scale of finished iterates (slots < nc_pad) into column-major Z.
 __global__ void finalize_kernel(FinalizeArgs a) {
     __shared__ double tile[32][33];
+    __shared__ int vec[32];
     if (a.out->bad || a.out->tnorm == 0.0) return;   // invalid input / Z = I (host handles)
-    const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+    const int64_t s0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+    if (s0 >= __ldcg(&a.out->nc_pad)) return;
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    if (ty == 0) vec[tx] = a.perm[s0 + tx];
     for (int r = ty; r < 32; r += 8) {
-        int64_t i = i0 + r, j = j0 + tx;
-        tile[r][tx] = (i < a.n && j < a.n) ? a.X[bix(i, j, a.n)] : 0.0;
+        const int64_t i = i0 + r;
+        tile[r][tx] = (i < a.n) ? a.X[bix(i, s0 + tx, a.n)] : 0.0;
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
-        int64_t j = j0 + r, i = i0 + tx;
-        if (j < a.n && i < a.n && a.jc[j] == 0) a.Z[j * a.ldz + i] = tile[tx][r] * a.zscale[j];
+        const int64_t j = vec[r], i = i0 + tx;
+        if (j >= 0 && i < a.n) a.Z[j * a.ldz + i] = tile[tx][r] * a.zscale[j];
     }
 }
 
@@ -374,26 +461,28 @@ __global__ void identity_kernel(double* Z, int64_t n, int64_t ldz) {
         Z[j * ldz + i] = (i == j) ? 1.0 : 0.0;
 }
 
+int64_t batched_slot_cap(int64_t n) { return (n + 31) / 32 * 32 + 32; }
+
 void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm) {
-    int64_t nb = (a.n + 31) / 32;
+    const int64_t nb = batched_slot_cap(a.n) / 32;
     BatchedArgs b = a;
     if (nb <= nsm) {
-        const size_t de = (size_t)(((a.n + 1) & ~int64_t(1)) + (a.n & ~int64_t(1))) * 8;
-        size_t sm = sizeof(Stage) * NS_DEEP + 8 * (NS_DEEP + 2);
+        const size_t de = (size_t)(((a.n + 1) & ~int64_t(1)) + a.n) * 8;
+        size_t sm = smem_fixed<NS_DEEP>();
         b.stage_de = (sm + de <= 200 * 1024) ? 1 : 0;
         if (b.stage_de) sm += de;
         cudaFuncSetAttribute(batched_lu_kernel<NS_DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        batched_lu_kernel<NS_DEEP><<<(unsigned)nb, 32, sm, s>>>(b);
+        batched_lu_kernel<NS_DEEP><<<(unsigned)nb, 64, sm, s>>>(b);
     } else {
         b.stage_de = 0;
-        const size_t sm = sizeof(Stage) * NS_SHALLOW + 8 * (NS_SHALLOW + 2);
+        const size_t sm = smem_fixed<NS_SHALLOW>();
         cudaFuncSetAttribute(batched_lu_kernel<NS_SHALLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 32, sm, s>>>(b);
+        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 64, sm, s>>>(b);
     }
 }
 
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
-    dim3 grid((unsigned)((a.n + 31) / 32), (unsigned)((a.n + 31) / 32));
+    dim3 grid((unsigned)(batched_slot_cap(a.n) / 32), (unsigned)((a.n + 31) / 32));
     finalize_kernel<<<grid, dim3(32, 8), 0, s>>>(a);
 }
 

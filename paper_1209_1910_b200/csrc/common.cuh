@@ -127,9 +127,10 @@ __device__ __forceinline__ void group_sync(GroupBarrier* b, int G, unsigned int&
 }
 
 // ---------------------------------------------------------------- batched (per-vector) arrays
-// Factors and iterates of the batched solve: blocks of 32 vectors (one warp), each block
-// row-major [row i][lane] (256 B per row), blocks one after the other: element (i, j) at
-// ((j / 32) n + i) 32 + j % 32.  A warp's rows [a, b) are one contiguous span.
+// Factors and iterates of the batched solve: blocks of 32 slots (one warp; vector perm[slot],
+// prep.cu), each block row-major [row i][lane] (256 B per row), blocks one after the other:
+// element (i, slot) at ((slot / 32) n + i) 32 + slot % 32.  A warp's rows [a, b) are one
+// contiguous span.
 __host__ __device__ __forceinline__ int64_t bix(int64_t i, int64_t j, int64_t n) {
     return ((j >> 5) * n + i) * 32 + (j & 31);
 }

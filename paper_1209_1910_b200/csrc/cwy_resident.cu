@@ -21,9 +21,10 @@
 //   TN  that = -t T_p s, x' = T_p Y[p,:]^T + y0 that (the T_j erratum fix), column p of T, Y
 //   D   q = Y_{p+1} x' - e_p, norms/argmax, forward-sweep chunk maps
 //   TEST, then either z_j = q/||q|| or the chained solve: exact forward carries from the
-//   composed maps -> t rows (gathered in CTA 0), serial back sweep by one thread of CTA 0
-//   (factor records streamed by TMA) in place over t, then every CTA copies its x rows, while
-//   every other warp computes the look-ahead pass A of vector p+1.
+//   composed maps -> t rows (gathered in CTA 0), back substitution in CTA 0 (factor records
+//   staged in shared memory by all its threads, then one thread's dependent chain), then
+//   every CTA copies its x rows, while every other warp computes the look-ahead pass A of
+//   vector p+1.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -36,8 +37,6 @@ namespace res {
 
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
-constexpr int CH = 256;          // back-sweep ring chunk (rows)
-constexpr int kRing = 4;         // back-sweep ring depth
 constexpr int kXS = 16;          // scalar slots of the exchange area
 enum { U2 = 0, X2 = 1, U0 = 2, Q2 = 3, QINF = 4, QARG = 5, Q1 = 6, FA = 7, FB = 8, X2N = 9, GPN = 10 };
 
@@ -72,16 +71,16 @@ struct L {        // shared-memory carve-up (doubles unless noted)
     double* yrow;
     double* PX;   // 2 x (M2 + kXS): exchange (double-buffered)
     double* PXL;  // M2 + kXS: look-ahead exchange
-    double* tf;   // n + 2: t rows gathered for the back sweep (CTA 0)
-    double* ring; // kRing x 4 CH: factor records of the back sweep
+    double* tf;   // n + 2: t rows gathered for the back sweep (CTA 0), x written in place
+    double* bc;   // 2 n: (u1/u0, u2/u0) of every row, staged by CTA 0 for the back sweep
     double* red;  // NW + 8
     double2* acc; // NT
     uint64_t* mbar;
 };
 
 __host__ __device__ inline size_t smem_doubles(int64_t n, int RL, int M2) {
-    return (size_t)RL * (M2 + 4) + (size_t)M2 * M2 + 5 * (size_t)(M2 + 2) + 3 * (size_t)(M2 + kXS) + (n + 2) +
-           (size_t)kRing * 4 * CH + (NW + 8) + 2 * NT + kRing + 8;
+    return (size_t)RL * (M2 + 4) + (size_t)M2 * M2 + 5 * (size_t)(M2 + 2) + 3 * (size_t)(M2 + kXS) +
+           (n + 2) + 2 * (size_t)n + 2 + (NW + 8) + 2 * NT + 8;
 }
 
 // block-wide exclusive scan of affine maps (thread order), total returned
@@ -142,69 +141,53 @@ __device__ void colacc_local(const L& sm, int M2, int r0, int a, int b, int P, C
     sync();
 }
 
-// Chained back substitution x_i = t_i - b_i x_{i+1} - c_i x_{i+2} (rows n-1 .. 0) by the
-// calling thread, in place over t (shared memory): t_i is read before x_i overwrites it.
-// Factor records (l, 1/u0, b, c) stream through a kRing-deep TMA ring; the loop keeps the
-// next 8 rows' shared-memory loads ahead of the dependent chain (13 cycles/row on B200,
-// tools/micro/chain.cu).
-__device__ void back_sweep_inplace(const double* __restrict__ F, double* tf, int64_t n, double* ring, uint64_t* mbar,
-                                   uint32_t& mbph) {
-    const int64_t C = (n + CH - 1) / CH;
-    fence_proxy_async_global();
-    auto issue = [&](int64_t k) {
-        const int slot = (int)(k % kRing);
-        const int64_t c = C - 1 - k;
-        const int64_t lo = c * CH, hi = min64(lo + CH, n);
-        mbar_expect_tx(mbar + slot, (uint32_t)((hi - lo) * 32));
-        bulk_g2s(ring + (int64_t)slot * 4 * CH, F + lo * 4, (uint32_t)((hi - lo) * 32), mbar + slot);
-    };
-    for (int64_t k = 0; k < C && k < kRing; k++) issue(k);
+// Back substitution x_i = t_i - b_i x_{i+1} - c_i x_{i+2} (rows n-1 .. 0; the row-normalised
+// U of the chained solve), in place over t.  The recurrence stays sequential: expanding it
+// over blocks of rows multiplies the b, c of neighbouring rows, which for nearly decoupled
+// blocks (pivots ~ eps ||T||, |b| ~ 1e11 in glued Wilkinson matrices) cancels catastrophically.
+// All threads of CTA 0 first stage (b, c) of every row into shared memory (back_stage); then
+// one thread runs the chain from shared memory with the next 8 rows' loads ahead of it
+// (back_sweep_smem).
+__device__ void back_stage(const double* __restrict__ F, double* bc, int64_t n) {
+    for (int64_t i = threadIdx.x; i < n; i += NT)
+        reinterpret_cast<double2*>(bc)[i] = __ldg(reinterpret_cast<const double2*>(F + i * 4 + 2));
+}
+__device__ void back_sweep_smem(const double* __restrict__ bc, double* tf, int64_t n) {
+    const double2* BC = reinterpret_cast<const double2*>(bc);
     double x1 = 0.0, x2 = 0.0;
-    for (int64_t k = 0; k < C; k++) {
-        const int slot = (int)(k % kRing);
-        mbar_wait(mbar + slot, (mbph >> slot) & 1u);
-        mbph ^= 1u << slot;
-        const double* Fs = ring + (int64_t)slot * 4 * CH;
-        const int64_t lo = (C - 1 - k) * CH, hi = min64(lo + CH, n);
-        double* Ts = tf + lo;
-        const int cnt = (int)(hi - lo);
-        const int top = cnt & ~7;
-        for (int u = cnt - 1; u >= top; u--) {
-            const double2 bc = *reinterpret_cast<const double2*>(Fs + u * 4 + 2);
-            const double xi = fma(-bc.x, x1, fma(-bc.y, x2, Ts[u]));
-            Ts[u] = xi;
+    const int64_t top = n & ~int64_t(7);
+    for (int64_t u = n - 1; u >= top; u--) {
+        const double2 v = BC[u];
+        const double xi = fma(-v.x, x1, fma(-v.y, x2, tf[u]));
+        tf[u] = xi;
+        x2 = x1;
+        x1 = xi;
+    }
+    if (top == 0) return;
+    double b[8], c[8], t[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        const double2 v = BC[top - 8 + u];
+        b[u] = v.x; c[u] = v.y; t[u] = tf[top - 8 + u];
+    }
+    for (int64_t u0 = top - 8; u0 >= 0; u0 -= 8) {
+        double bn[8], cn[8], tn[8], xv[8];
+        const int64_t nx = u0 >= 8 ? u0 - 8 : 0;
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const double2 v = BC[nx + u];
+            bn[u] = v.x; cn[u] = v.y; tn[u] = tf[nx + u];
+        }
+#pragma unroll
+        for (int u = 7; u >= 0; u--) {
+            xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u]));
             x2 = x1;
-            x1 = xi;
+            x1 = xv[u];
         }
-        if (top > 0) {
-            double b[8], c[8], t[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const double2 bc = *reinterpret_cast<const double2*>(Fs + (top - 8 + u) * 4 + 2);
-                b[u] = bc.x; c[u] = bc.y; t[u] = Ts[top - 8 + u];
-            }
-            for (int u0 = top - 8; u0 >= 0; u0 -= 8) {
-                double bn[8], cn[8], tn[8], xv[8];
-                const int nx = u0 >= 8 ? u0 - 8 : 0;
+        for (int u = 0; u < 8; u += 2) *reinterpret_cast<double2*>(tf + u0 + u) = make_double2(xv[u], xv[u + 1]);
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const double2 bc = *reinterpret_cast<const double2*>(Fs + (nx + u) * 4 + 2);
-                    bn[u] = bc.x; cn[u] = bc.y; tn[u] = Ts[nx + u];
-                }
-#pragma unroll
-                for (int u = 7; u >= 0; u--) {
-                    xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u]));
-                    x2 = x1;
-                    x1 = xv[u];
-                }
-#pragma unroll
-                for (int u = 0; u < 8; u += 2)
-                    *reinterpret_cast<double2*>(Ts + u0 + u) = make_double2(xv[u], xv[u + 1]);
-#pragma unroll
-                for (int u = 0; u < 8; u++) { b[u] = bn[u]; c[u] = cn[u]; t[u] = tn[u]; }
-            }
-        }
-        if (k + kRing < C) issue(k + kRing);
+        for (int u = 0; u < 8; u++) { b[u] = bn[u]; c[u] = cn[u]; t[u] = tn[u]; }
     }
 }
 
@@ -235,19 +218,14 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         sm.yrow = p; p += M2 + 2;
         sm.PX = p; p += 2 * (M2 + kXS);
         sm.PXL = p; p += M2 + kXS;
-        sm.tf = p; p += n + 2;
         p += (reinterpret_cast<uintptr_t>(p) & 15) ? 1 : 0;
-        sm.ring = p; p += kRing * 4 * CH;
+        sm.tf = p; p += (n + 2 + 1) & ~int64_t(1);
+        sm.bc = p; p += 2 * n;
         sm.red = p; p += NW + 8;
         sm.acc = reinterpret_cast<double2*>(p); p += 2 * NT;
         sm.mbar = reinterpret_cast<uint64_t*>(p);
     }
-    if (tid == 0) {
-        for (int k = 0; k < kRing; k++) mbar_init(sm.mbar + k, 1);
-        fence_mbar_init();
-    }
     __syncthreads();
-    uint32_t mbph = 0;
     const double thr = sqrt(0.1 / (double)n);
     // optional phase timers (unit 0, CTA 0, thread 0; globaltimer ns)
     const bool timing = a.prof && unit == 0 && crank == 0 && tid == 0;
@@ -280,12 +258,134 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         const int64_t j1 = a.cstart[clid];
         const int m = (int)(a.cstart[clid + 1] - j1);
 
+        // ================= leader z_{j1} (handover): plain inverse iteration from x^(1), the
+        // batched LU's stopping rule (||x||_inf >= sqrt(0.1/n) twice, MAXITS) and chained solves
+        // with its factors (Alg. 4 l.5-7 and l.20; the same arithmetic as batched_lu.cu)
+        double lscl = 0.0;
+        if (a.handover) {
+            const int64_t j = j1;
+            const double* Fj = a.F + j * n * 4;
+            const int8_t* FPj = a.FP + j * n;
+            if (crank == 0 && tid == 0)
+                for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
+            {
+                const double* x1 = a.X1c + j * n2v;
+                for (int i = tid; i < nl; i += NT) sm.ql[i] = __ldcg(x1 + r0 + i);
+            }
+            const int s0 = max(0, r0 - 1), s1 = (int)min64(r1 - 1, n - 1);
+            const int FL = s1 > s0 ? (s1 - s0 + NT - 1) / NT : 0;
+            const int fta = s0 + min(max(s1 - s0, 0), tid * FL), ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FL);
+            int its = 1, passes = 0;
+            __syncthreads();
+            while (true) {
+                // norms and argmax of the iterate, forward maps of its next solve
+                double* px = sm.PX + pxb * (M2 + kXS);
+                double q2 = 0.0, q1 = 0.0, qinf = -1.0;
+                int64_t qarg = 0;
+                for (int i = tid; i < nl; i += NT) {
+                    const double qi = sm.ql[i];
+                    q2 = fma(qi, qi, q2);
+                    const double aq = fabs(qi);
+                    q1 += aq;
+                    if (aq > qinf) { qinf = aq; qarg = r0 + i; }
+                }
+                q2 = block_sum_(q2, sm.red);
+                q1 = block_sum_(q1, sm.red);
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double oq = __shfl_xor_sync(0xffffffffu, qinf, o);
+                    const long long oa = __shfl_xor_sync(0xffffffffu, (long long)qarg, o);
+                    if (oq > qinf || (oq == qinf && oa < qarg)) { qinf = oq; qarg = oa; }
+                }
+                if (lane == 0) sm.acc[warp] = make_double2(qinf, (double)qarg);
+                __syncthreads();
+                if (tid == 0) {
+                    for (int w = 1; w < NW; w++) {
+                        const double2 t = sm.acc[w];
+                        if (t.x > qinf || (t.x == qinf && (int64_t)t.y < qarg)) { qinf = t.x; qarg = (int64_t)t.y; }
+                    }
+                    px[M2 + Q2] = q2;
+                    px[M2 + Q1] = q1;
+                    px[M2 + QINF] = qinf;
+                    px[M2 + QARG] = (double)qarg;
+                }
+                Aff f{1.0, 0.0};
+                for (int s = fta; s < ftb; s++) {
+                    const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
+                    if (FPj[s]) f.b = fma(-l, bn, f.b);
+                    else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
+                }
+                Aff tot;
+                const Aff fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
+                if (tid == 0) { px[M2 + FA] = tot.a; px[M2 + FB] = tot.b; }
+                cl.sync();
+                const double q2t = csum(pxb, Q2);
+                qinf = -1.0;
+                qarg = 0;
+                for (int c2 = 0; c2 < CS; c2++) {
+                    const double v = PXo(c2, pxb)[M2 + QINF];
+                    const int64_t ia = (int64_t)PXo(c2, pxb)[M2 + QARG];
+                    if (v > qinf || (v == qinf && ia < qarg)) { qinf = v; qarg = ia; }
+                }
+                if (qinf >= thr) passes++;
+                if (passes >= kPasses || its >= kMaxIts) {
+                    const int own = (int)(qarg / RL);
+                    const double sgn = (cl.map_shared_rank(sm.ql, own)[qarg - (int64_t)own * RL] < 0.0) ? -1.0 : 1.0;
+                    lscl = sgn / sqrt(q2t);
+                    double* zj = a.Z + j * a.ldz;
+                    for (int i = tid; i < nl; i += NT) zj[r0 + i] = sm.ql[i] * lscl;
+                    if (crank == 0 && tid == 0) {
+                        a.iters[j] = its;
+                        if (passes < kPasses) atomicAdd(&a.out->nflag, 1);
+                    }
+                    pxb ^= 1;
+                    cl.sync();
+                    break;
+                }
+                its++;
+                {   // forward pass 2: exact carries -> t rows in CTA 0; scale sigma / ||x||_1
+                    Aff pre{1.0, 0.0};
+                    for (int c2 = 0; c2 < crank; c2++)
+                        pre = comp(Aff{PXo(c2, pxb)[M2 + FA], PXo(c2, pxb)[M2 + FB]}, pre);
+                    const double q0 = cl.map_shared_rank(sm.ql, 0)[0];
+                    double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
+                    const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(pxb, Q1);
+                    double* tf0 = cl.map_shared_rank(sm.tf, 0);
+                    for (int s = fta; s < ftb; s++) {
+                        const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
+                        const double rr = __ldg(Fj + (int64_t)s * 4 + 1);
+                        double y;
+                        if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
+                        else { y = cc; cc = fma(-l, cc, bn); }
+                        tf0[s] = sc * y * rr;
+                    }
+                    if (ftb == n - 1 && fta < ftb) {
+                        tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
+                    } else if (n == 1 && tid == 0) {
+                        tf0[0] = sc * cc * __ldg(Fj + 1);
+                    }
+                }
+                pxb ^= 1;
+                cl.sync();
+                if (crank == 0) {
+                    back_stage(Fj, sm.bc, n);
+                    __syncthreads();
+                    if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
+                }
+                cl.sync();
+                {
+                    const double* x0 = cl.map_shared_rank(sm.tf, 0);
+                    for (int i = tid; i < nl; i += NT) sm.ql[i] = x0[r0 + i];
+                }
+                cl.sync();
+            }
+        }
+
         // ================= first reflector from z_{j1}
         {
             const double* z = a.Z + j1 * a.ldz;
             double u2 = 0.0;
             for (int i = tid; i < nl; i += NT) {
-                const double zi = __ldcg(z + r0 + i);
+                const double zi = a.handover ? sm.ql[i] * lscl : __ldcg(z + r0 + i);
                 sm.ul[i] = zi;
                 u2 = fma(zi, zi, u2);
             }
@@ -444,14 +544,16 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     }
                     if (ftb == n - 1 && fta < ftb) {
                         tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
-                        tf0[n] = 0.0;
                     } else if (n == 1 && tid == 0) {
                         tf0[0] = sc * cc * __ldg(Fj + 1);
-                        tf0[1] = 0.0;
                     }
                     pxb ^= 1;   // the buffer used above is now the "previous" one
                     cl.sync();
-                    if (crank == 0 && tid == 0) back_sweep_inplace(a.F + j * n * 4, sm.tf, n, sm.ring, sm.mbar, mbph);
+                    if (crank == 0) {
+                        back_stage(a.F + j * n * 4, sm.bc, n);
+                        __syncthreads();
+                        if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
+                    }
                     cl.sync();
                     {   // every CTA takes its rows of x from CTA 0
                         const double* x0 = cl.map_shared_rank(sm.tf, 0);
@@ -613,14 +715,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         }
                         if (ftb == n - 1 && fta < ftb) {
                             tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
-                            tf0[n] = 0.0;
-                        }
+                            }
                     }
                     pxb ^= 1;
                     cl.sync();
                     PH(5);
                     const bool la = !la_done && p + 1 < m;
-                    if (crank == 0 && tid == 0) back_sweep_inplace(a.F + j * n * 4, sm.tf, n, sm.ring, sm.mbar, mbph);
+                    if (crank == 0) {
+                        back_stage(a.F + j * n * 4, sm.bc, n);
+                        __syncthreads();
+                        if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
+                    }
                     if (la) {
                         // look-ahead pass A of vector p+1 (every warp except CTA 0's warp 0):
                         // columns 0..p-1 of Y_{p+1} are final

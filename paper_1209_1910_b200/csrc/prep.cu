@@ -120,6 +120,58 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         nclustered += __shfl_xor_sync(0xffffffffu, nclustered, o);
     }
     if ((tid & 31) == 0) { atomicMax(&a.out->max_cluster, maxm); atomicAdd(&a.out->n_clustered, nclustered); }
+
+    // ---- slot permutation of the batched LU (tinv_internal.h PrepArgs): stable compaction
+    // of the vectors it iterates (class c) to the front, the first-solve vectors behind them
+    // from a warp boundary, so that every warp holds one class
+    __syncthreads();   // jc, cstart complete
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += kPrepThreads) {
+        const int64_t j = base + tid;
+        int cflag = 0;
+        if (j < n && a.jc[j] == 0) {
+            const int c = a.cid[j];
+            const int m = a.cstart[c + 1] - a.cstart[c];
+            cflag = !(a.handover && m >= 2 && m <= kNarrowM);
+        }
+        int v = cflag;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if ((tid & 31) >= o) v += t;
+        }
+        if ((tid & 31) == 31) sscan[tid >> 5] = v;
+        __syncthreads();
+        if (tid < 32) {
+            int s = sscan[tid];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, s, o);
+                if (tid >= o) s += t;
+            }
+            sscan[tid] = s;
+        }
+        __syncthreads();
+        const int incl = v + ((tid >> 5) > 0 ? sscan[(tid >> 5) - 1] : 0) + s_carry;
+        const int rc = incl - cflag;   // class-c vectors before j
+        // class c: its rank; first-solve: -(1 + its rank among them), resolved below
+        if (j < n) a.slot[j] = cflag ? rc : -(1 + (int)(j - rc));
+        __syncthreads();
+        if (tid == kPrepThreads - 1) s_carry = incl;
+        __syncthreads();
+    }
+    const int nc = s_carry;
+    const int ncp = (nc + 31) & ~31;
+    for (int64_t s = tid; s < a.nslot_cap; s += kPrepThreads) a.perm[s] = -1;
+    __syncthreads();
+    for (int64_t j = tid; j < n; j += kPrepThreads) {
+        int s = a.slot[j];
+        if (s < 0) s = ncp + (-s - 1);
+        a.slot[j] = s;
+        a.perm[s] = (int)j;
+    }
+    if (tid == 0) a.out->nc_pad = ncp;
 }
 
 void launch_prep(const PrepArgs& a, cudaStream_t s) {

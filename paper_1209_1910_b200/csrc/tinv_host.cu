@@ -76,7 +76,7 @@ struct tinv_s {
     double *wt = nullptr, *X = nullptr, *fl = nullptr, *fr = nullptr, *fb = nullptr, *fc = nullptr;
     double *unn = nullptr, *zscale = nullptr, *F = nullptr, *X1c = nullptr;
     int8_t *fp = nullptr, *FP = nullptr;
-    int *cstart = nullptr, *cid = nullptr, *jc = nullptr, *iters = nullptr;
+    int *cstart = nullptr, *cid = nullptr, *jc = nullptr, *iters = nullptr, *slot = nullptr, *perm = nullptr;
     PrepOut* out = nullptr;
     // cWY workspace (schedule-dependent)
     void* cw = nullptr;
@@ -90,6 +90,9 @@ struct tinv_s {
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
     int res_cs2 = 1000, res_cs4 = 1000;   // m from which a cluster gets >= 2 / 4 CTAs
+    int handover = 1;                 // narrow leaders finish in the resident kernel (n <= 2048)
+    double leader_w = 0.5;            // LPT weight of a handed-over leader (vector equivalents)
+    double lpt_m = 1.0;               // LPT weight per vector: 1 + lpt_m m / 32
     // row split over real ranks: peers' cWY workspaces mapped through CUDA IPC
     int* res_buf = nullptr;           // resident kernel unit lists (device)
     size_t res_cap = 0;
@@ -110,6 +113,8 @@ struct tinv_s {
     cudaStream_t rs[4] = {};          // resident-kernel launches (one per cluster size) run concurrently
     cudaEvent_t rev[5] = {};
     cudaEvent_t ev_prep = nullptr;
+    cudaStream_t bst = nullptr;       // handover: the iterating batched-LU warps + finalize
+    cudaEvent_t ev_b2 = nullptr;
     tinv_stats_t stats{};
 };
 
@@ -147,7 +152,7 @@ int ensure_base(tinv_s* h, int64_t n) {
     int64_t ldv = (n + 31) / 32 * 32;
     auto layout = [&](char* p) {
         Carve c{p};
-        size_t nn = (size_t)n * (size_t)ldv;
+        const size_t nn = (size_t)n * (size_t)batched_slot_cap(n);   // block-row layout over slots
         h->wt = c.take<double>(n);
         h->unn = c.take<double>(n);
         h->zscale = c.take<double>(n);
@@ -155,6 +160,8 @@ int ensure_base(tinv_s* h, int64_t n) {
         h->cid = c.take<int>(n);
         h->jc = c.take<int>(n);
         h->iters = c.take<int>(n);
+        h->slot = c.take<int>(n);
+        h->perm = c.take<int>(batched_slot_cap(n));
         h->out = c.take<PrepOut>(1);
         h->X = c.take<double>(nn);
         h->fl = c.take<double>(nn);
@@ -376,12 +383,17 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     CK(cudaMallocHost(&h->h_out, sizeof(PrepOut)));
     if (const char* v = getenv("TINV_RES_CS2")) h->res_cs2 = atoi(v);
     if (const char* v = getenv("TINV_RES_CS4")) h->res_cs4 = atoi(v);
+    if (const char* v = getenv("TINV_HANDOVER")) h->handover = atoi(v);
+    if (const char* v = getenv("TINV_LEADER_W")) h->leader_w = atof(v);
+    if (const char* v = getenv("TINV_LPT_M")) h->lpt_m = atof(v);
     CK(cudaMalloc(&h->bnd, 32 * sizeof(double)));   // [0,4) bisection bounds, [8,16) resident timers
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     for (auto& q : h->rs) CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
     for (auto& q : h->rev) CK(cudaEventCreateWithFlags(&q, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&h->bst, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_b2, cudaEventDisableTiming));
     if (h->nranks > 1) {
         if (!cfg->nccl_id || !g_nccl.load()) { delete h; return TINV_ERR_NCCL; }
         ncclUniqueId id;
@@ -412,6 +424,8 @@ int tinv_destroy(tinv_t h) {
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
     if (h->ev_prep) cudaEventDestroy(h->ev_prep);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->bst) cudaStreamDestroy(h->bst);
+    if (h->ev_b2) cudaEventDestroy(h->ev_b2);
     for (auto& q : h->rs) if (q) cudaStreamDestroy(q);
     for (auto& q : h->rev) if (q) cudaEventDestroy(q);
     delete h;
@@ -464,9 +478,19 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     // ---------------- prep, then (without waiting for the host) the batched LU, the
     // finalize of finished vectors and the factor/iterate packing of clustered vectors; the
     // cluster table is read back on a side stream meanwhile and scheduled on the host.
+    // Handover (n <= 2048, resident kernel on): the leaders of narrow clusters stop after
+    // x^(1) like the rest of their cluster and finish in the resident kernel, so the batched
+    // LU splits into two concurrent launches -- the first-solve warps (2 sweeps; the resident
+    // kernel waits only for them and the packing) and the iterating warps (singletons, other
+    // leaders; up to 2 MAXITS sweeps) with their finalize on a second stream.
+    const int handover = (h->resident && h->handover && n >= 2 && n <= 2048) ? 1 : 0;
+    auto join_b2 = [&]() -> int {
+        if (handover) CK(cudaStreamWaitEvent(st, h->ev_b2, 0));
+        return 0;
+    };
     ev_record(h, 0);
     CK(cudaMemsetAsync(h->out, 0, sizeof(PrepOut), st));
-    PrepArgs pa{n, d, e, w, h->wt, h->cstart, h->cid, h->jc, h->out};
+    PrepArgs pa{n, d, e, w, h->wt, h->cstart, h->cid, h->jc, h->slot, h->perm, batched_slot_cap(n), handover, h->out};
     launch_prep(pa, st);
     launches++;
     CK(cudaGetLastError());
@@ -476,19 +500,34 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, h->side));
     CK(cudaMemcpyAsync(h->h_cstart, h->cstart, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, h->side));
     ev_record(h, 2);
-    BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
+    BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, h->perm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
                    h->X, h->unn, h->zscale, h->iters, h->out,
-                   h->profiling ? reinterpret_cast<unsigned long long*>(h->bnd + 16) : nullptr};
-    launch_batched(ba, st, h->nsm);
-    launches++;
-    CK(cudaGetLastError());
-    ev_record(h, 3);
-    FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->jc, Z, ldz, h->out};
-    launch_finalize(fa, st);
-    launches++;
-    CK(cudaGetLastError());
-    ev_record(h, 4);
-    PackArgs pk{n, h->ldv, h->jc, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP, h->X, h->X1c};
+                   h->profiling ? reinterpret_cast<unsigned long long*>(h->bnd + 16) : nullptr, 0, 0};
+    FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->perm, Z, ldz, h->out};
+    PackArgs pk{n, h->ldv, h->perm, h->out, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP, h->X, h->X1c};
+    if (handover) {
+        CK(cudaStreamWaitEvent(h->bst, h->ev_prep, 0));
+        ba.mode = 2;
+        launch_batched(ba, h->bst, h->nsm);
+        launch_finalize(fa, h->bst);
+        CK(cudaEventRecord(h->ev_b2, h->bst));
+        ba.mode = 1;
+        ba.prof = nullptr;
+        launch_batched(ba, st, h->nsm);
+        launches += 2;
+        CK(cudaGetLastError());
+        ev_record(h, 3);
+        ev_record(h, 4);
+    } else {
+        launch_batched(ba, st, h->nsm);
+        launches++;
+        CK(cudaGetLastError());
+        ev_record(h, 3);
+        launch_finalize(fa, st);
+        launches++;
+        CK(cudaGetLastError());
+        ev_record(h, 4);
+    }
     launch_pack(pk, st);
     launches++;
     CK(cudaGetLastError());
@@ -496,6 +535,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     CK(cudaStreamSynchronize(h->side));
     const PrepOut po = *h->h_out;
     if (po.bad) {
+        if (join_b2()) return TINV_ERR_CUDA;
         CK(cudaStreamSynchronize(st));
         if (po.bad & 1) return -3;
         if (po.bad & 2) return -4;
@@ -507,6 +547,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     S.max_cluster = po.max_cluster;
     S.n_clustered = po.n_clustered;
     if (n == 1 || tnorm == 0.0) {
+        if (join_b2()) return TINV_ERR_CUDA;
         launch_identity(Z, n, ldz, st);
         launches++;
         CK(cudaGetLastError());
@@ -530,6 +571,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     if (smem > 232448 && nstg) { nstg = 0; smem = cwy_smem_bytes(vcap, 0); }
     if (po.n_clustered > 0 && smem > 232448) {
         fprintf(stderr, "[tinv] cluster of %d vectors exceeds the shared-memory staging limit\n", po.max_cluster);
+        join_b2();
         return TINV_ERR_DEVICE;
     }
     const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
@@ -577,6 +619,15 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             }
         }
         for (auto& rg : rgroups) rg.smem = resident_smem_bytes(n, rg.RL, rg.M2);
+        if (handover)   // the batched LU stopped every narrow leader: all of them must be resident
+            for (int c = rlo[h->rank]; c < rhi[h->rank]; c++) {
+                const int m = cs[c + 1] - cs[c];
+                if (m >= 2 && m <= cwy_narrow_max() && !resident[c]) {
+                    fprintf(stderr, "[tinv] narrow cluster of %d vectors does not fit the resident kernel\n", m);
+                    join_b2();
+                    return TINV_ERR_DEVICE;
+                }
+            }
         // the largest clusters first (longest dependent chains)
         std::sort(rgroups.begin(), rgroups.end(), [](const ResGroup& a, const ResGroup& b) { return a.cs > b.cs; });
     }
@@ -613,13 +664,14 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             double wrest = 0.0;
             for (size_t q = 0; q < rgroups.size(); q++) {
                 double vec = 0.0;
-                for (int c : rgroups[q].cl) vec += (double)(cs[c + 1] - cs[c] - 1);
+                for (int c : rgroups[q].cl) vec += (double)(cs[c + 1] - cs[c] - 1) + (handover ? h->leader_w : 0.0);
                 // measured: a unit spends about the same time per vector whatever its CTA
                 // count (fewer rows per CTA but more exchange), so SM-time ~ vectors x CTAs
                 wg[q] = vec;
                 if (q > 0) wrest += vec * rgroups[q].cs;
             }
-            int budget = h->nsm;
+            // SMs still held by the iterating batched-LU warps (handover: they run concurrently)
+            int budget = h->nsm - (handover ? po.nc_pad / 32 : 0);
             want_units[0] = std::max(1, std::min<int>((int)rgroups[0].cl.size(), budget / rgroups[0].cs));
             budget -= want_units[0] * rgroups[0].cs;
             for (size_t q = 1; q < rgroups.size(); q++)
@@ -642,7 +694,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 lists[b].push_back(c);
                 // per-vector cost is dominated by the m-independent chained solve: weight by
                 // the number of vectors (m - 1), with a small m term for the passes
-                load[b] += (m - 1) * (1.0 + m / 32.0);
+                load[b] += (m - 1) * (1.0 + h->lpt_m * m / 32.0) + (handover ? h->leader_w : 0.0);
             }
             units[q] = nu;
             if (getenv("TINV_DEBUG")) {
@@ -682,14 +734,29 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             ra.u_off = h->res_buf + offs[q];
             ra.u_list = h->res_buf + offs[q] + units[q] + 1;
             ra.X1c = h->X1c; ra.F = h->F; ra.FP = h->FP; ra.unn = h->unn; ra.Z = Z; ra.ldz = ldz;
-            ra.iters = h->iters; ra.out = h->out;
+            ra.iters = h->iters; ra.out = h->out; ra.handover = handover;
             ra.prof = (h->profiling && q == 0) ? reinterpret_cast<unsigned long long*>(h->bnd + 8) : nullptr;
             CK(launch_resident(ra, rg.cs, units[q], rg.smem, sq));
             launches++;
             CK(cudaEventRecord(h->rev[q], sq));
+            if (getenv("TINV_DEBUG") && q < 4) CK(cudaEventRecord(h->ev[10 + q], sq));
         }
         for (size_t q = 0; q < rgroups.size(); q++) CK(cudaStreamWaitEvent(st, h->rev[q], 0));
         S.ngroups += 0;
+    }
+    if (join_b2()) return TINV_ERR_CUDA;   // iterating warps + their finalize (handover)
+    if (getenv("TINV_DEBUG") && !rgroups.empty()) {
+        if (handover) CK(cudaEventRecord(h->ev[14], h->bst));
+        CK(cudaStreamSynchronize(st));
+        float t;
+        for (size_t q = 0; q < rgroups.size() && q < 4; q++) {
+            cudaEventElapsedTime(&t, h->ev[5], h->ev[10 + q]);
+            fprintf(stderr, "[tinv] resident group cs=%d ends %.3f ms after launch\n", rgroups[q].cs, t);
+        }
+        if (handover && cudaEventElapsedTime(&t, h->ev[5], h->ev[14]) == cudaSuccess)
+            fprintf(stderr, "[tinv] iterating batched warps + finalize end %.3f ms after it\n", t);
+        cudaEventElapsedTime(&t, h->ev[0], h->ev[5]);
+        fprintf(stderr, "[tinv] resident launch at %.3f ms\n", t);
     }
     if (!sc.size.empty()) {
         const int ng = (int)sc.size.size();

@@ -15,7 +15,8 @@ struct PrepOut {
     int max_cluster;
     int n_clustered;
     int nflag;          // vectors that missed the stopping rule
-    int pad[3];
+    int nc_pad;         // slots of the vectors the batched LU iterates, rounded up to 32
+    int pad[2];
 };
 
 struct PrepArgs {
@@ -27,6 +28,14 @@ struct PrepArgs {
     int* cstart;        // cluster starts (n+1)
     int* cid;           // cluster of each vector (n)
     int* jc;            // position inside its cluster (n)
+    // Slot permutation of the batched LU (warps hold 32 consecutive slots): the vectors it
+    // iterates to convergence (cluster leaders, singletons) take slots [0, nc), the rest
+    // (j_c >= 1, and leaders handed to the resident kernel) slots [nc_pad, nc_pad + n - nc);
+    // the gap and the tail are dead slots (perm = -1).  perm has nslot_cap entries.
+    int* slot;          // slot of each vector (n)
+    int* perm;          // vector of each slot, or -1
+    int64_t nslot_cap;  // roundup(n, 32) + 32
+    int handover;       // leaders of clusters with 2 <= m <= kNarrowM finish in the resident kernel
     PrepOut* out;
 };
 
@@ -39,8 +48,9 @@ struct BatchedArgs {
     const double* e;
     const double* wt;
     const int* jc;
+    const int* perm;    // vector of each slot (prep), -1 for dead slots
     uint64_t seed;
-    // factors, block-row layout (common.cuh bix)
+    // factors, block-row layout over slots (common.cuh bix(i, slot, n))
     double* fl;         // multipliers l_i (row i < n-1)
     int8_t* fp;         // row swap flags
     double* fr;         // 1/u0_i
@@ -53,12 +63,15 @@ struct BatchedArgs {
     PrepOut* out;
     unsigned long long* prof;   // optional sweep timers of warp 0 (ns), or NULL
     int stage_de;               // set by the launcher: d, e staged in shared memory
+    int mode;                   // 0: every warp; 1: only the first-solve warps (slots >= nc_pad);
+                                // 2: only the iterating warps (slots < nc_pad)
 };
 
 struct PackArgs {
     int64_t n;
     int64_t ldv;
-    const int* jc;
+    const int* perm;    // slots >= out->nc_pad are packed
+    const PrepOut* out;
     const double* fl;
     const double* fr;
     const double* fb;
@@ -75,7 +88,7 @@ struct FinalizeArgs {
     int64_t ldv;
     const double* X;
     const double* zscale;
-    const int* jc;
+    const int* perm;    // slots < out->nc_pad are finished here
     double* Z;
     int64_t ldz;
     const PrepOut* out;
@@ -165,6 +178,7 @@ struct ResArgs {
     int* iters;
     PrepOut* out;
     unsigned long long* prof;   // optional 8 phase timers of unit 0 (ns), or NULL
+    int handover;           // the batched LU stopped the leaders after x^(1): iterate them here
 };
 size_t resident_smem_bytes(int64_t n, int RL, int M2);
 cudaError_t launch_resident(const ResArgs& a, int cs, int nunits, size_t smem, cudaStream_t s);
@@ -173,6 +187,7 @@ int resident_max_clusters(int cs, size_t smem);
 void launch_prep(const PrepArgs& a, cudaStream_t s);
 void launch_bisect(int64_t n, const double* d, const double* e, double* w, double* bnd, cudaStream_t s);
 void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm);
+int64_t batched_slot_cap(int64_t n);
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 void launch_pack(const PackArgs& a, cudaStream_t s);
 void launch_identity(double* Z, int64_t n, int64_t ldz, cudaStream_t s);
