@@ -38,7 +38,7 @@ namespace res {
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int kXS = 16;          // scalar slots of the exchange area
-enum { U2 = 0, X2 = 1, U0 = 2, Q2 = 3, QINF = 4, QARG = 5, Q1 = 6, FA = 7, FB = 8, X2N = 9, GPN = 10 };
+enum { U2 = 0, X2 = 1, U0 = 2, Q2 = 3, QINF = 4, QARG = 5, Q1 = 6, FA = 7, FB = 8, X2N = 9, GPN = 10, QSGN = 11, Q0 = 12 };
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 // bulk L2 prefetch (16-byte aligned, size rounded up to 16 bytes)
@@ -68,19 +68,20 @@ struct L {        // shared-memory carve-up (doubles unless noted)
     double* gp;
     double* s;
     double* xp;
-    double* yrow;
-    double* PX;   // 2 x (M2 + kXS): exchange (double-buffered)
-    double* PXL;  // M2 + kXS: look-ahead exchange
+    double* yrow; // M2 + 2: row p of Y (pushed by its owner CTA)
+    double* PX;   // [2][CS][XW]: exchange, double-buffered; record c written by CTA c into every CTA
+    double* PXL;  // [CS][XW]: look-ahead exchange
     double* tf;   // n + 2: t rows gathered for the back sweep (CTA 0), x written in place
     double* bc;   // 2 n: (u1/u0, u2/u0) of every row, staged by CTA 0 for the back sweep
-    double* red;  // NW + 8
+    double* red;  // 2 x NW x 6: block reductions (double-buffered)
+    double* cred; // NW: colacc scalar partials
     double2* acc; // NT
-    uint64_t* mbar;
 };
 
-__host__ __device__ inline size_t smem_doubles(int64_t n, int RL, int M2) {
-    return (size_t)RL * (M2 + 4) + (size_t)M2 * M2 + 5 * (size_t)(M2 + 2) + 3 * (size_t)(M2 + kXS) +
-           (n + 2) + 2 * (size_t)n + 2 + (NW + 8) + 2 * NT + 8;
+__host__ __device__ inline size_t smem_doubles(int64_t n, int RL, int M2, int CS) {
+    const size_t XW = (size_t)M2 + kXS;
+    return (size_t)RL * (M2 + 4) + (size_t)M2 * M2 + 5 * (size_t)(M2 + 2) + 3 * CS * XW + (n + 2) + 2 * (size_t)n +
+           4 + 2 * NW * 6 + NW + 2 * NT + 8;
 }
 
 // block-wide exclusive scan of affine maps (thread order), total returned
@@ -105,40 +106,102 @@ __device__ __forceinline__ Aff scan_excl(Aff f, Aff* buf, Aff& total) {
     return comp(ex, pre);
 }
 
-// Column accumulate over local rows [a, b) (local indices): out[k] = sum Y[i][k] c_i for
-// k < min(gi + 1, P) (gi = global row); threads [t0, t0 + nth); fixed-order slice reduction.
-template <class Coef, class Sync>
-__device__ void colacc_local(const L& sm, int M2, int r0, int a, int b, int P, Coef coef, double* out, int t0,
-                             int nth, Sync sync) {
-    const int t = threadIdx.x - t0;
-    const int CPT = min(32, pow2ceil((P + 1) / 2 > 0 ? (P + 1) / 2 : 1));
-    const int RS = nth / CPT, cp = t % CPT, rs = t / CPT;
+// Fixed-order block reduction of K sums and, with ARG, an argmax (larger value wins, then the
+// lower index) in one barrier: butterfly inside each warp, then every thread folds the NW warp
+// records in warp order, so every thread holds the (bitwise identical) results.  `red` is
+// double-buffered by the caller's parity `par` (every thread runs the same sequence of calls,
+// and a buffer is rewritten only after the next call's barrier).
+template <int K, bool ARG>
+__device__ __forceinline__ void block_reduce(double (&v)[K], double& mx, long long& ix, double* red, int& par) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; k++) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        if (ARG) {
+            const double om = __shfl_xor_sync(0xffffffffu, mx, o);
+            const long long oi = __shfl_xor_sync(0xffffffffu, ix, o);
+            if (om > mx || (om == mx && oi < ix)) { mx = om; ix = oi; }
+        }
+    }
+    double* B = red + par * NW * 6;
+    par ^= 1;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) B[w * 6 + k] = v[k];
+        if (ARG) { B[w * 6 + 4] = mx; B[w * 6 + 5] = (double)ix; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; k++) v[k] = 0.0;
+    if (ARG) { mx = -1.0; ix = 0; }
+    for (int q = 0; q < NW; q++) {
+#pragma unroll
+        for (int k = 0; k < K; k++) v[k] += B[q * 6 + k];
+        if (ARG) {
+            const double m = B[q * 6 + 4];
+            const long long i = (long long)B[q * 6 + 5];
+            if (m > mx || (m == mx && i < ix)) { mx = m; ix = i; }
+        }
+    }
+}
+
+// Column accumulate over local rows [a, b) (local indices): out(k, sum_i Y[i][k] coef(i)) for
+// k < P, Y lower-trapezoidal (row gi = r0 + i holds columns 0..gi).  Threads [t0, t0 + nth)
+// (whole warps): a warp covers 32 / CPT rows per step with CPT lanes per row (two columns per
+// lane), two rows per lane in flight; lanes of a row slice combine by butterfly, warps through
+// shared memory in warp order (deterministic).  The per-thread scalar `s` is summed alongside
+// and returned to thread t0.
+template <class Coef, class Out, class Sync>
+__device__ __forceinline__ double colacc(const L& sm, int M2, int r0, int a, int b, int P, Coef coef, Out out,
+                                         double s, int t0, int nth, Sync sync) {
+    const int t = threadIdx.x - t0, w = t >> 5, ln = t & 31, W = nth >> 5;
+    const int KP = max(1, (P + 1) >> 1);
+    const int CPT = min(32, pow2ceil(KP));
+    const int cp = ln & (CPT - 1), rl = ln / CPT;
+    const int RS = W * (32 / CPT);
     const int k = 2 * cp;
-    double a0 = 0.0, a1 = 0.0;
-    for (int i = a + rs; i < b; i += RS) {
-        const int gi = r0 + i;
-        const int le = min(gi + 1, P);
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    auto row = [&](int i, double& x0, double& x1) {
+        const int le = min(r0 + i + 1, P);
         if (k < le) {
             const double2 y = *reinterpret_cast<const double2*>(sm.Y + (size_t)i * M2 + k);
             const double c = coef(i);
-            a0 = fma(y.x, c, a0);
-            if (k + 1 < le) a1 = fma(y.y, c, a1);
+            x0 = fma(y.x, c, x0);
+            if (k + 1 < le) x1 = fma(y.y, c, x1);
         }
+    };
+    int i = a + w * (32 / CPT) + rl;
+    for (; i + RS < b; i += 2 * RS) {
+        row(i, a0, a1);
+        row(i + RS, b0, b1);
     }
+    if (i < b) row(i, a0, a1);
+    a0 += b0;
+    a1 += b1;
+    for (int o = CPT; o < 32; o <<= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    s = warp_sum(s);
+    sync();   // acc / cred free
+    if (rl == 0) sm.acc[w * 32 + cp] = make_double2(a0, a1);
+    if (ln == 0) sm.cred[w] = s;
     sync();
-    sm.acc[t] = make_double2(a0, a1);
-    sync();
-    if (rs == 0 && t < CPT) {
-        for (int q = 1; q < RS; q++) {
-            const double2 v = sm.acc[cp + q * CPT];
-            a0 += v.x;
-            a1 += v.y;
+    if (2 * t < P) {
+        double v0 = 0.0, v1 = 0.0;
+        for (int q = 0; q < W; q++) {
+            const double2 v = sm.acc[q * 32 + t];
+            v0 += v.x;
+            v1 += v.y;
         }
-        if (k < P) out[k] = a0;
-        if (k + 1 < P) out[k + 1] = a1;
+        out(2 * t, v0);
+        if (2 * t + 1 < P) out(2 * t + 1, v1);
     }
-    // columns beyond 2 CPT (P <= 64 always here)
-    sync();
+    double r = 0.0;
+    if (t == 0)
+        for (int q = 0; q < W; q++) r += sm.cred[q];
+    return r;
 }
 
 // Back substitution x_i = t_i - b_i x_{i+1} - c_i x_{i+2} (rows n-1 .. 0; the row-normalised
@@ -191,8 +254,6 @@ __device__ void back_sweep_smem(const double* __restrict__ bc, double* tf, int64
     }
 }
 
-__device__ __forceinline__ double block_sum_(double v, double* red) { return block_sum<NT>(v, red); }
-
 __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cgr::cluster_group cl = cgr::this_cluster();
@@ -202,6 +263,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = a.n;
     const int RL = a.RL, M2 = a.M2;
+    const int XW = M2 + kXS;
     L sm;
     {
         double* p = reinterpret_cast<double*>(smem_raw);
@@ -216,18 +278,21 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         sm.s = p; p += M2 + 2;
         sm.xp = p; p += M2 + 2;
         sm.yrow = p; p += M2 + 2;
-        sm.PX = p; p += 2 * (M2 + kXS);
-        sm.PXL = p; p += M2 + kXS;
+        sm.PX = p; p += 2 * (size_t)CS * XW;
+        sm.PXL = p; p += (size_t)CS * XW;
         p += (reinterpret_cast<uintptr_t>(p) & 15) ? 1 : 0;
         sm.tf = p; p += (n + 2 + 1) & ~int64_t(1);
         sm.bc = p; p += 2 * n;
-        sm.red = p; p += NW + 8;
-        sm.acc = reinterpret_cast<double2*>(p); p += 2 * NT;
-        sm.mbar = reinterpret_cast<uint64_t*>(p);
+        sm.red = p; p += 2 * NW * 6;
+        sm.cred = p; p += NW;
+        p += (reinterpret_cast<uintptr_t>(p) & 15) ? 1 : 0;
+        sm.acc = reinterpret_cast<double2*>(p);
     }
     __syncthreads();
     const double thr = sqrt(0.1 / (double)n);
-    // optional phase timers (unit 0, CTA 0, thread 0; globaltimer ns)
+    // optional phase timers (unit 0, CTA 0, thread 0; globaltimer ns): 0 A/R1, 1 TT+BC,
+    // 2 R2+TN, 3 D+TEST(+done), 4 back-sweep staging, 5 forward pass 2, 6 back sweep (+LA),
+    // 7 x push + barrier
     const bool timing = a.prof && unit == 0 && crank == 0 && tid == 0;
     uint64_t tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint64_t tmark = 0;
@@ -240,7 +305,16 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     const int r0 = crank * RL, r1 = (int)min64(n, (int64_t)r0 + RL);
     const int nl = max(0, r1 - r0);
     int pxb = 0;   // exchange buffer parity
-    auto PXo = [&](int c, int b) -> double* { return cl.map_shared_rank(sm.PX, c) + b * (M2 + kXS); };
+    int rpar = 0;  // block_reduce buffer parity
+    // Exchange (push model): a CTA stores its record into slot [buffer][its rank] of every CTA
+    // of the cluster; after the cluster barrier every read is local.
+    auto PXo = [&](int c, int b) -> const double* { return sm.PX + ((size_t)b * CS + c) * XW; };
+    auto pub = [&](int b, int k, double v) {
+        for (int c = 0; c < CS; c++) cl.map_shared_rank(sm.PX, c)[((size_t)b * CS + crank) * XW + k] = v;
+    };
+    auto publ = [&](int k, double v) {
+        for (int c = 0; c < CS; c++) cl.map_shared_rank(sm.PXL, c)[(size_t)crank * XW + k] = v;
+    };
     auto csum = [&](int b, int slot) {   // sum over CTAs of a scalar slot, fixed order
         double v = 0.0;
         for (int c = 0; c < CS; c++) v += PXo(c, b)[M2 + slot];
@@ -248,10 +322,60 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     };
     auto csumL = [&](int slot) {
         double v = 0.0;
-        for (int c = 0; c < CS; c++) v += cl.map_shared_rank(sm.PXL, c)[M2 + slot];
+        for (int c = 0; c < CS; c++) v += sm.PXL[(size_t)c * XW + M2 + slot];
         return v;
     };
     auto bsync = []() { __syncthreads(); };
+    // x rows from CTA 0's back sweep into every CTA's `dst` (called by all threads of CTA 0)
+    auto push_x = [&](double* dst) {
+        for (int c = 0; c < CS; c++) {
+            double* d = cl.map_shared_rank(dst, c);
+            const int c0 = c * RL, c1 = (int)min64(n, (int64_t)c0 + RL);
+            for (int i = c0 + tid; i < c1; i += NT) d[i - c0] = sm.tf[i];
+        }
+    };
+    // forward pass 2 of a chained solve: exact carries from the composed maps (exchange buffer
+    // b) -> t rows scattered into CTA 0; rhs(i) the right-hand side's row i (local rows)
+    auto fwd_pass2 = [&](const double* Fj, const int8_t* FPj, int fta, int ftb, const Aff& fex, double q0, double sc,
+                         int b, auto rhs) {
+        Aff pre{1.0, 0.0};
+        for (int c2 = 0; c2 < crank; c2++) pre = comp(Aff{PXo(c2, b)[M2 + FA], PXo(c2, b)[M2 + FB]}, pre);
+        double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
+        double* tf0 = cl.map_shared_rank(sm.tf, 0);
+        for (int s = fta; s < ftb; s++) {
+            const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1), rr = __ldg(Fj + (int64_t)s * 4 + 1);
+            double y;
+            if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
+            else { y = cc; cc = fma(-l, cc, bn); }
+            tf0[s] = sc * y * rr;
+        }
+        if (ftb == n - 1 && fta < ftb) tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
+        else if (n == 1 && tid == 0) tf0[0] = sc * cc * __ldg(Fj + 1);
+    };
+    // forward maps (pass 1) of this thread's steps [fta, ftb), rhs(i) local rows
+    auto fwd_maps = [&](const double* Fj, const int8_t* FPj, int fta, int ftb, auto rhs) {
+        Aff f{1.0, 0.0};
+        for (int s = fta; s < ftb; s++) {
+            const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1);
+            if (FPj[s]) f.b = fma(-l, bn, f.b);
+            else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
+        }
+        return f;
+    };
+    // this thread's forward steps: CTA c runs steps [max(0, r0-1), min(r1-1, n-1)), which read
+    // its own rows of the right-hand side
+    const int s0 = max(0, r0 - 1), s1 = (int)min64(r1 - 1, n - 1);
+    const int FLn = s1 > s0 ? (s1 - s0 + NT - 1) / NT : 0;
+    const int fta = s0 + min(max(s1 - s0, 0), tid * FLn), ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FLn);
+    // the back sweep in CTA 0 (all its threads stage, thread 0 sweeps)
+    auto sweep = [&](const double* Fj) {
+        if (crank == 0) {
+            back_stage(Fj, sm.bc, n);
+            __syncthreads();
+            PH(4);
+            if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
+        }
+    };
 
     for (int ci = a.u_off[unit]; ci < a.u_off[unit + 1]; ci++) {
         const int clid = a.u_list[ci];
@@ -262,7 +386,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         // batched LU's stopping rule (||x||_inf >= sqrt(0.1/n) twice, MAXITS) and chained solves
         // with its factors (Alg. 4 l.5-7 and l.20; the same arithmetic as batched_lu.cu)
         double lscl = 0.0;
-        if (a.handover) {
+        const bool lead = m <= a.handover;
+        if (lead) {
             const int64_t j = j1;
             const double* Fj = a.F + j * n * 4;
             const int8_t* FPj = a.FP + j * n;
@@ -272,65 +397,45 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 const double* x1 = a.X1c + j * n2v;
                 for (int i = tid; i < nl; i += NT) sm.ql[i] = __ldcg(x1 + r0 + i);
             }
-            const int s0 = max(0, r0 - 1), s1 = (int)min64(r1 - 1, n - 1);
-            const int FL = s1 > s0 ? (s1 - s0 + NT - 1) / NT : 0;
-            const int fta = s0 + min(max(s1 - s0, 0), tid * FL), ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FL);
             int its = 1, passes = 0;
-            __syncthreads();
             while (true) {
                 // norms and argmax of the iterate, forward maps of its next solve
-                double* px = sm.PX + pxb * (M2 + kXS);
-                double q2 = 0.0, q1 = 0.0, qinf = -1.0;
-                int64_t qarg = 0;
+                double v[2] = {0.0, 0.0}, qinf = -1.0;
+                long long qarg = 0;
                 for (int i = tid; i < nl; i += NT) {
                     const double qi = sm.ql[i];
-                    q2 = fma(qi, qi, q2);
+                    v[0] = fma(qi, qi, v[0]);
                     const double aq = fabs(qi);
-                    q1 += aq;
+                    v[1] += aq;
                     if (aq > qinf) { qinf = aq; qarg = r0 + i; }
                 }
-                q2 = block_sum_(q2, sm.red);
-                q1 = block_sum_(q1, sm.red);
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double oq = __shfl_xor_sync(0xffffffffu, qinf, o);
-                    const long long oa = __shfl_xor_sync(0xffffffffu, (long long)qarg, o);
-                    if (oq > qinf || (oq == qinf && oa < qarg)) { qinf = oq; qarg = oa; }
-                }
-                if (lane == 0) sm.acc[warp] = make_double2(qinf, (double)qarg);
-                __syncthreads();
-                if (tid == 0) {
-                    for (int w = 1; w < NW; w++) {
-                        const double2 t = sm.acc[w];
-                        if (t.x > qinf || (t.x == qinf && (int64_t)t.y < qarg)) { qinf = t.x; qarg = (int64_t)t.y; }
-                    }
-                    px[M2 + Q2] = q2;
-                    px[M2 + Q1] = q1;
-                    px[M2 + QINF] = qinf;
-                    px[M2 + QARG] = (double)qarg;
-                }
-                Aff f{1.0, 0.0};
-                for (int s = fta; s < ftb; s++) {
-                    const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
-                    if (FPj[s]) f.b = fma(-l, bn, f.b);
-                    else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
-                }
+                block_reduce<2, true>(v, qinf, qarg, sm.red, rpar);   // also orders ql for the maps
+                const Aff f = fwd_maps(Fj, FPj, fta, ftb, [&](int64_t i) { return sm.ql[i - r0]; });
                 Aff tot;
                 const Aff fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
-                if (tid == 0) { px[M2 + FA] = tot.a; px[M2 + FB] = tot.b; }
+                if (tid == 0) {
+                    pub(pxb, M2 + Q2, v[0]);
+                    pub(pxb, M2 + Q1, v[1]);
+                    pub(pxb, M2 + QINF, qinf);
+                    pub(pxb, M2 + QARG, (double)qarg);
+                    pub(pxb, M2 + QSGN, (qinf >= 0.0 && sm.ql[qarg - r0] < 0.0) ? -1.0 : 1.0);
+                    pub(pxb, M2 + FA, tot.a);
+                    pub(pxb, M2 + FB, tot.b);
+                    if (crank == 0) pub(pxb, M2 + Q0, sm.ql[0]);
+                }
                 cl.sync();
                 const double q2t = csum(pxb, Q2);
-                qinf = -1.0;
-                qarg = 0;
+                double qi = -1.0;
+                long long qa = 0;
+                int own = 0;
                 for (int c2 = 0; c2 < CS; c2++) {
-                    const double v = PXo(c2, pxb)[M2 + QINF];
-                    const int64_t ia = (int64_t)PXo(c2, pxb)[M2 + QARG];
-                    if (v > qinf || (v == qinf && ia < qarg)) { qinf = v; qarg = ia; }
+                    const double vv = PXo(c2, pxb)[M2 + QINF];
+                    const long long ia = (long long)PXo(c2, pxb)[M2 + QARG];
+                    if (vv > qi || (vv == qi && ia < qa)) { qi = vv; qa = ia; own = c2; }
                 }
-                if (qinf >= thr) passes++;
+                if (qi >= thr) passes++;
                 if (passes >= kPasses || its >= kMaxIts) {
-                    const int own = (int)(qarg / RL);
-                    const double sgn = (cl.map_shared_rank(sm.ql, own)[qarg - (int64_t)own * RL] < 0.0) ? -1.0 : 1.0;
-                    lscl = sgn / sqrt(q2t);
+                    lscl = PXo(own, pxb)[M2 + QSGN] / sqrt(q2t);
                     double* zj = a.Z + j * a.ldz;
                     for (int i = tid; i < nl; i += NT) zj[r0 + i] = sm.ql[i] * lscl;
                     if (crank == 0 && tid == 0) {
@@ -338,43 +443,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         if (passes < kPasses) atomicAdd(&a.out->nflag, 1);
                     }
                     pxb ^= 1;
-                    cl.sync();
                     break;
                 }
                 its++;
-                {   // forward pass 2: exact carries -> t rows in CTA 0; scale sigma / ||x||_1
-                    Aff pre{1.0, 0.0};
-                    for (int c2 = 0; c2 < crank; c2++)
-                        pre = comp(Aff{PXo(c2, pxb)[M2 + FA], PXo(c2, pxb)[M2 + FB]}, pre);
-                    const double q0 = cl.map_shared_rank(sm.ql, 0)[0];
-                    double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
-                    const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(pxb, Q1);
-                    double* tf0 = cl.map_shared_rank(sm.tf, 0);
-                    for (int s = fta; s < ftb; s++) {
-                        const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
-                        const double rr = __ldg(Fj + (int64_t)s * 4 + 1);
-                        double y;
-                        if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
-                        else { y = cc; cc = fma(-l, cc, bn); }
-                        tf0[s] = sc * y * rr;
-                    }
-                    if (ftb == n - 1 && fta < ftb) {
-                        tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
-                    } else if (n == 1 && tid == 0) {
-                        tf0[0] = sc * cc * __ldg(Fj + 1);
-                    }
-                }
+                const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(pxb, Q1);
+                fwd_pass2(Fj, FPj, fta, ftb, fex, PXo(0, pxb)[M2 + Q0], sc, pxb, [&](int64_t i) { return sm.ql[i - r0]; });
                 pxb ^= 1;
                 cl.sync();
+                sweep(Fj);
                 if (crank == 0) {
-                    back_stage(Fj, sm.bc, n);
                     __syncthreads();
-                    if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
-                }
-                cl.sync();
-                {
-                    const double* x0 = cl.map_shared_rank(sm.tf, 0);
-                    for (int i = tid; i < nl; i += NT) sm.ql[i] = x0[r0 + i];
+                    push_x(sm.ql);
                 }
                 cl.sync();
             }
@@ -383,39 +462,42 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         // ================= first reflector from z_{j1}
         {
             const double* z = a.Z + j1 * a.ldz;
-            double u2 = 0.0;
+            double v[1] = {0.0}, dm = 0.0;
+            long long di = 0;
             for (int i = tid; i < nl; i += NT) {
-                const double zi = a.handover ? sm.ql[i] * lscl : __ldcg(z + r0 + i);
+                const double zi = lead ? sm.ql[i] * lscl : __ldcg(z + r0 + i);
                 sm.ul[i] = zi;
-                u2 = fma(zi, zi, u2);
+                v[0] = fma(zi, zi, v[0]);
             }
-            u2 = block_sum_(u2, sm.red);
-            double* px = sm.PX + pxb * (M2 + kXS);
-            if (tid == 0) px[M2 + U2] = u2;
+            block_reduce<1, false>(v, dm, di, sm.red, rpar);
+            if (tid == 0) {
+                pub(pxb, M2 + U2, v[0]);
+                if (crank == 0) pub(pxb, M2 + U0, sm.ul[0]);
+            }
             cl.sync();
             const double un = sqrt(csum(pxb, U2));
-            const double u0 = cl.map_shared_rank(sm.ul, 0)[0];
+            const double u0 = PXo(0, pxb)[M2 + U0];
             const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
             const double tt = 1.0 / (c * c - u0 * c);
             for (int i = tid; i < nl; i += NT) sm.Y[(size_t)i * M2] = (r0 + i == 0) ? (u0 - c) : sm.ul[i];
             if (tid == 0) sm.T[0] = tt;
             pxb ^= 1;
-            cl.sync();
+            __syncthreads();
         }
 
         bool la_have = false;
         for (int p = 1; p < m; p++) {
             const int64_t j = j1 + p;
+            const double* Fj = a.F + j * n * 4;
+            const int8_t* FPj = a.FP + j * n;
             int its = 1, kin = 1, passes = 0, restart = 0;
             bool done = false, flagged = false;
             bool use_la = la_have;
             bool la_done = false;
             la_have = false;
             bool first = true;
-            if (crank == 0 && tid == 0) {   // this vector's factor records for the chained solve
-                const double* Fj = a.F + j * n * 4;
+            if (crank == 0 && tid == 0)   // this vector's factor records for the chained solve
                 for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
-            }
             // x^(1)_j into xl (the look-ahead already loaded it into x1l)
             if (use_la) {
                 for (int i = tid; i < nl; i += NT) sm.xl[i] = sm.x1l[i];
@@ -430,24 +512,24 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 if (first && use_la) {
                     for (int k = tid; k < p - 1; k += NT) {
                         double v = 0.0;
-                        for (int c = 0; c < CS; c++) v += cl.map_shared_rank(sm.PXL, c)[k];
+                        for (int c = 0; c < CS; c++) v += sm.PXL[(size_t)c * XW + k];
                         sm.g[k] = v;
                     }
                     if (tid == 0) sm.g[p - 1] = csumL(GPN);
                     x2 = csumL(X2N);
                     __syncthreads();
                 } else {
-                    double* px = sm.PX + pxb * (M2 + kXS);
-                    colacc_local(sm, M2, r0, 0, nl, p, [&](int i) { return sm.xl[i]; }, px, 0, NT, bsync);
-                    double v = 0.0;
-                    for (int i = tid; i < nl; i += NT) v = fma(sm.xl[i], sm.xl[i], v);
-                    v = block_sum_(v, sm.red);
-                    if (tid == 0) px[M2 + X2] = v;
+                    double s = 0.0;
+                    for (int i = tid; i < nl; i += NT) s = fma(sm.xl[i], sm.xl[i], s);
+                    const int b = pxb;
+                    const double x2p = colacc(sm, M2, r0, 0, nl, p, [&](int i) { return sm.xl[i]; },
+                                              [&](int k, double v) { pub(b, k, v); }, s, 0, NT, bsync);
+                    if (tid == 0) pub(pxb, M2 + X2, x2p);
                     cl.sync();
                     for (int k = tid; k < p; k += NT) {
-                        double s = 0.0;
-                        for (int c = 0; c < CS; c++) s += PXo(c, pxb)[k];
-                        sm.g[k] = s;
+                        double v = 0.0;
+                        for (int c = 0; c < CS; c++) v += PXo(c, pxb)[k];
+                        sm.g[k] = v;
                     }
                     x2 = csum(pxb, X2);
                     pxb ^= 1;
@@ -463,9 +545,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     sm.gp[k] = v;
                 }
                 __syncthreads();
-                // ---------------- BC: uhat (local rows >= p), s' partial, ||uhat||^2, uhat_p
+                // ---------------- BC: uhat (local rows >= p), s' partial, ||uhat||^2, uhat_p;
+                // the owner of row p pushes Y[p, 0..p-1] to every CTA
                 {
-                    double* px = sm.PX + pxb * (M2 + kXS);
                     const int ia = max(0, p - r0);
                     double u2 = 0.0;
                     for (int i = ia + tid; i < nl; i += NT) {
@@ -482,12 +564,18 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         sm.ul[i] = ui;
                         u2 = fma(ui, ui, u2);
                     }
+                    if (p >= r0 && p < r1)
+                        for (int k = tid; k < p; k += NT) {
+                            const double yv = sm.Y[(size_t)(p - r0) * M2 + k];
+                            for (int c = 0; c < CS; c++) cl.map_shared_rank(sm.yrow, c)[k] = yv;
+                        }
                     __syncthreads();
-                    colacc_local(sm, M2, r0, ia, nl, p, [&](int i) { return sm.ul[i]; }, px, 0, NT, bsync);
-                    u2 = block_sum_(u2, sm.red);
+                    const int b = pxb;
+                    const double u2s = colacc(sm, M2, r0, ia, nl, p, [&](int i) { return sm.ul[i]; },
+                                              [&](int k, double v) { pub(b, k, v); }, u2, 0, NT, bsync);
                     if (tid == 0) {
-                        px[M2 + U2] = u2;
-                        px[M2 + U0] = (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0;
+                        pub(pxb, M2 + U2, u2s);
+                        pub(pxb, M2 + U0, (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0);
                     }
                     cl.sync();
                 }
@@ -497,67 +585,32 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 double u0 = csum(pxb, U0);
                 const bool zero_u = (un == 0.0);
                 if (zero_u) { u0 = 1.0; un = 1.0; }
-                {
-                    const int own = p / RL;
-                    const double* yrp = cl.map_shared_rank(sm.Y, own) + (size_t)(p - own * RL) * M2;
-                    for (int k = tid; k < p; k += NT) sm.yrow[k] = yrp[k];
-                }
                 if (un <= (double)n * kEps * sqrt(x2) && restart < kMaxRestart && !zero_u) {
-                    // degenerate iterate (reading 16): restart from a fresh start vector
+                    // degenerate iterate (reading 16): restart from a fresh start vector; its
+                    // exchange uses the other buffer (the A buffer, read before the BC barrier)
                     restart++;
                     its++;
                     kin = 1;
                     passes = 0;
-                    // forward maps of the start vector over this CTA's steps
-                    double* px = sm.PX + (pxb ^ 1) * (M2 + kXS);
-                    const double* Fj = a.F + j * n * 4;
-                    const int8_t* FPj = a.FP + j * n;
-                    const int s0 = max(0, r0 - 1), s1 = (int)min64(r1 - 1, n - 1);
-                    const int FL = s1 > s0 ? (s1 - s0 + NT - 1) / NT : 0;
-                    const int fta = s0 + min(max(s1 - s0, 0), tid * FL), ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FL);
+                    const int b = pxb ^ 1;
                     auto rhs = [&](int64_t i) { return start_entry(a.seed, n, j, restart, i); };
-                    Aff f{1.0, 0.0};
-                    double q1 = 0.0;
-                    for (int i = tid; i < nl; i += NT) q1 += fabs(rhs(r0 + i));
-                    for (int s = fta; s < ftb; s++) {
-                        const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1);
-                        if (FPj[s]) f.b = fma(-l, bn, f.b);
-                        else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
-                    }
+                    double v[1] = {0.0}, dm = 0.0;
+                    long long di = 0;
+                    for (int i = tid; i < nl; i += NT) v[0] += fabs(rhs(r0 + i));
+                    const Aff f = fwd_maps(Fj, FPj, fta, ftb, rhs);
                     Aff tot;
                     const Aff ex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
-                    q1 = block_sum_(q1, sm.red);
-                    if (tid == 0) { px[M2 + FA] = tot.a; px[M2 + FB] = tot.b; px[M2 + Q1] = q1; }
+                    block_reduce<1, false>(v, dm, di, sm.red, rpar);
+                    if (tid == 0) { pub(b, M2 + FA, tot.a); pub(b, M2 + FB, tot.b); pub(b, M2 + Q1, v[0]); }
                     cl.sync();
-                    Aff pre{1.0, 0.0};
-                    for (int c = 0; c < crank; c++) pre = comp(Aff{PXo(c, pxb ^ 1)[M2 + FA], PXo(c, pxb ^ 1)[M2 + FB]}, pre);
-                    const double q1t = csum(pxb ^ 1, Q1);
-                    const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / q1t;
-                    double cc = fma(ex.a, fma(pre.a, rhs(0), pre.b), ex.b);
-                    double* tf0 = cl.map_shared_rank(sm.tf, 0);
-                    for (int s = fta; s < ftb; s++) {
-                        const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1), rr = __ldg(Fj + (int64_t)s * 4 + 1);
-                        double y;
-                        if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
-                        else { y = cc; cc = fma(-l, cc, bn); }
-                        tf0[s] = sc * y * rr;
-                    }
-                    if (ftb == n - 1 && fta < ftb) {
-                        tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
-                    } else if (n == 1 && tid == 0) {
-                        tf0[0] = sc * cc * __ldg(Fj + 1);
-                    }
+                    const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(b, Q1);
+                    fwd_pass2(Fj, FPj, fta, ftb, ex, rhs(0), sc, b, rhs);
                     pxb ^= 1;   // the buffer used above is now the "previous" one
                     cl.sync();
+                    sweep(Fj);
                     if (crank == 0) {
-                        back_stage(a.F + j * n * 4, sm.bc, n);
                         __syncthreads();
-                        if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
-                    }
-                    cl.sync();
-                    {   // every CTA takes its rows of x from CTA 0
-                        const double* x0 = cl.map_shared_rank(sm.tf, 0);
-                        for (int i = tid; i < nl; i += NT) sm.xl[i] = x0[r0 + i];
+                        push_x(sm.xl);
                     }
                     cl.sync();
                     first = false;
@@ -598,11 +651,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 // ---------------- D: q = Y_{p+1} x' - e_p, norms, argmax, look-ahead column,
                 // forward-sweep chunk maps over this CTA's steps
                 Aff fex{1.0, 0.0};
-                int fta = 0, ftb = 0;
                 {
-                    double* px = sm.PX + pxb * (M2 + kXS);
-                    double q2 = 0.0, q1 = 0.0, qinf = -1.0, gpn = 0.0;
-                    int64_t qarg = 0;
+                    double v[3] = {0.0, 0.0, 0.0}, qinf = -1.0;   // ||q||^2, ||q||_1, gpn
+                    long long qarg = 0;
                     for (int i = tid; i < nl; i += NT) {
                         const int gi = r0 + i;
                         const int le = min(gi + 1, p + 1);
@@ -617,69 +668,44 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         if (k < le) d0 = fma(yr[k], sm.xp[k], d0);
                         const double qi = (gi == p) ? (d0 + d1) - 1.0 : (d0 + d1);
                         sm.ql[i] = qi;
-                        q2 = fma(qi, qi, q2);
+                        v[0] = fma(qi, qi, v[0]);
                         const double aq = fabs(qi);
-                        q1 += aq;
+                        v[1] += aq;
                         if (aq > qinf) { qinf = aq; qarg = gi; }
-                        if (la_done && gi >= p) gpn = fma(yr[p], sm.x1l[i], gpn);
+                        if (la_done && gi >= p) v[2] = fma(yr[p], sm.x1l[i], v[2]);
                     }
-                    q2 = block_sum_(q2, sm.red);
-                    q1 = block_sum_(q1, sm.red);
-                    gpn = block_sum_(gpn, sm.red);
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const double oq = __shfl_xor_sync(0xffffffffu, qinf, o);
-                        const long long oa = __shfl_xor_sync(0xffffffffu, (long long)qarg, o);
-                        if (oq > qinf || (oq == qinf && oa < qarg)) { qinf = oq; qarg = oa; }
-                    }
-                    if (lane == 0) sm.acc[warp] = make_double2(qinf, (double)qarg);
-                    __syncthreads();
-                    if (tid == 0) {
-                        for (int w = 1; w < NW; w++) {
-                            const double2 t = sm.acc[w];
-                            if (t.x > qinf || (t.x == qinf && (int64_t)t.y < qarg)) { qinf = t.x; qarg = (int64_t)t.y; }
-                        }
-                        px[M2 + Q2] = q2;
-                        px[M2 + Q1] = q1;
-                        px[M2 + QINF] = qinf;
-                        px[M2 + QARG] = (double)qarg;
-                        sm.PXL[M2 + GPN] = gpn;
-                    }
-                    // forward sweep pass 1: steps [max(0, r0-1), min(r1-1, n-1)) use this CTA's q
-                    const double* Fj = a.F + j * n * 4;
-                    const int8_t* FPj = a.FP + j * n;
-                    const int s0 = max(0, r0 - 1), s1 = (int)min64(r1 - 1, n - 1);
-                    const int FL = s1 > s0 ? (s1 - s0 + NT - 1) / NT : 0;
-                    fta = s0 + min(max(s1 - s0, 0), tid * FL);
-                    ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FL);
-                    Aff f{1.0, 0.0};
-                    __syncthreads();
-                    for (int s = fta; s < ftb; s++) {
-                        const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
-                        if (FPj[s]) f.b = fma(-l, bn, f.b);
-                        else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
-                    }
+                    block_reduce<3, true>(v, qinf, qarg, sm.red, rpar);   // also orders ql for the maps
+                    const Aff f = fwd_maps(Fj, FPj, fta, ftb, [&](int64_t i) { return sm.ql[i - r0]; });
                     Aff tot;
                     fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
-                    if (tid == 0) { px[M2 + FA] = tot.a; px[M2 + FB] = tot.b; }
+                    if (tid == 0) {
+                        pub(pxb, M2 + Q2, v[0]);
+                        pub(pxb, M2 + Q1, v[1]);
+                        pub(pxb, M2 + QINF, qinf);
+                        pub(pxb, M2 + QARG, (double)qarg);
+                        pub(pxb, M2 + QSGN, (qinf >= 0.0 && sm.ql[qarg - r0] < 0.0) ? -1.0 : 1.0);
+                        pub(pxb, M2 + FA, tot.a);
+                        pub(pxb, M2 + FB, tot.b);
+                        if (crank == 0) pub(pxb, M2 + Q0, sm.ql[0]);
+                        publ(M2 + GPN, v[2]);
+                    }
                     cl.sync();
                 }
-                PH(3);
                 // ---------------- TEST (replicated)
                 const double q2 = csum(pxb, Q2);
                 double qinf = -1.0;
-                int64_t qarg = 0;
+                long long qarg = 0;
+                int own = 0;
                 for (int c2 = 0; c2 < CS; c2++) {
-                    const double v = PXo(c2, pxb)[M2 + QINF];
-                    const int64_t ia = (int64_t)PXo(c2, pxb)[M2 + QARG];
-                    if (v > qinf || (v == qinf && ia < qarg)) { qinf = v; qarg = ia; }
+                    const double vv = PXo(c2, pxb)[M2 + QINF];
+                    const long long ia = (long long)PXo(c2, pxb)[M2 + QARG];
+                    if (vv > qinf || (vv == qinf && ia < qarg)) { qinf = vv; qarg = ia; own = c2; }
                 }
                 if (fabs(c) * qinf >= thr) passes++;
                 if (passes >= kPasses) done = true;
                 else if (kin >= kMaxIts) { done = true; flagged = true; }
                 if (done) {
-                    const int own = (int)(qarg / RL);
-                    const double sgn = (cl.map_shared_rank(sm.ql, own)[qarg - (int64_t)own * RL] < 0.0) ? -1.0 : 1.0;
-                    const double scl = sgn / sqrt(q2);
+                    const double scl = PXo(own, pxb)[M2 + QSGN] / sqrt(q2);
                     double* zj = a.Z + j * a.ldz;
                     for (int i = tid; i < nl; i += NT) zj[r0 + i] = sm.ql[i] * scl;
                     if (crank == 0 && tid == 0) {
@@ -688,44 +714,22 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     }
                     la_have = la_done;
                     pxb ^= 1;
-                    cl.sync();   // exchange buffer and ql reads done before the next vector
-                    PH(4);
+                    __syncthreads();
+                    PH(3);
                 } else {
                     its++;
                     kin++;
+                    PH(3);
                     // forward pass 2: exact carries -> t rows, gathered into CTA 0
-                    {
-                        const double* Fj = a.F + j * n * 4;
-                        const int8_t* FPj = a.FP + j * n;
-                        Aff pre{1.0, 0.0};
-                        for (int c2 = 0; c2 < crank; c2++)
-                            pre = comp(Aff{PXo(c2, pxb)[M2 + FA], PXo(c2, pxb)[M2 + FB]}, pre);
-                        const double q0 = cl.map_shared_rank(sm.ql, 0)[0];
-                        double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
-                        const double q1 = csum(pxb, Q1);
-                        const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / q1;
-                        double* tf0 = cl.map_shared_rank(sm.tf, 0);
-                        for (int s = fta; s < ftb; s++) {
-                            const double l = __ldg(Fj + (int64_t)s * 4), bn = sm.ql[s + 1 - r0];
-                            const double rr = __ldg(Fj + (int64_t)s * 4 + 1);
-                            double y;
-                            if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
-                            else { y = cc; cc = fma(-l, cc, bn); }
-                            tf0[s] = sc * y * rr;
-                        }
-                        if (ftb == n - 1 && fta < ftb) {
-                            tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
-                            }
-                    }
+                    const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(pxb, Q1);
+                    fwd_pass2(Fj, FPj, fta, ftb, fex, PXo(0, pxb)[M2 + Q0], sc, pxb,
+                              [&](int64_t i) { return sm.ql[i - r0]; });
                     pxb ^= 1;
                     cl.sync();
                     PH(5);
-                    const bool la = !la_done && p + 1 < m;
-                    if (crank == 0) {
-                        back_stage(a.F + j * n * 4, sm.bc, n);
-                        __syncthreads();
-                        if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
-                    }
+                    const bool la = !la_done && p + 1 < m && !(a.flags & 1);
+                    sweep(Fj);
+                    if (timing) PH(6);
                     if (la) {
                         // look-ahead pass A of vector p+1 (every warp except CTA 0's warp 0):
                         // columns 0..p-1 of Y_{p+1} are final
@@ -744,25 +748,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                                 x2n = fma(v, v, x2n);
                             }
                             ssync();
-                            colacc_local(sm, M2, r0, 0, nl, p, [&](int i) { return sm.x1l[i]; }, sm.PXL, t0, nth, ssync);
-                            x2n = warp_sum(x2n);
-                            if (lane == 0) sm.red[warp] = x2n;
-                            ssync();
-                            if (tid == t0) {
-                                double v = 0.0;
-                                for (int w = t0 / 32; w < NW; w++) v += sm.red[w];
-                                sm.PXL[M2 + X2N] = v;
-                            }
+                            const double x2s = colacc(sm, M2, r0, 0, nl, p, [&](int i) { return sm.x1l[i]; },
+                                                      [&](int k, double v) { publ(k, v); }, x2n, t0, nth, ssync);
+                            if (tid == t0) publ(M2 + X2N, x2s);
                         }
                         la_done = true;
                     }
-                    if (timing) PH(6);
-                    cl.sync();   // x complete in CTA 0, look-ahead partials published
-                    {   // every CTA takes its rows of x from CTA 0
-                        const double* x0 = cl.map_shared_rank(sm.tf, 0);
-                        for (int i = tid; i < nl; i += NT) sm.xl[i] = x0[r0 + i];
+                    if (crank == 0) {
+                        __syncthreads();   // x complete in CTA 0's tf
+                        push_x(sm.xl);
                     }
-                    cl.sync();   // CTA 0's t/x buffer is free again
+                    cl.sync();   // x rows in every CTA, look-ahead partials published
                     PH(7);
                 }
             }
@@ -775,7 +771,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
 
 }  // namespace res
 
-size_t resident_smem_bytes(int64_t n, int RL, int M2) { return sizeof(double) * res::smem_doubles(n, RL, M2); }
+size_t resident_smem_bytes(int64_t n, int RL, int M2, int cs) { return sizeof(double) * res::smem_doubles(n, RL, M2, cs); }
 
 cudaError_t launch_resident(const ResArgs& a, int cs, int nunits, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(res::cwy_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

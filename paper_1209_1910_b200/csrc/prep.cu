@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         if (j < n && a.jc[j] == 0) {
             const int c = a.cid[j];
             const int m = a.cstart[c + 1] - a.cstart[c];
-            cflag = !(a.handover && m >= 2 && m <= kNarrowM);
+            cflag = !(m >= 2 && m <= a.handover);
         }
         int v = cflag;
 #pragma unroll

@@ -483,7 +483,13 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     // LU splits into two concurrent launches -- the first-solve warps (2 sweeps; the resident
     // kernel waits only for them and the packing) and the iterating warps (singletons, other
     // leaders; up to 2 MAXITS sweeps) with their finalize on a second stream.
-    const int handover = (h->resident && h->handover && n >= 2 && n <= 2048) ? 1 : 0;
+    // handover: the largest cluster whose rows fit the resident kernel's 8-CTA shared memory
+    int handover = 0;
+    if (h->resident && h->handover && n >= 2 && n <= 2048) {
+        const int RL8 = (int)(((n + 7) / 8 + 1) & ~int64_t(1));
+        for (int mm = 2; mm <= cwy_narrow_max(); mm++)
+            if (resident_smem_bytes(n, RL8, (mm + 1) & ~1, 8) <= 232448) handover = mm;
+    }
     auto join_b2 = [&]() -> int {
         if (handover) CK(cudaStreamWaitEvent(st, h->ev_b2, 0));
         return 0;
@@ -603,7 +609,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             const int want = (m >= h->res_cs4) ? 4 : (m >= h->res_cs2 ? 2 : 1);
             for (int q = 0; q < 4; q++) {
                 const int RL = (int)(((n + css[q] - 1) / css[q] + 1) & ~int64_t(1));
-                if (css[q] >= want && resident_smem_bytes(n, RL, m2) <= 232448) {
+                if (css[q] >= want && resident_smem_bytes(n, RL, m2, css[q]) <= 232448) {
                     int gi = -1;
                     for (int k = 0; k < (int)rgroups.size(); k++)
                         if (rgroups[k].cs == css[q]) gi = k;
@@ -618,11 +624,11 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 }
             }
         }
-        for (auto& rg : rgroups) rg.smem = resident_smem_bytes(n, rg.RL, rg.M2);
+        for (auto& rg : rgroups) rg.smem = resident_smem_bytes(n, rg.RL, rg.M2, rg.cs);
         if (handover)   // the batched LU stopped every narrow leader: all of them must be resident
             for (int c = rlo[h->rank]; c < rhi[h->rank]; c++) {
                 const int m = cs[c + 1] - cs[c];
-                if (m >= 2 && m <= cwy_narrow_max() && !resident[c]) {
+                if (m >= 2 && m <= handover && !resident[c]) {
                     fprintf(stderr, "[tinv] narrow cluster of %d vectors does not fit the resident kernel\n", m);
                     join_b2();
                     return TINV_ERR_DEVICE;
@@ -735,6 +741,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             ra.u_list = h->res_buf + offs[q] + units[q] + 1;
             ra.X1c = h->X1c; ra.F = h->F; ra.FP = h->FP; ra.unn = h->unn; ra.Z = Z; ra.ldz = ldz;
             ra.iters = h->iters; ra.out = h->out; ra.handover = handover;
+            if (const char* v = getenv("TINV_RES_FLAGS")) ra.flags = atoi(v);
             ra.prof = (h->profiling && q == 0) ? reinterpret_cast<unsigned long long*>(h->bnd + 8) : nullptr;
             CK(launch_resident(ra, rg.cs, units[q], rg.smem, sq));
             launches++;

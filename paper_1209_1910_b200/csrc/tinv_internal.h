@@ -35,7 +35,7 @@ struct PrepArgs {
     int* slot;          // slot of each vector (n)
     int* perm;          // vector of each slot, or -1
     int64_t nslot_cap;  // roundup(n, 32) + 32
-    int handover;       // leaders of clusters with 2 <= m <= kNarrowM finish in the resident kernel
+    int handover;       // leaders of clusters with 2 <= m <= handover finish in the resident kernel (0: none)
     PrepOut* out;
 };
 
@@ -178,9 +178,11 @@ struct ResArgs {
     int* iters;
     PrepOut* out;
     unsigned long long* prof;   // optional 8 phase timers of unit 0 (ns), or NULL
-    int handover;           // the batched LU stopped the leaders after x^(1): iterate them here
+    int handover;           // clusters with m <= handover: the batched LU stopped the leader after
+                            // x^(1), iterate it here (0: none)
+    int flags;              // experiments: bit 0 disables the look-ahead pass
 };
-size_t resident_smem_bytes(int64_t n, int RL, int M2);
+size_t resident_smem_bytes(int64_t n, int RL, int M2, int cs);
 cudaError_t launch_resident(const ResArgs& a, int cs, int nunits, size_t smem, cudaStream_t s);
 int resident_max_clusters(int cs, size_t smem);
 
