@@ -58,12 +58,13 @@ struct Aff {
 __device__ __forceinline__ Aff comp(const Aff& f, const Aff& g) { return Aff{f.a * g.a, fma(f.a, g.b, f.b)}; }
 
 struct L {        // shared-memory carve-up (doubles unless noted)
-    double* Y;    // RL x M2, local rows
+    double* Y;    // RL x M2, local rows; the 16-byte column pairs of row i are XOR-swizzled
+                  // (yo) so that a warp's loads of one pair from consecutive rows hit distinct banks
     double* xl;   // RL: current iterate
     double* ul;   // RL: uhat
     double* ql;   // RL: q
     double* x1l;  // RL: x^(1) of the next vector (look-ahead)
-    double* T;    // M2 x M2 row-major, T[l][k]
+    double* T;    // M2 x TS row-major, T[l][k] (odd stride TS = M2 + 1: threads walking rows do not collide)
     double* g;    // M2 + 2
     double* gp;
     double* s;
@@ -80,9 +81,27 @@ struct L {        // shared-memory carve-up (doubles unless noted)
 
 __host__ __device__ inline size_t smem_doubles(int64_t n, int RL, int M2, int CS) {
     const size_t XW = (size_t)M2 + kXS;
-    return (size_t)RL * (M2 + 4) + (size_t)M2 * M2 + 5 * (size_t)(M2 + 2) + 3 * CS * XW + (n + 2) + 2 * (size_t)n +
+    const size_t TS = M2 + 1;
+    return (size_t)RL * (M2 + 4) + (size_t)M2 * TS + 1 + 5 * (size_t)(M2 + 2) + 3 * CS * XW + (n + 2) + 2 * (size_t)n +
            4 + 2 * NW * 6 + NW + 2 * NT + 8;
 }
+
+// Offset of element (i, k) of Y (row stride M2, even).  A row is U = M2/2 16-byte units; rows
+// i and i' share a bank group for the same unit when (i - i') U = 0 mod 8, i.e. every 8 / 2^s
+// rows with 2^s || U (s <= 3).  Unit u of row i is stored at u ^ ((i >> (3 - s)) & (2^s - 1)),
+// which spreads 8 consecutive rows over distinct bank groups and stays inside the row.
+struct YSw {
+    int M2, sh, msk;
+    __device__ explicit YSw(int m2) : M2(m2) {
+        const int U = m2 >> 1;
+        const int s = U ? min(3, __ffs(U) - 1) : 0;
+        sh = 3 - s;
+        msk = (1 << s) - 1;
+    }
+    __device__ __forceinline__ int x(int i) const { return (i >> sh) & msk; }                  // row's key
+    __device__ __forceinline__ int pair(int i, int u) const { return i * M2 + 2 * (u ^ x(i)); }  // unit u
+    __device__ __forceinline__ int at(int i, int k) const { return pair(i, k >> 1) + (k & 1); }
+};
 
 // block-wide exclusive scan of affine maps (thread order), total returned
 __device__ __forceinline__ Aff scan_excl(Aff f, Aff* buf, Aff& total) {
@@ -153,7 +172,7 @@ __device__ __forceinline__ void block_reduce(double (&v)[K], double& mx, long lo
 // shared memory in warp order (deterministic).  The per-thread scalar `s` is summed alongside
 // and returned to thread t0.
 template <class Coef, class Out, class Sync>
-__device__ __forceinline__ double colacc(const L& sm, int M2, int r0, int a, int b, int P, Coef coef, Out out,
+__device__ __forceinline__ double colacc(const L& sm, const YSw& ys, int r0, int a, int b, int P, Coef coef, Out out,
                                          double s, int t0, int nth, Sync sync) {
     const int t = threadIdx.x - t0, w = t >> 5, ln = t & 31, W = nth >> 5;
     const int KP = max(1, (P + 1) >> 1);
@@ -165,7 +184,7 @@ __device__ __forceinline__ double colacc(const L& sm, int M2, int r0, int a, int
     auto row = [&](int i, double& x0, double& x1) {
         const int le = min(r0 + i + 1, P);
         if (k < le) {
-            const double2 y = *reinterpret_cast<const double2*>(sm.Y + (size_t)i * M2 + k);
+            const double2 y = *reinterpret_cast<const double2*>(sm.Y + ys.pair(i, cp));
             const double c = coef(i);
             x0 = fma(y.x, c, x0);
             if (k + 1 < le) x1 = fma(y.y, c, x1);
@@ -209,48 +228,40 @@ __device__ __forceinline__ double colacc(const L& sm, int M2, int r0, int a, int
 // over blocks of rows multiplies the b, c of neighbouring rows, which for nearly decoupled
 // blocks (pivots ~ eps ||T||, |b| ~ 1e11 in glued Wilkinson matrices) cancels catastrophically.
 // All threads of CTA 0 first stage (b, c) of every row into shared memory (back_stage); then
-// one thread runs the chain from shared memory with the next 8 rows' loads ahead of it
-// (back_sweep_smem).
+// one thread runs the chain from shared memory in 16-row batches (back_sweep_smem).
 __device__ void back_stage(const double* __restrict__ F, double* bc, int64_t n) {
+#pragma unroll 8
     for (int64_t i = threadIdx.x; i < n; i += NT)
         reinterpret_cast<double2*>(bc)[i] = __ldg(reinterpret_cast<const double2*>(F + i * 4 + 2));
 }
-__device__ void back_sweep_smem(const double* __restrict__ bc, double* tf, int64_t n) {
+__device__ void back_sweep_smem(const double* __restrict__ bc, double* tf, int64_t n64) {
     const double2* BC = reinterpret_cast<const double2*>(bc);
+    const int n = (int)n64;
     double x1 = 0.0, x2 = 0.0;
-    const int64_t top = n & ~int64_t(7);
-    for (int64_t u = n - 1; u >= top; u--) {
+    const int top = n & ~15;
+    for (int u = n - 1; u >= top; u--) {
         const double2 v = BC[u];
         const double xi = fma(-v.x, x1, fma(-v.y, x2, tf[u]));
         tf[u] = xi;
         x2 = x1;
         x1 = xi;
     }
-    if (top == 0) return;
-    double b[8], c[8], t[8];
+    // 16-row batches: the batch's loads first (independent), then the dependent chain
+    for (int u0 = top - 16; u0 >= 0; u0 -= 16) {
+        double b[16], c[16], t[16], xv[16];
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
-        const double2 v = BC[top - 8 + u];
-        b[u] = v.x; c[u] = v.y; t[u] = tf[top - 8 + u];
-    }
-    for (int64_t u0 = top - 8; u0 >= 0; u0 -= 8) {
-        double bn[8], cn[8], tn[8], xv[8];
-        const int64_t nx = u0 >= 8 ? u0 - 8 : 0;
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            const double2 v = BC[nx + u];
-            bn[u] = v.x; cn[u] = v.y; tn[u] = tf[nx + u];
+        for (int u = 0; u < 16; u++) {
+            const double2 v = BC[u0 + u];
+            b[u] = v.x; c[u] = v.y; t[u] = tf[u0 + u];
         }
 #pragma unroll
-        for (int u = 7; u >= 0; u--) {
+        for (int u = 15; u >= 0; u--) {
             xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u]));
             x2 = x1;
             x1 = xv[u];
         }
 #pragma unroll
-        for (int u = 0; u < 8; u += 2) *reinterpret_cast<double2*>(tf + u0 + u) = make_double2(xv[u], xv[u + 1]);
-#pragma unroll
-        for (int u = 0; u < 8; u++) { b[u] = bn[u]; c[u] = cn[u]; t[u] = tn[u]; }
+        for (int u = 0; u < 16; u += 2) *reinterpret_cast<double2*>(tf + u0 + u) = make_double2(xv[u], xv[u + 1]);
     }
 }
 
@@ -263,6 +274,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = a.n;
     const int RL = a.RL, M2 = a.M2;
+    const int TS = M2 + 1;
+    const YSw ys(M2);
     const int XW = M2 + kXS;
     L sm;
     {
@@ -272,7 +285,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         sm.ul = p; p += RL;
         sm.ql = p; p += RL;
         sm.x1l = p; p += RL;
-        sm.T = p; p += (size_t)M2 * M2;
+        sm.T = p; p += (size_t)M2 * TS;
         sm.g = p; p += M2 + 2;
         sm.gp = p; p += M2 + 2;
         sm.s = p; p += M2 + 2;
@@ -290,13 +303,14 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     }
     __syncthreads();
     const double thr = sqrt(0.1 / (double)n);
-    // optional phase timers (unit 0, CTA 0, thread 0; globaltimer ns): 0 A/R1, 1 TT+BC,
-    // 2 R2+TN, 3 D+TEST(+done), 4 back-sweep staging, 5 forward pass 2, 6 back sweep (+LA),
-    // 7 x push + barrier
-    const bool timing = a.prof && unit == 0 && crank == 0 && tid == 0;
-    uint64_t tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // optional phase timers (unit 0, CTA 0, thread 0; SM cycles): 0 A/R1, 1 TT, 2 BC,
+    // 3 R2 (+restart), 4 TN, 5 D rows + reduction, 6 D forward maps, 7 D scan + exchange,
+    // 8 TEST (+done), 9 back-sweep staging, 10 forward pass 2, 11 back sweep, 12 look-ahead,
+    // 13 x push + barrier, 14 leader iterations, 15 first reflector
+    const bool timing = a.prof && unit == 0 && crank == ((a.flags >> 4) & 7) && tid == 0;   // flags: timed CTA
+    uint64_t tacc[16] = {};
     uint64_t tmark = 0;
-    auto now = []() { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+    auto now = []() { return (uint64_t)clock64(); };   // SM cycles (the host converts)
     if (timing) tmark = now();
     auto PH = [&](int k) {
         if (timing) { const uint64_t t = now(); tacc[k] += t - tmark; tmark = t; }
@@ -326,6 +340,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         return v;
     };
     auto bsync = []() { __syncthreads(); };
+    // cluster barrier; a one-CTA cluster only needs the CTA barrier (all its stores are local)
+    auto csync = [&]() {
+        if (CS == 1) __syncthreads();
+        else cl.sync();
+    };
     // x rows from CTA 0's back sweep into every CTA's `dst` (called by all threads of CTA 0)
     auto push_x = [&](double* dst) {
         for (int c = 0; c < CS; c++) {
@@ -342,12 +361,28 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         for (int c2 = 0; c2 < crank; c2++) pre = comp(Aff{PXo(c2, b)[M2 + FA], PXo(c2, b)[M2 + FB]}, pre);
         double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
         double* tf0 = cl.map_shared_rank(sm.tf, 0);
-        for (int s = fta; s < ftb; s++) {
-            const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1), rr = __ldg(Fj + (int64_t)s * 4 + 1);
+        auto step = [&](int s, double l, double rr, bool sw, double bn) {
             double y;
-            if (FPj[s]) { y = bn; cc = fma(-l, bn, cc); }
+            if (sw) { y = bn; cc = fma(-l, bn, cc); }
             else { y = cc; cc = fma(-l, cc, bn); }
             tf0[s] = sc * y * rr;
+        };
+        int s = fta;
+        for (; s + 4 <= ftb; s += 4) {   // the four steps' loads in flight together
+            double2 lr[4], bn[4];
+            bool sw[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                lr[u] = __ldg(reinterpret_cast<const double2*>(Fj + (int64_t)(s + u) * 4));
+                sw[u] = FPj[s + u] != 0;
+                bn[u].x = rhs(s + u + 1);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) step(s + u, lr[u].x, lr[u].y, sw[u], bn[u].x);
+        }
+        for (; s < ftb; s++) {
+            const double2 lr = __ldg(reinterpret_cast<const double2*>(Fj + (int64_t)s * 4));
+            step(s, lr.x, lr.y, FPj[s] != 0, rhs(s + 1));
         }
         if (ftb == n - 1 && fta < ftb) tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
         else if (n == 1 && tid == 0) tf0[0] = sc * cc * __ldg(Fj + 1);
@@ -355,11 +390,24 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     // forward maps (pass 1) of this thread's steps [fta, ftb), rhs(i) local rows
     auto fwd_maps = [&](const double* Fj, const int8_t* FPj, int fta, int ftb, auto rhs) {
         Aff f{1.0, 0.0};
-        for (int s = fta; s < ftb; s++) {
-            const double l = __ldg(Fj + (int64_t)s * 4), bn = rhs(s + 1);
-            if (FPj[s]) f.b = fma(-l, bn, f.b);
+        auto step = [&](double l, bool sw, double bn) {
+            if (sw) f.b = fma(-l, bn, f.b);
             else { f.a = -l * f.a; f.b = fma(-l, f.b, bn); }
+        };
+        int s = fta;
+        for (; s + 4 <= ftb; s += 4) {   // the four steps' loads in flight together
+            double l[4], bn[4];
+            bool sw[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                l[u] = __ldg(Fj + (int64_t)(s + u) * 4);
+                sw[u] = FPj[s + u] != 0;
+                bn[u] = rhs(s + u + 1);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) step(l[u], sw[u], bn[u]);
         }
+        for (; s < ftb; s++) step(__ldg(Fj + (int64_t)s * 4), FPj[s] != 0, rhs(s + 1));
         return f;
     };
     // this thread's forward steps: CTA c runs steps [max(0, r0-1), min(r1-1, n-1)), which read
@@ -372,7 +420,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         if (crank == 0) {
             back_stage(Fj, sm.bc, n);
             __syncthreads();
-            PH(4);
+            PH(9);
             if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
         }
     };
@@ -395,6 +443,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
             {
                 const double* x1 = a.X1c + j * n2v;
+                #pragma unroll 4
                 for (int i = tid; i < nl; i += NT) sm.ql[i] = __ldcg(x1 + r0 + i);
             }
             int its = 1, passes = 0;
@@ -423,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     pub(pxb, M2 + FB, tot.b);
                     if (crank == 0) pub(pxb, M2 + Q0, sm.ql[0]);
                 }
-                cl.sync();
+                csync();
                 const double q2t = csum(pxb, Q2);
                 double qi = -1.0;
                 long long qa = 0;
@@ -449,16 +498,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(pxb, Q1);
                 fwd_pass2(Fj, FPj, fta, ftb, fex, PXo(0, pxb)[M2 + Q0], sc, pxb, [&](int64_t i) { return sm.ql[i - r0]; });
                 pxb ^= 1;
-                cl.sync();
+                csync();
                 sweep(Fj);
                 if (crank == 0) {
                     __syncthreads();
                     push_x(sm.ql);
                 }
-                cl.sync();
+                csync();
             }
         }
 
+        PH(14);
         // ================= first reflector from z_{j1}
         {
             const double* z = a.Z + j1 * a.ldz;
@@ -474,16 +524,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 pub(pxb, M2 + U2, v[0]);
                 if (crank == 0) pub(pxb, M2 + U0, sm.ul[0]);
             }
-            cl.sync();
+            csync();
             const double un = sqrt(csum(pxb, U2));
             const double u0 = PXo(0, pxb)[M2 + U0];
             const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
             const double tt = 1.0 / (c * c - u0 * c);
-            for (int i = tid; i < nl; i += NT) sm.Y[(size_t)i * M2] = (r0 + i == 0) ? (u0 - c) : sm.ul[i];
+            for (int i = tid; i < nl; i += NT) sm.Y[ys.at(i, 0)] = (r0 + i == 0) ? (u0 - c) : sm.ul[i];
             if (tid == 0) sm.T[0] = tt;
             pxb ^= 1;
             __syncthreads();
         }
+        PH(15);
 
         bool la_have = false;
         for (int p = 1; p < m; p++) {
@@ -503,6 +554,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 for (int i = tid; i < nl; i += NT) sm.xl[i] = sm.x1l[i];
             } else {
                 const double* x1 = a.X1c + j * n2v;
+                #pragma unroll 4
                 for (int i = tid; i < nl; i += NT) sm.xl[i] = __ldcg(x1 + r0 + i);
             }
             __syncthreads();
@@ -522,10 +574,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     double s = 0.0;
                     for (int i = tid; i < nl; i += NT) s = fma(sm.xl[i], sm.xl[i], s);
                     const int b = pxb;
-                    const double x2p = colacc(sm, M2, r0, 0, nl, p, [&](int i) { return sm.xl[i]; },
+                    const double x2p = colacc(sm, ys, r0, 0, nl, p, [&](int i) { return sm.xl[i]; },
                                               [&](int k, double v) { pub(b, k, v); }, s, 0, NT, bsync);
                     if (tid == 0) pub(pxb, M2 + X2, x2p);
-                    cl.sync();
+                    csync();
                     for (int k = tid; k < p; k += NT) {
                         double v = 0.0;
                         for (int c = 0; c < CS; c++) v += PXo(c, pxb)[k];
@@ -541,10 +593,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 // ---------------- TT: g' = T_p^T g (replicated)
                 for (int k = tid; k < p; k += NT) {
                     double v = 0.0;
-                    for (int l = 0; l <= k; l++) v = fma(sm.T[l * M2 + k], sm.g[l], v);
+                    for (int l = 0; l <= k; l++) v = fma(sm.T[l * TS + k], sm.g[l], v);
                     sm.gp[k] = v;
                 }
                 __syncthreads();
+                PH(1);
                 // ---------------- BC: uhat (local rows >= p), s' partial, ||uhat||^2, uhat_p;
                 // the owner of row p pushes Y[p, 0..p-1] to every CTA
                 {
@@ -552,34 +605,35 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     double u2 = 0.0;
                     for (int i = ia + tid; i < nl; i += NT) {
                         const double* yr = sm.Y + (size_t)i * M2;
+                        const int xk = ys.x(i);
                         double d0 = 0.0, d1 = 0.0;
                         int k = 0;
                         for (; k + 1 < p; k += 2) {
-                            const double2 y = *reinterpret_cast<const double2*>(yr + k);
+                            const double2 y = *reinterpret_cast<const double2*>(yr + 2 * ((k >> 1) ^ xk));
                             d0 = fma(y.x, sm.gp[k], d0);
                             d1 = fma(y.y, sm.gp[k + 1], d1);
                         }
-                        if (k < p) d0 = fma(yr[k], sm.gp[k], d0);
+                        if (k < p) d0 = fma(yr[2 * ((k >> 1) ^ xk)], sm.gp[k], d0);
                         const double ui = sm.xl[i] - (d0 + d1);
                         sm.ul[i] = ui;
                         u2 = fma(ui, ui, u2);
                     }
                     if (p >= r0 && p < r1)
                         for (int k = tid; k < p; k += NT) {
-                            const double yv = sm.Y[(size_t)(p - r0) * M2 + k];
+                            const double yv = sm.Y[ys.at(p - r0, k)];
                             for (int c = 0; c < CS; c++) cl.map_shared_rank(sm.yrow, c)[k] = yv;
                         }
                     __syncthreads();
                     const int b = pxb;
-                    const double u2s = colacc(sm, M2, r0, ia, nl, p, [&](int i) { return sm.ul[i]; },
+                    const double u2s = colacc(sm, ys, r0, ia, nl, p, [&](int i) { return sm.ul[i]; },
                                               [&](int k, double v) { pub(b, k, v); }, u2, 0, NT, bsync);
                     if (tid == 0) {
                         pub(pxb, M2 + U2, u2s);
                         pub(pxb, M2 + U0, (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0);
                     }
-                    cl.sync();
+                    csync();
                 }
-                PH(1);
+                PH(2);
                 // ---------------- R2: scalars; s = s' - c Y[p,:]
                 double un = sqrt(csum(pxb, U2));
                 double u0 = csum(pxb, U0);
@@ -602,17 +656,17 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     const Aff ex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
                     block_reduce<1, false>(v, dm, di, sm.red, rpar);
                     if (tid == 0) { pub(b, M2 + FA, tot.a); pub(b, M2 + FB, tot.b); pub(b, M2 + Q1, v[0]); }
-                    cl.sync();
+                    csync();
                     const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(b, Q1);
                     fwd_pass2(Fj, FPj, fta, ftb, ex, rhs(0), sc, b, rhs);
                     pxb ^= 1;   // the buffer used above is now the "previous" one
-                    cl.sync();
+                    csync();
                     sweep(Fj);
                     if (crank == 0) {
                         __syncthreads();
                         push_x(sm.xl);
                     }
-                    cl.sync();
+                    csync();
                     first = false;
                     continue;
                 }
@@ -628,26 +682,27 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 }
                 pxb ^= 1;
                 __syncthreads();
+                PH(3);
                 // ---------------- TN (replicated): that, x', column p of T; column p of local Y
                 for (int l = tid; l < p; l += NT) {
                     double a1 = 0.0, a2 = 0.0;
-                    const double* tr = sm.T + (size_t)l * M2;
+                    const double* tr = sm.T + (size_t)l * TS;
                     for (int k = l; k < p; k++) {
                         a1 = fma(tr[k], sm.s[k], a1);
                         a2 = fma(tr[k], sm.yrow[k], a2);
                     }
                     const double that = -tt * a1;
                     sm.xp[l] = a2 + y0 * that;
-                    sm.T[(size_t)l * M2 + p] = that;
+                    sm.T[(size_t)l * TS + p] = that;
                 }
                 if (tid == 0) {
                     sm.xp[p] = tt * y0;
-                    sm.T[(size_t)p * M2 + p] = tt;
+                    sm.T[(size_t)p * TS + p] = tt;
                 }
                 for (int i = max(0, p - r0) + tid; i < nl; i += NT)
-                    sm.Y[(size_t)i * M2 + p] = (r0 + i == p) ? y0 : (zero_u ? 0.0 : sm.ul[i]);
+                    sm.Y[ys.at(i, p)] = (r0 + i == p) ? y0 : (zero_u ? 0.0 : sm.ul[i]);
                 __syncthreads();
-                PH(2);
+                PH(4);
                 // ---------------- D: q = Y_{p+1} x' - e_p, norms, argmax, look-ahead column,
                 // forward-sweep chunk maps over this CTA's steps
                 Aff fex{1.0, 0.0};
@@ -658,24 +713,27 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         const int gi = r0 + i;
                         const int le = min(gi + 1, p + 1);
                         const double* yr = sm.Y + (size_t)i * M2;
+                        const int xk = ys.x(i);
                         double d0 = 0.0, d1 = 0.0;
                         int k = 0;
                         for (; k + 1 < le; k += 2) {
-                            const double2 y = *reinterpret_cast<const double2*>(yr + k);
+                            const double2 y = *reinterpret_cast<const double2*>(yr + 2 * ((k >> 1) ^ xk));
                             d0 = fma(y.x, sm.xp[k], d0);
                             d1 = fma(y.y, sm.xp[k + 1], d1);
                         }
-                        if (k < le) d0 = fma(yr[k], sm.xp[k], d0);
+                        if (k < le) d0 = fma(yr[2 * ((k >> 1) ^ xk)], sm.xp[k], d0);
                         const double qi = (gi == p) ? (d0 + d1) - 1.0 : (d0 + d1);
                         sm.ql[i] = qi;
                         v[0] = fma(qi, qi, v[0]);
                         const double aq = fabs(qi);
                         v[1] += aq;
                         if (aq > qinf) { qinf = aq; qarg = gi; }
-                        if (la_done && gi >= p) v[2] = fma(yr[p], sm.x1l[i], v[2]);
+                        if (la_done && gi >= p) v[2] = fma(yr[2 * ((p >> 1) ^ xk) + (p & 1)], sm.x1l[i], v[2]);
                     }
                     block_reduce<3, true>(v, qinf, qarg, sm.red, rpar);   // also orders ql for the maps
+                    PH(5);
                     const Aff f = fwd_maps(Fj, FPj, fta, ftb, [&](int64_t i) { return sm.ql[i - r0]; });
+                    PH(6);
                     Aff tot;
                     fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
                     if (tid == 0) {
@@ -689,7 +747,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         if (crank == 0) pub(pxb, M2 + Q0, sm.ql[0]);
                         publ(M2 + GPN, v[2]);
                     }
-                    cl.sync();
+                    csync();
+                    PH(7);
                 }
                 // ---------------- TEST (replicated)
                 const double q2 = csum(pxb, Q2);
@@ -715,21 +774,21 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     la_have = la_done;
                     pxb ^= 1;
                     __syncthreads();
-                    PH(3);
+                    PH(8);
                 } else {
                     its++;
                     kin++;
-                    PH(3);
+                    PH(8);
                     // forward pass 2: exact carries -> t rows, gathered into CTA 0
                     const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(pxb, Q1);
                     fwd_pass2(Fj, FPj, fta, ftb, fex, PXo(0, pxb)[M2 + Q0], sc, pxb,
                               [&](int64_t i) { return sm.ql[i - r0]; });
                     pxb ^= 1;
-                    cl.sync();
-                    PH(5);
+                    csync();
+                    PH(10);
                     const bool la = !la_done && p + 1 < m && !(a.flags & 1);
                     sweep(Fj);
-                    if (timing) PH(6);
+                    if (timing) PH(11);
                     if (la) {
                         // look-ahead pass A of vector p+1 (every warp except CTA 0's warp 0):
                         // columns 0..p-1 of Y_{p+1} are final
@@ -742,31 +801,33 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                             };
                             const double* x1 = a.X1c + (j + 1) * n2v;
                             double x2n = 0.0;
+#pragma unroll 4
                             for (int i = tid - t0; i < nl; i += nth) {
                                 const double v = __ldcg(x1 + r0 + i);
                                 sm.x1l[i] = v;
                                 x2n = fma(v, v, x2n);
                             }
                             ssync();
-                            const double x2s = colacc(sm, M2, r0, 0, nl, p, [&](int i) { return sm.x1l[i]; },
+                            const double x2s = colacc(sm, ys, r0, 0, nl, p, [&](int i) { return sm.x1l[i]; },
                                                       [&](int k, double v) { publ(k, v); }, x2n, t0, nth, ssync);
                             if (tid == t0) publ(M2 + X2N, x2s);
                         }
                         la_done = true;
                     }
+                    PH(12);
                     if (crank == 0) {
                         __syncthreads();   // x complete in CTA 0's tf
                         push_x(sm.xl);
                     }
-                    cl.sync();   // x rows in every CTA, look-ahead partials published
-                    PH(7);
+                    csync();   // x rows in every CTA, look-ahead partials published
+                    PH(13);
                 }
             }
         }
-        cl.sync();   // shared workspace reuse by the unit's next cluster
+        csync();   // shared workspace reuse by the unit's next cluster
     }
     if (timing)
-        for (int k = 0; k < 8; k++) a.prof[k] = tacc[k];
+        for (int k = 0; k < 16; k++) a.prof[k] = tacc[k];
 }
 
 }  // namespace res

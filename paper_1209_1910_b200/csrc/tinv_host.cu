@@ -386,7 +386,7 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     if (const char* v = getenv("TINV_HANDOVER")) h->handover = atoi(v);
     if (const char* v = getenv("TINV_LEADER_W")) h->leader_w = atof(v);
     if (const char* v = getenv("TINV_LPT_M")) h->lpt_m = atof(v);
-    CK(cudaMalloc(&h->bnd, 32 * sizeof(double)));   // [0,4) bisection bounds, [8,16) resident timers
+    CK(cudaMalloc(&h->bnd, 32 * sizeof(double)));   // [0,4) bisection bounds, [8,24) resident timers, [24,32) batched
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     for (auto& q : h->rs) CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
@@ -508,7 +508,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     ev_record(h, 2);
     BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, h->perm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
                    h->X, h->unn, h->zscale, h->iters, h->out,
-                   h->profiling ? reinterpret_cast<unsigned long long*>(h->bnd + 16) : nullptr, 0, 0};
+                   h->profiling ? reinterpret_cast<unsigned long long*>(h->bnd + 24) : nullptr, 0, 0};
     FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->perm, Z, ldz, h->out};
     PackArgs pk{n, h->ldv, h->perm, h->out, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP, h->X, h->X1c};
     if (handover) {
@@ -742,7 +742,9 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             ra.X1c = h->X1c; ra.F = h->F; ra.FP = h->FP; ra.unn = h->unn; ra.Z = Z; ra.ldz = ldz;
             ra.iters = h->iters; ra.out = h->out; ra.handover = handover;
             if (const char* v = getenv("TINV_RES_FLAGS")) ra.flags = atoi(v);
-            ra.prof = (h->profiling && q == 0) ? reinterpret_cast<unsigned long long*>(h->bnd + 8) : nullptr;
+            // phase timers of unit 0 of one group (the first; TINV_PROF_GROUP picks another)
+            const int pg = getenv("TINV_PROF_GROUP") ? atoi(getenv("TINV_PROF_GROUP")) : 0;
+            ra.prof = (h->profiling && (int)q == pg) ? reinterpret_cast<unsigned long long*>(h->bnd + 8) : nullptr;
             CK(launch_resident(ra, rg.cs, units[q], rg.smem, sq));
             launches++;
             CK(cudaEventRecord(h->rev[q], sq));
@@ -905,16 +907,30 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     S.resident_groups = (int64_t)rgroups.size();
     if (h->profiling) {   // batched-LU sweep timers (warp 0) -> phase slots 0..5
         unsigned long long hb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        CK(cudaMemcpyAsync(hb, h->bnd + 16, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hb, h->bnd + 24, sizeof(hb), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (sc.size.empty())
             for (int k = 0; k < 6; k++) S.cwy_phase_ms[k] = (double)hb[k] * 1e-6;
     }
     if (h->profiling && !rgroups.empty()) {   // resident phase timers -> the last 8 phase slots
-        unsigned long long hp[8];
+        unsigned long long hp[16];
         CK(cudaMemcpyAsync(hp, h->bnd + 8, sizeof(hp), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        for (int k = 0; k < 8; k++) S.cwy_phase_ms[8 + k] = (double)hp[k] * 1e-6;
+        // fine timers (cwy_resident.cu) aggregated into the documented eight: A/R1 (+ leader,
+        // first reflector), TT+BC, R2+TN, D+TEST, staging, forward pass, back sweep (+LA), push
+        const int agg[16] = {0, 1, 1, 2, 2, 3, 3, 3, 3, 4, 5, 6, 6, 7, 0, 0};
+        for (int k = 0; k < 8; k++) S.cwy_phase_ms[8 + k] = 0.0;
+        int khz = 0;   // the timers count SM cycles: converted at the maximum SM clock
+        cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, h->device);
+        const double cyc_ms = 1.0 / std::max(1, khz);
+        for (int k = 0; k < 16; k++) S.cwy_phase_ms[8 + agg[k]] += (double)hp[k] * cyc_ms;
+        if (getenv("TINV_DEBUG")) {
+            static const char* nm[16] = {"A", "TT", "BC", "R2", "TN", "Drows", "Dmaps", "Dxchg", "TEST", "stage",
+                                         "fwd2", "sweep", "LA", "push", "leader", "refl1"};
+            fprintf(stderr, "[tinv] resident unit-0 phases (ms):");
+            for (int k = 0; k < 16; k++) fprintf(stderr, " %s %.3f", nm[k], (double)hp[k] * cyc_ms);
+            fprintf(stderr, "\n");
+        }
     }
     S.solve_bytes = 144.0 * (double)n * (double)n;  // factor 32n + 2 x 56n per vector
 

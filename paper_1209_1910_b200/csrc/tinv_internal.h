@@ -177,7 +177,7 @@ struct ResArgs {
     int64_t ldz;
     int* iters;
     PrepOut* out;
-    unsigned long long* prof;   // optional 8 phase timers of unit 0 (ns), or NULL
+    unsigned long long* prof;   // optional 16 phase timers of unit 0 (ns), or NULL
     int handover;           // clusters with m <= handover: the batched LU stopped the leader after
                             // x^(1), iterate it here (0: none)
     int flags;              // experiments: bit 0 disables the look-ahead pass
