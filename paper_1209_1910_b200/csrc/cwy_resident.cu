@@ -165,15 +165,27 @@ __device__ __forceinline__ void block_reduce(double (&v)[K], double& mx, long lo
     }
 }
 
-// Column accumulate over local rows [a, b) (local indices): out(k, sum_i Y[i][k] coef(i)) for
+// Distributed shared memory: the shared::cluster address of `p` in CTA `cta`, and a store to it
+// (explicit PTX: a 32-bit cluster address instead of a generic one).
+__device__ __forceinline__ uint32_t cl_addr(const void* p, int cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void st_cl(uint32_t a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
+// Column accumulate over local rows [a, b) (local indices): out(k, sum_i Y[i][k] coef(i), c) for
 // k < P, Y lower-trapezoidal (row gi = r0 + i holds columns 0..gi).  Threads [t0, t0 + nth)
 // (whole warps): a warp covers 32 / CPT rows per step with CPT lanes per row (two columns per
 // lane), two rows per lane in flight; lanes of a row slice combine by butterfly, warps through
-// shared memory in warp order (deterministic).  The per-thread scalar `s` is summed alongside
-// and returned to thread t0.
+// shared memory in warp order (deterministic); the column sums are delivered to NC
+// destinations by NC x ceil(P/2) threads (thread (pair, c) calls out(k, v, c)).  The
+// per-thread scalar `s` is summed alongside and returned to every thread.
 template <class Coef, class Out, class Sync>
 __device__ __forceinline__ double colacc(const L& sm, const YSw& ys, int r0, int a, int b, int P, Coef coef, Out out,
-                                         double s, int t0, int nth, Sync sync) {
+                                         int NC, double s, int t0, int nth, Sync sync) {
     const int t = threadIdx.x - t0, w = t >> 5, ln = t & 31, W = nth >> 5;
     const int KP = max(1, (P + 1) >> 1);
     const int CPT = min(32, pow2ceil(KP));
@@ -207,19 +219,21 @@ __device__ __forceinline__ double colacc(const L& sm, const YSw& ys, int r0, int
     if (rl == 0) sm.acc[w * 32 + cp] = make_double2(a0, a1);
     if (ln == 0) sm.cred[w] = s;
     sync();
-    if (2 * t < P) {
-        double v0 = 0.0, v1 = 0.0;
-        for (int q = 0; q < W; q++) {
-            const double2 v = sm.acc[q * 32 + t];
-            v0 += v.x;
-            v1 += v.y;
+    for (int u = t; u < KP * NC; u += nth) {
+        const int pc = u / NC, c = u - pc * NC;
+        if (2 * pc < P) {
+            double v0 = 0.0, v1 = 0.0;
+            for (int q = 0; q < W; q++) {
+                const double2 v = sm.acc[q * 32 + pc];
+                v0 += v.x;
+                v1 += v.y;
+            }
+            out(2 * pc, v0, c);
+            if (2 * pc + 1 < P) out(2 * pc + 1, v1, c);
         }
-        out(2 * t, v0);
-        if (2 * t + 1 < P) out(2 * t + 1, v1);
     }
     double r = 0.0;
-    if (t == 0)
-        for (int q = 0; q < W; q++) r += sm.cred[q];
+    for (int q = 0; q < W; q++) r += sm.cred[q];
     return r;
 }
 
@@ -323,11 +337,20 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     // Exchange (push model): a CTA stores its record into slot [buffer][its rank] of every CTA
     // of the cluster; after the cluster barrier every read is local.
     auto PXo = [&](int c, int b) -> const double* { return sm.PX + ((size_t)b * CS + c) * XW; };
-    auto pub = [&](int b, int k, double v) {
-        for (int c = 0; c < CS; c++) cl.map_shared_rank(sm.PX, c)[((size_t)b * CS + crank) * XW + k] = v;
+    // slot k of this CTA's record in buffer b (look-ahead area: b < 0) of CTA c
+    auto pub1 = [&](int b, int k, double v, int c) {
+        const double* own = (b < 0) ? sm.PXL + (size_t)crank * XW : sm.PX + ((size_t)b * CS + crank) * XW;
+        st_cl(cl_addr(own + k, c), v);
     };
-    auto publ = [&](int k, double v) {
-        for (int c = 0; c < CS; c++) cl.map_shared_rank(sm.PXL, c)[(size_t)crank * XW + k] = v;
+    // K scalars (val(k) -> slot, value; every calling thread can evaluate it) to every CTA, one
+    // store per thread
+    auto pubs = [&](int b, int K, auto val) {
+        for (int t = tid; t < K * CS; t += NT) {
+            const int k = t / CS, c = t - k * CS;
+            int slot;
+            const double v = val(k, slot);
+            pub1(b, M2 + slot, v, c);
+        }
     };
     auto csum = [&](int b, int slot) {   // sum over CTAs of a scalar slot, fixed order
         double v = 0.0;
@@ -348,9 +371,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     // x rows from CTA 0's back sweep into every CTA's `dst` (called by all threads of CTA 0)
     auto push_x = [&](double* dst) {
         for (int c = 0; c < CS; c++) {
-            double* d = cl.map_shared_rank(dst, c);
+            const uint32_t d = cl_addr(dst, c);
             const int c0 = c * RL, c1 = (int)min64(n, (int64_t)c0 + RL);
-            for (int i = c0 + tid; i < c1; i += NT) d[i - c0] = sm.tf[i];
+#pragma unroll 4
+            for (int i = c0 + tid; i < c1; i += NT) st_cl(d + 8u * (uint32_t)(i - c0), sm.tf[i]);
         }
     };
     // forward pass 2 of a chained solve: exact carries from the composed maps (exchange buffer
@@ -360,12 +384,12 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         Aff pre{1.0, 0.0};
         for (int c2 = 0; c2 < crank; c2++) pre = comp(Aff{PXo(c2, b)[M2 + FA], PXo(c2, b)[M2 + FB]}, pre);
         double cc = fma(fex.a, fma(pre.a, q0, pre.b), fex.b);
-        double* tf0 = cl.map_shared_rank(sm.tf, 0);
+        const uint32_t tf0 = cl_addr(sm.tf, 0);
         auto step = [&](int s, double l, double rr, bool sw, double bn) {
             double y;
             if (sw) { y = bn; cc = fma(-l, bn, cc); }
             else { y = cc; cc = fma(-l, cc, bn); }
-            tf0[s] = sc * y * rr;
+            st_cl(tf0 + 8u * (uint32_t)s, sc * y * rr);
         };
         int s = fta;
         for (; s + 4 <= ftb; s += 4) {   // the four steps' loads in flight together
@@ -384,8 +408,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
             const double2 lr = __ldg(reinterpret_cast<const double2*>(Fj + (int64_t)s * 4));
             step(s, lr.x, lr.y, FPj[s] != 0, rhs(s + 1));
         }
-        if (ftb == n - 1 && fta < ftb) tf0[n - 1] = sc * cc * __ldg(Fj + (n - 1) * 4 + 1);
-        else if (n == 1 && tid == 0) tf0[0] = sc * cc * __ldg(Fj + 1);
+        if (ftb == n - 1 && fta < ftb) st_cl(tf0 + 8u * (uint32_t)(n - 1), sc * cc * __ldg(Fj + (n - 1) * 4 + 1));
+        else if (n == 1 && tid == 0) st_cl(tf0, sc * cc * __ldg(Fj + 1));
     };
     // forward maps (pass 1) of this thread's steps [fta, ftb), rhs(i) local rows
     auto fwd_maps = [&](const double* Fj, const int8_t* FPj, int fta, int ftb, auto rhs) {
@@ -462,15 +486,21 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 const Aff f = fwd_maps(Fj, FPj, fta, ftb, [&](int64_t i) { return sm.ql[i - r0]; });
                 Aff tot;
                 const Aff fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
-                if (tid == 0) {
-                    pub(pxb, M2 + Q2, v[0]);
-                    pub(pxb, M2 + Q1, v[1]);
-                    pub(pxb, M2 + QINF, qinf);
-                    pub(pxb, M2 + QARG, (double)qarg);
-                    pub(pxb, M2 + QSGN, (qinf >= 0.0 && sm.ql[qarg - r0] < 0.0) ? -1.0 : 1.0);
-                    pub(pxb, M2 + FA, tot.a);
-                    pub(pxb, M2 + FB, tot.b);
-                    if (crank == 0) pub(pxb, M2 + Q0, sm.ql[0]);
+                {
+                    const double sg = (qinf >= 0.0 && sm.ql[qarg - r0] < 0.0) ? -1.0 : 1.0;
+                    const double q0v = sm.ql[0];
+                    pubs(pxb, crank == 0 ? 8 : 7, [&](int k, int& slot) {
+                        switch (k) {
+                            case 0: slot = Q2; return v[0];
+                            case 1: slot = Q1; return v[1];
+                            case 2: slot = QINF; return qinf;
+                            case 3: slot = QARG; return (double)qarg;
+                            case 4: slot = QSGN; return sg;
+                            case 5: slot = FA; return tot.a;
+                            case 6: slot = FB; return tot.b;
+                            default: slot = Q0; return q0v;
+                        }
+                    });
                 }
                 csync();
                 const double q2t = csum(pxb, Q2);
@@ -520,9 +550,13 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 v[0] = fma(zi, zi, v[0]);
             }
             block_reduce<1, false>(v, dm, di, sm.red, rpar);
-            if (tid == 0) {
-                pub(pxb, M2 + U2, v[0]);
-                if (crank == 0) pub(pxb, M2 + U0, sm.ul[0]);
+            {
+                const double u0v = sm.ul[0];
+                pubs(pxb, crank == 0 ? 2 : 1, [&](int k, int& slot) {
+                    if (k == 0) { slot = U2; return v[0]; }
+                    slot = U0;
+                    return u0v;
+                });
             }
             csync();
             const double un = sqrt(csum(pxb, U2));
@@ -575,8 +609,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     for (int i = tid; i < nl; i += NT) s = fma(sm.xl[i], sm.xl[i], s);
                     const int b = pxb;
                     const double x2p = colacc(sm, ys, r0, 0, nl, p, [&](int i) { return sm.xl[i]; },
-                                              [&](int k, double v) { pub(b, k, v); }, s, 0, NT, bsync);
-                    if (tid == 0) pub(pxb, M2 + X2, x2p);
+                                              [&](int k, double v, int c) { pub1(b, k, v, c); }, CS, s, 0, NT, bsync);
+                    if (tid < CS) pub1(pxb, M2 + X2, x2p, tid);
                     csync();
                     for (int k = tid; k < p; k += NT) {
                         double v = 0.0;
@@ -619,17 +653,21 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         u2 = fma(ui, ui, u2);
                     }
                     if (p >= r0 && p < r1)
-                        for (int k = tid; k < p; k += NT) {
-                            const double yv = sm.Y[ys.at(p - r0, k)];
-                            for (int c = 0; c < CS; c++) cl.map_shared_rank(sm.yrow, c)[k] = yv;
+                        for (int t = tid; t < p * CS; t += NT) {
+                            const int k = t / CS, c = t - k * CS;
+                            st_cl(cl_addr(sm.yrow + k, c), sm.Y[ys.at(p - r0, k)]);
                         }
                     __syncthreads();
                     const int b = pxb;
                     const double u2s = colacc(sm, ys, r0, ia, nl, p, [&](int i) { return sm.ul[i]; },
-                                              [&](int k, double v) { pub(b, k, v); }, u2, 0, NT, bsync);
-                    if (tid == 0) {
-                        pub(pxb, M2 + U2, u2s);
-                        pub(pxb, M2 + U0, (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0);
+                                              [&](int k, double v, int c) { pub1(b, k, v, c); }, CS, u2, 0, NT, bsync);
+                    {
+                        const double u0v = (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0;
+                        pubs(pxb, 2, [&](int k, int& slot) {
+                            if (k == 0) { slot = U2; return u2s; }
+                            slot = U0;
+                            return u0v;
+                        });
                     }
                     csync();
                 }
@@ -655,7 +693,12 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     Aff tot;
                     const Aff ex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
                     block_reduce<1, false>(v, dm, di, sm.red, rpar);
-                    if (tid == 0) { pub(b, M2 + FA, tot.a); pub(b, M2 + FB, tot.b); pub(b, M2 + Q1, v[0]); }
+                    pubs(b, 3, [&](int k, int& slot) {
+                        if (k == 0) { slot = FA; return tot.a; }
+                        if (k == 1) { slot = FB; return tot.b; }
+                        slot = Q1;
+                        return v[0];
+                    });
                     csync();
                     const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(b, Q1);
                     fwd_pass2(Fj, FPj, fta, ftb, ex, rhs(0), sc, b, rhs);
@@ -736,17 +779,25 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     PH(6);
                     Aff tot;
                     fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
-                    if (tid == 0) {
-                        pub(pxb, M2 + Q2, v[0]);
-                        pub(pxb, M2 + Q1, v[1]);
-                        pub(pxb, M2 + QINF, qinf);
-                        pub(pxb, M2 + QARG, (double)qarg);
-                        pub(pxb, M2 + QSGN, (qinf >= 0.0 && sm.ql[qarg - r0] < 0.0) ? -1.0 : 1.0);
-                        pub(pxb, M2 + FA, tot.a);
-                        pub(pxb, M2 + FB, tot.b);
-                        if (crank == 0) pub(pxb, M2 + Q0, sm.ql[0]);
-                        publ(M2 + GPN, v[2]);
+                    PH(12);
+                    {
+                        const double sg = (qinf >= 0.0 && sm.ql[qarg - r0] < 0.0) ? -1.0 : 1.0;
+                        const double q0v = sm.ql[0];
+                        pubs(pxb, crank == 0 ? 8 : 7, [&](int k, int& slot) {
+                            switch (k) {
+                                case 0: slot = Q2; return v[0];
+                                case 1: slot = Q1; return v[1];
+                                case 2: slot = QINF; return qinf;
+                                case 3: slot = QARG; return (double)qarg;
+                                case 4: slot = QSGN; return sg;
+                                case 5: slot = FA; return tot.a;
+                                case 6: slot = FB; return tot.b;
+                                default: slot = Q0; return q0v;
+                            }
+                        });
+                        if (tid >= NT - CS) pub1(-1, M2 + GPN, v[2], tid - (NT - CS));
                     }
+                    PH(15);
                     csync();
                     PH(7);
                 }
@@ -809,8 +860,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                             }
                             ssync();
                             const double x2s = colacc(sm, ys, r0, 0, nl, p, [&](int i) { return sm.x1l[i]; },
-                                                      [&](int k, double v) { publ(k, v); }, x2n, t0, nth, ssync);
-                            if (tid == t0) publ(M2 + X2N, x2s);
+                                                      [&](int k, double v, int c) { pub1(-1, k, v, c); }, CS, x2n, t0,
+                                                      nth, ssync);
+                            if (tid >= t0 && tid < t0 + CS) pub1(-1, M2 + X2N, x2s, tid - t0);
                         }
                         la_done = true;
                     }

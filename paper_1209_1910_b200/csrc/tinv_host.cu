@@ -91,7 +91,7 @@ struct tinv_s {
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
     int res_cs2 = 1000, res_cs4 = 1000;   // m from which a cluster gets >= 2 / 4 CTAs
     int handover = 1;                 // narrow leaders finish in the resident kernel (n <= 2048)
-    double leader_w = 0.5;            // LPT weight of a handed-over leader (vector equivalents)
+    double leader_w = 1.0;            // LPT weight of a handed-over leader (vector equivalents)
     double lpt_m = 1.0;               // LPT weight per vector: 1 + lpt_m m / 32
     // row split over real ranks: peers' cWY workspaces mapped through CUDA IPC
     int* res_buf = nullptr;           // resident kernel unit lists (device)
