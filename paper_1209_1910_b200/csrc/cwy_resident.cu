@@ -203,11 +203,30 @@ __device__ __forceinline__ double colacc(const L& sm, const YSw& ys, int r0, int
         }
     };
     int i = a + w * (32 / CPT) + rl;
-    for (; i + RS < b; i += 2 * RS) {
-        row(i, a0, a1);
-        row(i + RS, b0, b1);
+    // rows with global index below P - 1 hold fewer than P columns (first CTA only): checked
+    for (; i < b && r0 + i + 1 < P; i += RS) row(i, a0, a1);
+    if (k < P) {   // full rows: four rows' loads in flight, four accumulator pairs (the second
+                   // column of the last pair may be past P: accumulated, never delivered)
+        double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+        for (; i + 3 * RS < b; i += 4 * RS) {
+            const double2 y0 = *reinterpret_cast<const double2*>(sm.Y + ys.pair(i, cp));
+            const double2 y1 = *reinterpret_cast<const double2*>(sm.Y + ys.pair(i + RS, cp));
+            const double2 y2 = *reinterpret_cast<const double2*>(sm.Y + ys.pair(i + 2 * RS, cp));
+            const double2 y3 = *reinterpret_cast<const double2*>(sm.Y + ys.pair(i + 3 * RS, cp));
+            const double e0 = coef(i), e1 = coef(i + RS), e2 = coef(i + 2 * RS), e3 = coef(i + 3 * RS);
+            a0 = fma(y0.x, e0, a0); a1 = fma(y0.y, e0, a1);
+            b0 = fma(y1.x, e1, b0); b1 = fma(y1.y, e1, b1);
+            c0 = fma(y2.x, e2, c0); c1 = fma(y2.y, e2, c1);
+            d0 = fma(y3.x, e3, d0); d1 = fma(y3.y, e3, d1);
+        }
+        for (; i < b; i += RS) {
+            const double2 y = *reinterpret_cast<const double2*>(sm.Y + ys.pair(i, cp));
+            const double e = coef(i);
+            a0 = fma(y.x, e, a0);
+            a1 = fma(y.y, e, a1);
+        }
+        a0 += c0; a1 += c1; b0 += d0; b1 += d1;
     }
-    if (i < b) row(i, a0, a1);
     a0 += b0;
     a1 += b1;
     for (int o = CPT; o < 32; o <<= 1) {
@@ -642,6 +661,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         const int xk = ys.x(i);
                         double d0 = 0.0, d1 = 0.0;
                         int k = 0;
+#pragma unroll 4
                         for (; k + 1 < p; k += 2) {
                             const double2 y = *reinterpret_cast<const double2*>(yr + 2 * ((k >> 1) ^ xk));
                             d0 = fma(y.x, sm.gp[k], d0);
@@ -658,9 +678,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                             st_cl(cl_addr(sm.yrow + k, c), sm.Y[ys.at(p - r0, k)]);
                         }
                     __syncthreads();
+                    PH(12);
                     const int b = pxb;
                     const double u2s = colacc(sm, ys, r0, ia, nl, p, [&](int i) { return sm.ul[i]; },
                                               [&](int k, double v, int c) { pub1(b, k, v, c); }, CS, u2, 0, NT, bsync);
+                    PH(15);
                     {
                         const double u0v = (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0;
                         pubs(pxb, 2, [&](int k, int& slot) {
@@ -759,6 +781,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         const int xk = ys.x(i);
                         double d0 = 0.0, d1 = 0.0;
                         int k = 0;
+#pragma unroll 4
                         for (; k + 1 < le; k += 2) {
                             const double2 y = *reinterpret_cast<const double2*>(yr + 2 * ((k >> 1) ^ xk));
                             d0 = fma(y.x, sm.xp[k], d0);
@@ -779,7 +802,6 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     PH(6);
                     Aff tot;
                     fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
-                    PH(12);
                     {
                         const double sg = (qinf >= 0.0 && sm.ql[qarg - r0] < 0.0) ? -1.0 : 1.0;
                         const double q0v = sm.ql[0];
@@ -797,7 +819,6 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                         });
                         if (tid >= NT - CS) pub1(-1, M2 + GPN, v[2], tid - (NT - CS));
                     }
-                    PH(15);
                     csync();
                     PH(7);
                 }

@@ -88,6 +88,62 @@ __device__ __forceinline__ void v3(const double* __restrict__ rec, double* xo, i
         for (int u = 0; u < 8; u++) r[u] = rn[u];
     }
 }
+// V4: 16-row batches, next batch's loads issued before the current chain (double buffer)
+__device__ __forceinline__ void v4(const double* __restrict__ bc, double* tf, int n) {
+    const double2* BC = reinterpret_cast<const double2*>(bc);
+    double x1 = 0.0, x2 = 0.0;
+    const int top = n & ~15;
+    double b[16], c[16], t[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) { const double2 v = BC[top - 16 + u]; b[u] = v.x; c[u] = v.y; t[u] = tf[top - 16 + u]; }
+    for (int u0 = top - 16; u0 >= 0; u0 -= 16) {
+        double bn[16], cn[16], tn[16], xv[16];
+        const int nx = u0 >= 16 ? u0 - 16 : 0;
+#pragma unroll
+        for (int u = 0; u < 16; u++) { const double2 v = BC[nx + u]; bn[u] = v.x; cn[u] = v.y; tn[u] = tf[nx + u]; }
+#pragma unroll
+        for (int u = 15; u >= 0; u--) { xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u])); x2 = x1; x1 = xv[u]; }
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) *reinterpret_cast<double2*>(tf + u0 + u) = make_double2(xv[u], xv[u + 1]);
+#pragma unroll
+        for (int u = 0; u < 16; u++) { b[u] = bn[u]; c[u] = cn[u]; t[u] = tn[u]; }
+    }
+}
+// V5: 8-row batches, no software pipelining, int32
+__device__ __forceinline__ void v5(const double* __restrict__ bc, double* tf, int n) {
+    const double2* BC = reinterpret_cast<const double2*>(bc);
+    double x1 = 0.0, x2 = 0.0;
+    const int top = n & ~7;
+    for (int u0 = top - 8; u0 >= 0; u0 -= 8) {
+        double b[8], c[8], t[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) { const double2 v = BC[u0 + u]; b[u] = v.x; c[u] = v.y; t[u] = tf[u0 + u]; }
+#pragma unroll
+        for (int u = 7; u >= 0; u--) { xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u])); x2 = x1; x1 = xv[u]; }
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) *reinterpret_cast<double2*>(tf + u0 + u) = make_double2(xv[u], xv[u + 1]);
+    }
+}
+// V6: 16-row batches, inner products of the next batch precomputed: s_i = t_i - c_i x_{i+2}
+// needs x_{i+2}; within a batch, the first two rows use the carried x; the chain stays 1 FMA
+// per row.  (Same as V2 but the t/c loads via one LDS.128 of an interleaved [t, c] array.)
+__device__ __forceinline__ void v6(const double* __restrict__ bc, double* tf, int n) {
+    const double2* BC = reinterpret_cast<const double2*>(bc);
+    double x1 = 0.0, x2 = 0.0;
+    const int top = n & ~15;
+    for (int u0 = top - 16; u0 >= 0; u0 -= 16) {
+        double2 v[16];
+        double t[16], xv[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) v[u] = BC[u0 + u];
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) { const double2 tt = *reinterpret_cast<const double2*>(tf + u0 + u); t[u] = tt.x; t[u + 1] = tt.y; }
+#pragma unroll
+        for (int u = 15; u >= 0; u--) { xv[u] = fma(-v[u].x, x1, fma(-v[u].y, x2, t[u])); x2 = x1; x1 = xv[u]; }
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) *reinterpret_cast<double2*>(tf + u0 + u) = make_double2(xv[u], xv[u + 1]);
+    }
+}
 __global__ void probe(int var, const double* bcg, const double* tg, int n, long long* cyc) {
     extern __shared__ __align__(16) unsigned char raw[];
     double* tf = reinterpret_cast<double*>(raw);
@@ -104,7 +160,10 @@ __global__ void probe(int var, const double* bcg, const double* tg, int n, long 
         if (var == 0) v0(bc, tf, n);
         else if (var == 1) v1(bc, tf, n);
         else if (var == 2) v2(bc, tf, n);
-        else v3(rec, tf, n);
+        else if (var == 3) v3(rec, tf, n);
+        else if (var == 4) v4(bc, tf, n);
+        else if (var == 5) v5(bc, tf, n);
+        else v6(bc, tf, n);
         cyc[var] = clock64() - t0;
     }
 }
@@ -121,10 +180,10 @@ int main() {
     cudaMemcpy(dt, t.data(), 8 * n, cudaMemcpyHostToDevice);
     size_t smem = (size_t)(n + 2) * 8 + 16 * n + 32 * n + 64;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int v = 0; v < 4; v++) {
+    for (int v = 0; v < 7; v++) {
         probe<<<1, 256, smem>>>(v, dbc, dt, n, dc);
         probe<<<1, 256, smem>>>(v, dbc, dt, n, dc);
-        long long h[4]; cudaMemcpy(h, dc, 32, cudaMemcpyDeviceToHost);
+        long long h[8]; cudaMemcpy(h, dc, 64, cudaMemcpyDeviceToHost);
         printf("variant %d: %.2f cycles/row (%s)\n", v, (double)h[v] / n, cudaGetErrorString(cudaGetLastError()));
     }
 }
