@@ -135,7 +135,12 @@ typedef struct {
                                    (forward sweep), chained solve (back sweep), wait for the
                                    look-ahead pass overlapped with the back sweep; then the
                                    narrow-cluster streams: ring wait, stage compute, stage
-                                   barrier; one spare */
+                                   barrier; one spare.  With resident launches slots 8..15
+                                   hold the resident kernel's unit-0 phases (A/R1, TT+BC,
+                                   R2+TN, D+TEST, back-sweep staging, forward pass, back
+                                   sweep, x copy); with no persistent launch slots 0..3 hold
+                                   the batched LU's warp-0 sweeps (factor, back, forward,
+                                   back) */
 } tinv_stats_t;
 
 int tinv_set_profiling(tinv_t h, int enable);
