@@ -57,6 +57,7 @@ def lib():
             "orc_bisect": (None, [I64, P, P, P]),
             "orc_eigvecs": (I64, [I64, P, P, P, P, I64, C.c_uint64, P]),
             "orc_eigvecs_range": (I64, [I64, P, P, P, P, I64, C.c_uint64, P, I64, I64]),
+            "orc_eigvecs_mgs_range": (I64, [I64, P, P, P, P, I64, C.c_uint64, P, I64, I64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -203,8 +204,9 @@ def bisect(d, e):
     return w
 
 
-def eigvecs(d, e, w, seed=1, j_lo=0, j_hi=None, return_iters=False):
-    """Alg. 4 (DSTEIN-cWY, PAPER.md:681-716).  Returns (Z, info[, iters]); Z is
+def eigvecs(d, e, w, seed=1, j_lo=0, j_hi=None, return_iters=False, mgs=False):
+    """Alg. 4 (DSTEIN-cWY), or with mgs=True Alg. 1 (classical MGS
+    reorthogonalisation, PAPER.md:140-166).  Returns (Z, info[, iters]); Z is
     column-major n x (j_hi - j_lo) holding eigenvectors j_lo .. j_hi-1."""
     d = _f64(d)
     w = _f64(w)
@@ -215,8 +217,8 @@ def eigvecs(d, e, w, seed=1, j_lo=0, j_hi=None, return_iters=False):
     Z = np.zeros((n, j_hi - j_lo), order="F")
     iters = np.zeros(n, dtype=np.int32)
     z0 = C.c_void_p(Z.ctypes.data - 8 * n * int(j_lo))
-    info = lib().orc_eigvecs_range(n, _p(d), _p(_e(e, n)), _p(w), z0,
-                                   n, int(seed), _p(iters), int(j_lo), int(j_hi))
+    fn = lib().orc_eigvecs_mgs_range if mgs else lib().orc_eigvecs_range
+    info = fn(n, _p(d), _p(_e(e, n)), _p(w), z0, n, int(seed), _p(iters), int(j_lo), int(j_hi))
     if return_iters:
         return Z, int(info), iters
     return Z, int(info)

@@ -496,10 +496,24 @@ static double norminf(int64_t n, const double* x)
     return s;
 }
 
-/* One cluster [j1, j2), vectors computed for j < jstop, written for j in [wlo, whi). */
+/* Alg. 1 l.10-12, the classical reorthogonalisation: modified Gram-Schmidt
+ * of x against the cluster's accepted vectors V[:, 0..p-1] (column-major, ld n), in order:
+ * x <- x - <x, v_i> v_i. */
+static void mgs_project(int64_t n, int64_t p, const double* V, double* x)
+{
+    for (int64_t i = 0; i < p; i++) {
+        const double* v = V + i * n;
+        double dot = 0.0;
+        for (int64_t r = 0; r < n; r++) dot += x[r] * v[r];
+        for (int64_t r = 0; r < n; r++) x[r] = x[r] - dot * v[r];
+    }
+}
+
+/* One cluster [j1, j2), vectors computed for j < jstop, written for j in [wlo, whi).
+ * mgs = 0: Alg. 4 (compact WY); mgs = 1: Alg. 1 (classical MGS) with the same readings. */
 static int64_t do_cluster(int64_t n, const double* d, const double* e, const double* wt,
                           double tnorm, uint64_t seed, int64_t j1, int64_t j2, int64_t jstop,
-                          int64_t wlo, int64_t whi, double* Z, int64_t ldz, int32_t* iters)
+                          int64_t wlo, int64_t whi, double* Z, int64_t ldz, int32_t* iters, int mgs)
 {
     int64_t m = j2 - j1;
     int64_t nflag = 0;
@@ -514,14 +528,16 @@ static int64_t do_cluster(int64_t n, const double* d, const double* e, const dou
     double* zacc = (double*)malloc(sizeof(double) * (size_t)n);
     orc_cwy_t acc;
     acc.P = NULL;
-    if (m > 1) orc_cwy_init(&acc, n, m);
+    if (m > 1 && !mgs) orc_cwy_init(&acc, n, m);
+    /* MGS: the cluster's accepted vectors, column-major n x m */
+    double* V = (m > 1 && mgs) ? (double*)malloc(sizeof(double) * (size_t)n * (size_t)m) : NULL;
     double thr = sqrt(0.1 / (double)n);                /* reading 9 (DSTEIN-style) */
 
     for (int64_t j = j1; j < jstop; j++) {
         int64_t p = j - j1;                            /* j_c, Alg.4 l.9 */
         orc_lu_factor(n, d, e, wt[j], tnorm, l, piv, u0, u1, u2);
         double unn = fabs(u0[n - 1]);
-        if (p == 1) orc_cwy_first(&acc, zacc);         /* Alg.4 l.10-11: Y_1,T_1 from v_{j1} */
+        if (p == 1 && !mgs) orc_cwy_first(&acc, zacc); /* Alg.4 l.10-11: Y_1,T_1 from v_{j1} */
         int converged = 0, its = 0, degen_final = 0;
         for (int64_t rs = 0; rs <= MAXRESTART; rs++) {
             orc_start_vector(n, seed, j, rs, b);       /* Alg.4 l.2 */
@@ -537,6 +553,19 @@ static int64_t do_cluster(int64_t n, const double* d, const double* e, const dou
                 if (p == 0) {
                     rinf = norminf(n, x);
                     memcpy(b, x, sizeof(double) * (size_t)n);
+                } else if (mgs) {
+                    /* Alg.1 l.10-12: MGS against v_{j1} .. v_{j-1}; the iterate r of reading 9
+                     * is the projected x (in exact arithmetic |c| q of the cWY step); the
+                     * degeneracy test of reading 16 compares its norm with ||x||_2 */
+                    double nx = nrm2(n, x);
+                    memcpy(q, x, sizeof(double) * (size_t)n);
+                    mgs_project(n, p, V, q);
+                    if (nrm2(n, q) <= (double)n * EPS * nx) {
+                        if (rs < MAXRESTART) { degenerate = 1; break; }
+                        degen_final = 1;
+                    }
+                    rinf = norminf(n, q);
+                    memcpy(b, q, sizeof(double) * (size_t)n);
                 } else {
                     double c, nu;
                     orc_cwy_step(&acc, p, x, q, &c, &nu);                              /* l.13-16 */
@@ -554,17 +583,19 @@ static int64_t do_cluster(int64_t n, const double* d, const double* e, const dou
         }
         if (!converged || degen_final) nflag++;
         finalize_vector(n, b, zacc);
+        if (V) memcpy(V + p * n, zacc, sizeof(double) * (size_t)n);
         if (iters && j >= wlo && j < whi) iters[j] = its;
         if (j >= wlo && j < whi) memcpy(Z + j * ldz, zacc, sizeof(double) * (size_t)n);
     }
-    if (m > 1) orc_cwy_free(&acc);
+    if (m > 1 && !mgs) orc_cwy_free(&acc);
+    free(V);
     free(l); free(piv); free(u0); free(u1); free(u2); free(b); free(x); free(q); free(zacc);
     return nflag;
 }
 
-int64_t orc_eigvecs_range(int64_t n, const double* d, const double* e, const double* w,
-                          double* Z, int64_t ldz, uint64_t seed, int32_t* iters,
-                          int64_t j_lo, int64_t j_hi)
+static int64_t eigvecs_range(int64_t n, const double* d, const double* e, const double* w,
+                             double* Z, int64_t ldz, uint64_t seed, int32_t* iters,
+                             int64_t j_lo, int64_t j_hi, int mgs)
 {
     if (n < 1 || ldz < n || !d || !w || !Z || (n > 1 && !e)) return -1;
     for (int64_t j = 1; j < n; j++) if (!(w[j] >= w[j - 1])) return -4;
@@ -586,10 +617,24 @@ int64_t orc_eigvecs_range(int64_t n, const double* d, const double* e, const dou
         int64_t j1 = cs[c], j2 = cs[c + 1];
         if (j2 <= j_lo || j1 >= j_hi) continue;
         int64_t jstop = j2 < j_hi ? j2 : j_hi;
-        nflag += do_cluster(n, d, e, wt, tnorm, seed, j1, j2, jstop, j_lo, j_hi, Z, ldz, iters);
+        nflag += do_cluster(n, d, e, wt, tnorm, seed, j1, j2, jstop, j_lo, j_hi, Z, ldz, iters, mgs);
     }
     free(cs); free(wt);
     return nflag;
+}
+
+int64_t orc_eigvecs_range(int64_t n, const double* d, const double* e, const double* w,
+                          double* Z, int64_t ldz, uint64_t seed, int32_t* iters,
+                          int64_t j_lo, int64_t j_hi)
+{
+    return eigvecs_range(n, d, e, w, Z, ldz, seed, iters, j_lo, j_hi, 0);
+}
+
+int64_t orc_eigvecs_mgs_range(int64_t n, const double* d, const double* e, const double* w,
+                              double* Z, int64_t ldz, uint64_t seed, int32_t* iters,
+                              int64_t j_lo, int64_t j_hi)
+{
+    return eigvecs_range(n, d, e, w, Z, ldz, seed, iters, j_lo, j_hi, 1);
 }
 
 int64_t orc_eigvecs(int64_t n, const double* d, const double* e, const double* w,

@@ -111,6 +111,14 @@ int64_t orc_eigvecs_range(int64_t n, const double* d, const double* e, const dou
                           double* Z, int64_t ldz, uint64_t seed, int32_t* iters,
                           int64_t j_lo, int64_t j_hi);
 
+/* Alg. 1 (classical inverse iteration): the same
+ * factorization, start vectors, scaling, stopping rule and restarts as Alg. 4, with the
+ * clustered vectors reorthogonalised by MGS against the cluster's accepted vectors after
+ * every solve instead of the compact-WY step.  Same arguments as orc_eigvecs_range. */
+int64_t orc_eigvecs_mgs_range(int64_t n, const double* d, const double* e, const double* w,
+                              double* Z, int64_t ldz, uint64_t seed, int32_t* iters,
+                              int64_t j_lo, int64_t j_hi);
+
 #ifdef __cplusplus
 }
 #endif

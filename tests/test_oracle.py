@@ -406,3 +406,63 @@ def test_eigvecs_seed_insensitive_where_determined():
     Z2, _ = O.eigvecs(d, e, w, seed=2)
     worst_vec, worst_sig, nv, ng = parity_report(w, O.tnorm(d, e), Z1, Z2)
     assert worst_vec <= 1e-10 and worst_sig >= 1 - 1e-10
+
+
+# ---------------------------------------------------------------- Alg. 1 (classical MGS)
+# the comparison path.  Pinned by the closed-form Laplacian vectors, by
+# LAPACK on cfg2, by the glued-Wilkinson subspaces, and by the compact-WY oracle (the two
+# reorthogonalisations orthogonalise the same solve outputs; they agree up to rounding where
+# the vectors are determined).
+
+
+def test_eigvecs_mgs_laplacian_closed_form():
+    n = 200
+    d, e = W.laplacian(n)
+    k = np.arange(1, n + 1)
+    lam = 2.0 - 2.0 * np.cos(k * np.pi / (n + 1))
+    Z, info, its = O.eigvecs(d, e, lam, seed=1, return_iters=True, mgs=True)
+    assert info == 0 and (its == 2).all()
+    V = _laplacian_vectors(n)
+    cs = O.clusters(lam, 4.0)
+    for a, b in zip(cs[:-1], cs[1:]):
+        if b - a == 1:
+            assert vec_diff_upto_sign(Z[:, a], V[:, a]) <= 1e-10
+        else:
+            assert sigma_min(Z[:, a:b], V[:, a:b]) >= 1 - 1e-10
+    assert residual_units(d, e, lam, Z) <= 10 and orth_units(Z) <= 10
+
+
+def test_eigvecs_mgs_cfg2_vs_lapack_and_cwy():
+    import scipy.linalg as sl
+
+    d, e, w = W.problem("cfg2", 1200)
+    Z, info = O.eigvecs(d, e, w, seed=1, mgs=True)
+    assert info == 0
+    assert residual_units_tridiag(d, e, w, Z) <= 10 and orth_units(Z) <= 10
+    _, V = sl.eigh_tridiagonal(d, e)
+    worst_vec, worst_sig, nv, ng = parity_report(w, O.tnorm(d, e), Z, V)
+    assert nv > 1100 and worst_vec <= 1e-10 and worst_sig >= 1 - 1e-10
+    Zc, _ = O.eigvecs(d, e, w, seed=1)
+    assert np.abs(Z - Zc).max() <= 1e-12       # same solves, same sign rule
+
+
+def test_eigvecs_mgs_glued_wilkinson_subspaces():
+    d, e = W.glued_wilkinson(5, 1e-4)
+    w = W.eigenvalues(d, e)
+    Z, info = O.eigvecs(d, e, w, seed=1, mgs=True)
+    assert info == 0
+    assert residual_units(d, e, w, Z) <= 10 and orth_units(Z) <= 10
+    _, V = np.linalg.eigh(dense(d, e))
+    cs = O.clusters(w, O.tnorm(d, e))
+    for a, b in zip(cs[:-1], cs[1:]):
+        assert sigma_min(Z[:, a:b], V[:, a:b]) >= 1 - 1e-10
+
+
+@pytest.mark.parametrize("cfg,n", [("cfg3", 630), ("type3", 420)])
+def test_eigvecs_mgs_invariants_and_range(cfg, n):
+    d, e, w = W.problem(cfg, n)
+    Z, info = O.eigvecs(d, e, w, seed=1, mgs=True)
+    assert info == 0
+    assert residual_units_tridiag(d, e, w, Z) <= 10 and orth_units(Z) <= 10
+    Zr, _ = O.eigvecs(d, e, w, seed=1, j_lo=40, j_hi=110, mgs=True)
+    assert np.array_equal(Zr, Z[:, 40:110])
