@@ -132,7 +132,7 @@ def reference_arm(args):
     return 0
 
 
-def cpu_baseline(d, e, w, budget_s=12.0):
+def cpu_baseline(d, e, w, budget_s=12.0, mgs=False):
     """The oracle timed on this host's cores on a bounded sample of the workload."""
     import oracle as O
 
@@ -142,7 +142,7 @@ def cpu_baseline(d, e, w, budget_s=12.0):
     if n <= 4200:
         reps = 0
         while True:
-            O.eigvecs(d, e, w, seed=1)
+            O.eigvecs(d, e, w, seed=1, mgs=mgs)
             reps += 1
             if time.perf_counter() - t0 > budget_s or reps >= 50:
                 break
@@ -150,7 +150,7 @@ def cpu_baseline(d, e, w, budget_s=12.0):
         return {"value": n * reps / dt, "unit": "eigenvectors/s", "cores": cores, "kind": "oracle",
                 "sample": f"{reps} full run(s) of all {n} eigenvectors, {dt:.1f} s"}
     k = 160 if n > 10000 else 256
-    O.eigvecs(d, e, w, seed=1, j_lo=0, j_hi=k)
+    O.eigvecs(d, e, w, seed=1, j_lo=0, j_hi=k, mgs=mgs)
     dt = time.perf_counter() - t0
     return {"value": k / dt, "unit": "eigenvectors/s", "cores": cores, "kind": "oracle",
             "sample": f"first {k} of {n} eigenvectors (start of the single cluster; later vectors cost more), {dt:.1f} s"}
@@ -165,6 +165,8 @@ def main():
     ap.add_argument("--impl", default="tinv", choices=["tinv", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reorth", default="cwy", choices=["cwy", "mgs"],
+                    help="cwy: compact WY (Alg. 4, the method); mgs: classical MGS (Alg. 1), the paper's comparison")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -201,6 +203,7 @@ def main():
     Zt = torch.empty((n, n), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     h = Tinv(local, stream=stream, nranks=ws, rank=rank, nccl_id=nccl_id)
+    h.set_reorth(args.reorth)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > 126 MB L2
 
     def barrier():
@@ -295,7 +298,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC[args.config], "name": args.config, "n": n,
-                   "parallelism": parallelism,
+                   "parallelism": parallelism, "reorth": args.reorth,
                    "l2": "flushed between timed steps (256 MB write)", "seed": args.seed},
         "roofline": roof,
         "e2e": e2e,
@@ -307,7 +310,7 @@ def main():
                  "cwy_ctas": st["cwy_ctas"], "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(d, e, w)
+        line["cpu_baseline"] = cpu_baseline(d, e, w, mgs=args.reorth == "mgs")
     if rank == 0:
         print(json.dumps(line))
     h.close()

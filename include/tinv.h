@@ -50,6 +50,8 @@ typedef struct {
 #define TINV_ERR_NCCL   -102
 #define TINV_ERR_HANDLE -103
 #define TINV_ERR_DEVICE -104
+#define TINV_ERR_UNSUPPORTED -105   /* a cluster exceeds the shared-memory staging limit, or
+                                       MGS mode with a cluster the resident kernel cannot hold */
 
 /* Create a handle bound to cfg->device and cfg->stream.  With nranks > 1 each rank
  * creates its handle with the same nccl_id (clusters are then sharded across ranks).
@@ -158,6 +160,16 @@ int tinv_set_virtual_ranks(tinv_t h, int nranks);
  * through the streaming persistent kernel instead (same results up to rounding; used to
  * compare the two paths).  Returns 0 or TINV_ERR_HANDLE. */
 int tinv_set_resident(tinv_t h, int enable);
+
+/* Reorthogonalisation of clustered vectors: mode 0 (default) = compact WY, Alg. 4
+ * (PAPER.md:681-716); mode 1 = the classical inverse iteration's modified Gram-Schmidt,
+ * Alg. 1, the paper's comparison method: after every
+ * solve, x <- x - <x, z_i> z_i for the cluster's accepted vectors in order, one cluster-wide
+ * reduction per z_i.  Same factorization, start vectors, stopping rule and restarts; the
+ * vectors agree with mode 0 up to rounding.  Mode 1 runs in the resident kernel only:
+ * tinv_eigvecs returns TINV_ERR_UNSUPPORTED when a cluster does not fit it (m > 64 or
+ * n > 4096).  Returns 0, -2 for another mode, TINV_ERR_HANDLE. */
+int tinv_set_reorth(tinv_t h, int mode);
 int tinv_get_stats(tinv_t h, tinv_stats_t* out);
 
 /* Number of exported entry points (for the loader test). */

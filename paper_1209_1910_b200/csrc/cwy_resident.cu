@@ -558,8 +558,12 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         }
 
         PH(14);
-        // ================= first reflector from z_{j1}
-        {
+        // ================= first reflector from z_{j1}; MGS keeps z itself
+        if (a.mgs) {
+            const double* z = a.Z + j1 * a.ldz;
+            for (int i = tid; i < nl; i += NT) sm.Y[ys.at(i, 0)] = lead ? sm.ql[i] * lscl : __ldcg(z + r0 + i);
+            __syncthreads();
+        } else {
             const double* z = a.Z + j1 * a.ldz;
             double v[1] = {0.0}, dm = 0.0;
             long long di = 0;
@@ -602,6 +606,148 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
             bool first = true;
             if (crank == 0 && tid == 0)   // this vector's factor records for the chained solve
                 for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
+            if (a.mgs) {
+                // ===== Alg. 1 (classical inverse iteration):
+                // after every solve, modified Gram-Schmidt against the cluster's accepted
+                // vectors z_{j1} .. z_{j-1} (columns 0..p-1 of Y), one cluster-wide reduction
+                // per vector in order (l.10-12); then the same test, restarts and chained solve
+                // as the compact-WY path.  The projected x is the iterate r of reading 9.
+                {
+                    const double* x1 = a.X1c + j * n2v;
+#pragma unroll 4
+                    for (int i = tid; i < nl; i += NT) sm.xl[i] = __ldcg(x1 + r0 + i);
+                }
+                __syncthreads();
+                while (true) {
+                    double x2 = 0.0;
+                    for (int k = 0; k < p; k++) {
+                        double v[2] = {0.0, 0.0}, dm = 0.0;
+                        long long di = 0;
+                        for (int i = tid; i < nl; i += NT) {
+                            v[0] = fma(sm.Y[ys.at(i, k)], sm.xl[i], v[0]);
+                            if (k == 0) v[1] = fma(sm.xl[i], sm.xl[i], v[1]);
+                        }
+                        block_reduce<2, false>(v, dm, di, sm.red, rpar);
+                        if (tid < CS) pub1(pxb, 0, v[0], tid);
+                        if (k == 0 && tid >= NT - CS) pub1(pxb, M2 + X2, v[1], tid - (NT - CS));
+                        csync();
+                        double dot = 0.0;
+                        for (int c = 0; c < CS; c++) dot += PXo(c, pxb)[0];
+                        if (k == 0) x2 = csum(pxb, X2);
+                        pxb ^= 1;
+                        for (int i = tid; i < nl; i += NT) sm.xl[i] = fma(-dot, sm.Y[ys.at(i, k)], sm.xl[i]);
+                    }
+                    // norms, argmax and sign of the projected x, forward maps of its solve
+                    double v[2] = {0.0, 0.0}, qinf = -1.0;
+                    long long qarg = 0;
+                    for (int i = tid; i < nl; i += NT) {
+                        const double qi = sm.xl[i];
+                        v[0] = fma(qi, qi, v[0]);
+                        const double aq = fabs(qi);
+                        v[1] += aq;
+                        if (aq > qinf) { qinf = aq; qarg = r0 + i; }
+                    }
+                    block_reduce<2, true>(v, qinf, qarg, sm.red, rpar);
+                    const Aff f = fwd_maps(Fj, FPj, fta, ftb, [&](int64_t i) { return sm.xl[i - r0]; });
+                    Aff tot;
+                    const Aff fex = scan_excl(f, reinterpret_cast<Aff*>(sm.acc), tot);
+                    {
+                        const double sg = (qinf >= 0.0 && sm.xl[qarg - r0] < 0.0) ? -1.0 : 1.0;
+                        const double q0v = sm.xl[0];
+                        pubs(pxb, crank == 0 ? 8 : 7, [&](int k, int& slot) {
+                            switch (k) {
+                                case 0: slot = Q2; return v[0];
+                                case 1: slot = Q1; return v[1];
+                                case 2: slot = QINF; return qinf;
+                                case 3: slot = QARG; return (double)qarg;
+                                case 4: slot = QSGN; return sg;
+                                case 5: slot = FA; return tot.a;
+                                case 6: slot = FB; return tot.b;
+                                default: slot = Q0; return q0v;
+                            }
+                        });
+                    }
+                    csync();
+                    const double q2 = csum(pxb, Q2);
+                    double qi = -1.0;
+                    long long qa = 0;
+                    int own = 0;
+                    for (int c2 = 0; c2 < CS; c2++) {
+                        const double vv = PXo(c2, pxb)[M2 + QINF];
+                        const long long ia = (long long)PXo(c2, pxb)[M2 + QARG];
+                        if (vv > qi || (vv == qi && ia < qa)) { qi = vv; qa = ia; own = c2; }
+                    }
+                    const bool degen = p > 0 && sqrt(q2) <= (double)n * kEps * sqrt(x2);   // reading 16
+                    if (degen && restart < kMaxRestart) {
+                        restart++;
+                        its++;
+                        kin = 1;
+                        passes = 0;
+                        const int b = pxb ^ 1;
+                        auto rhs = [&](int64_t i) { return start_entry(a.seed, n, j, restart, i); };
+                        double w1[1] = {0.0}, dm = 0.0;
+                        long long di = 0;
+                        for (int i = tid; i < nl; i += NT) w1[0] += fabs(rhs(r0 + i));
+                        const Aff fr = fwd_maps(Fj, FPj, fta, ftb, rhs);
+                        Aff totr;
+                        const Aff exr = scan_excl(fr, reinterpret_cast<Aff*>(sm.acc), totr);
+                        block_reduce<1, false>(w1, dm, di, sm.red, rpar);
+                        pubs(b, 3, [&](int k, int& slot) {
+                            if (k == 0) { slot = FA; return totr.a; }
+                            if (k == 1) { slot = FB; return totr.b; }
+                            slot = Q1;
+                            return w1[0];
+                        });
+                        csync();
+                        const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(b, Q1);
+                        fwd_pass2(Fj, FPj, fta, ftb, exr, rhs(0), sc, b, rhs);
+                        pxb ^= 1;
+                        csync();
+                        sweep(Fj);
+                        if (crank == 0) {
+                            __syncthreads();
+                            push_x(sm.xl);
+                        }
+                        csync();
+                        continue;
+                    }
+                    if (degen) flagged = true;
+                    if (qi >= thr) passes++;
+                    bool fin = false;
+                    if (passes >= kPasses) fin = true;
+                    else if (kin >= kMaxIts) { fin = true; flagged = true; }
+                    if (fin) {   // Alg. 1 l.14: normalise (sign rule of reading 15); z_j joins Y
+                        const double scl = PXo(own, pxb)[M2 + QSGN] / sqrt(q2);
+                        double* zj = a.Z + j * a.ldz;
+                        for (int i = tid; i < nl; i += NT) {
+                            const double zi = sm.xl[i] * scl;
+                            zj[r0 + i] = zi;
+                            sm.Y[ys.at(i, p)] = zi;
+                        }
+                        if (crank == 0 && tid == 0) {
+                            a.iters[j] = its;
+                            if (flagged) atomicAdd(&a.out->nflag, 1);
+                        }
+                        pxb ^= 1;
+                        __syncthreads();
+                        break;
+                    }
+                    its++;
+                    kin++;
+                    const double sc = (double)n * a.tnorm * fmax(kEps, __ldg(a.unn + j)) / csum(pxb, Q1);
+                    fwd_pass2(Fj, FPj, fta, ftb, fex, PXo(0, pxb)[M2 + Q0], sc, pxb,
+                              [&](int64_t i) { return sm.xl[i - r0]; });
+                    pxb ^= 1;
+                    csync();
+                    sweep(Fj);
+                    if (crank == 0) {
+                        __syncthreads();
+                        push_x(sm.xl);
+                    }
+                    csync();
+                }
+                continue;
+            }
             // x^(1)_j into xl (the look-ahead already loaded it into x1l)
             if (use_la) {
                 for (int i = tid; i < nl; i += NT) sm.xl[i] = sm.x1l[i];

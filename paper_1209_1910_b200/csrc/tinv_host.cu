@@ -89,6 +89,7 @@ struct tinv_s {
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
+    int mgs = 0;                      // 1: classical MGS reorthogonalisation (Alg. 1)
     int res_cs2 = 1000, res_cs4 = 1000;   // m from which a cluster gets >= 2 / 4 CTAs
     int handover = 1;                 // narrow leaders finish in the resident kernel (n <= 2048)
     double leader_w = 1.0;            // LPT weight of a handed-over leader (vector equivalents)
@@ -352,6 +353,7 @@ const char* tinv_strerror(int code) {
         case TINV_ERR_NCCL: return "NCCL failure";
         case TINV_ERR_HANDLE: return "invalid handle";
         case TINV_ERR_DEVICE: return "device is not an sm_100 (B200) GPU";
+        case TINV_ERR_UNSUPPORTED: return "unsupported configuration (a cluster exceeds the shared-memory staging limit, or MGS mode with a cluster outside the resident kernel)";
         case -2: return "invalid argument 2 (n < 1)";
         case -3: return "invalid argument 3 (d NULL or non-finite)";
         case -4: return "invalid argument 4 (e NULL or non-finite)";
@@ -442,6 +444,13 @@ int tinv_set_virtual_ranks(tinv_t h, int nranks) {
 int tinv_set_resident(tinv_t h, int enable) {
     if (!h) return TINV_ERR_HANDLE;
     h->resident = enable != 0;
+    return 0;
+}
+
+int tinv_set_reorth(tinv_t h, int mode) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (mode != 0 && mode != 1) return -2;
+    h->mgs = mode;
     return 0;
 }
 
@@ -578,7 +587,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     if (po.n_clustered > 0 && smem > 232448) {
         fprintf(stderr, "[tinv] cluster of %d vectors exceeds the shared-memory staging limit\n", po.max_cluster);
         join_b2();
-        return TINV_ERR_DEVICE;
+        return TINV_ERR_UNSUPPORTED;
     }
     const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
     // Row split: when the clustered work is one wide cluster (cfg4/cfg5), all
@@ -625,17 +634,25 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             }
         }
         for (auto& rg : rgroups) rg.smem = resident_smem_bytes(n, rg.RL, rg.M2, rg.cs);
+
         if (handover)   // the batched LU stopped every narrow leader: all of them must be resident
             for (int c = rlo[h->rank]; c < rhi[h->rank]; c++) {
                 const int m = cs[c + 1] - cs[c];
                 if (m >= 2 && m <= handover && !resident[c]) {
                     fprintf(stderr, "[tinv] narrow cluster of %d vectors does not fit the resident kernel\n", m);
                     join_b2();
-                    return TINV_ERR_DEVICE;
+                    return TINV_ERR_UNSUPPORTED;
                 }
             }
         // the largest clusters first (longest dependent chains)
         std::sort(rgroups.begin(), rgroups.end(), [](const ResGroup& a, const ResGroup& b) { return a.cs > b.cs; });
+    }
+    if (h->mgs) {   // MGS (Alg. 1) runs in the resident kernel only
+        for (int c = 0; c < nclus; c++)
+            if (cs[c + 1] - cs[c] >= 2 && (rs_real || !resident[c]) && (rs_real || (c >= rlo[h->rank] && c < rhi[h->rank]))) {
+                join_b2();
+                return TINV_ERR_UNSUPPORTED;
+            }
     }
     Schedule sc = rs_real ? make_schedule(cs, 0, nclus, n, nctas_max)
                           : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max, &resident);
@@ -740,7 +757,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             ra.u_off = h->res_buf + offs[q];
             ra.u_list = h->res_buf + offs[q] + units[q] + 1;
             ra.X1c = h->X1c; ra.F = h->F; ra.FP = h->FP; ra.unn = h->unn; ra.Z = Z; ra.ldz = ldz;
-            ra.iters = h->iters; ra.out = h->out; ra.handover = handover;
+            ra.iters = h->iters; ra.out = h->out; ra.handover = handover; ra.mgs = h->mgs;
             if (const char* v = getenv("TINV_RES_FLAGS")) ra.flags = atoi(v);
             // phase timers of unit 0 of one group (the first; TINV_PROF_GROUP picks another)
             const int pg = getenv("TINV_PROF_GROUP") ? atoi(getenv("TINV_PROF_GROUP")) : 0;

@@ -389,3 +389,55 @@ def test_resident_deterministic(handle, torch):
     Z1, _ = run_gpu(handle, torch, d, e, w)
     Z2, _ = run_gpu(handle, torch, d, e, w)
     assert torch.equal(Z1, Z2)
+
+
+# ------------------------------------------------------------------ Alg. 1 (classical MGS)
+# tinv_set_reorth(h, 1) -- modified Gram-Schmidt against the cluster's
+# accepted vectors in the resident kernel, compared with the MGS oracle.
+
+def _mgs_parity(handle, torch, d, e, w):
+    handle.set_reorth("mgs")
+    try:
+        Zg, rc = run_gpu(handle, torch, d, e, w)
+    finally:
+        handle.set_reorth("cwy")
+    assert rc == 0, f"tinv_eigvecs (MGS) returned {rc}"
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
+    Zo, info = O.eigvecs(d, e, w, seed=1, mgs=True)
+    assert info == 0
+    Zg_h = Zg.cpu().numpy()
+    wv, ws, nv, ng = parity_report(w, O.tnorm(d, e), Zg_h, Zo)
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+    return Zg_h
+
+
+@pytest.mark.parametrize("cfg,n", [("cfg2", 1200), ("cfg1", None), ("type3", 420)])
+def test_mgs_path_parity(handle, torch, cfg, n):
+    d, e, w = W.problem(cfg, n)
+    _mgs_parity(handle, torch, d, e, w)
+
+
+@pytest.mark.parametrize("n,sizes", [(2000, [60, 33, 17, 9, 2]), (1501, [40, 12, 7])])
+def test_mgs_cluster_sizes(handle, torch, n, sizes):
+    """1- to 8-CTA thread-block clusters, m up to 60: MGS vs its oracle, and vs the cWY path."""
+    d, e, w = _clustered(n, sizes)
+    Zm = _mgs_parity(handle, torch, d, e, w)
+    Zc, rc = run_gpu(handle, torch, d, e, w)
+    assert rc == 0
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zm, Zc.cpu().numpy())
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+
+
+def test_mgs_unsupported_for_wide_clusters(handle, torch):
+    from paper_1209_1910_b200.tinv import TinvError
+
+    d, e, w = W.problem("cfg4", 600)      # one cluster of 600 vectors: not resident
+    handle.set_reorth("mgs")
+    try:
+        with pytest.raises(TinvError, match="-105"):
+            run_gpu(handle, torch, d, e, w)
+    finally:
+        handle.set_reorth("cwy")
+    Z, rc = run_gpu(handle, torch, d, e, w)   # the handle still works in cWY mode
+    assert rc == 0
