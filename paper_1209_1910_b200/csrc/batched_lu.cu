@@ -66,7 +66,8 @@ __device__ __forceinline__ double rcp_pivot(double x) {
     return fma(r, e, r);
 }
 
-template <int NS>
+// SDE: d and e staged in shared memory (compile-time, so their loads are LDS, not generic)
+template <int NS, bool SDE>
 __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
     extern __shared__ __align__(128) unsigned char bl_smem[];
     static_assert(sizeof(Stage) * NS >= sizeof(double) * (RR * kRG + 1) * 32, "start-vector ring exceeds the stages");
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
     double* __restrict__ FB = a.fb + boff;
     double* __restrict__ FC = a.fc + boff;
     int8_t* __restrict__ FPv = a.fp + boff;
-    const bool stage_de = a.stage_de != 0;
+    constexpr bool stage_de = SDE;
     // d staged at sde[0, n2), e at sde[n2, n2 + n) with e[n-1] = 0 (the factor sweep's
     // enext past the last row); the bulk copies move whole 16-byte pairs inside the arrays
     const int64_t n2 = (n + 1) & ~int64_t(1);
@@ -183,12 +184,20 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
           mbar_wait(rfull + slot, (uint32_t)((k / kRG) & 1));
           const double* rb = ring + (size_t)slot * RR * 32;
           const int cnt = (int)(nrow - i0 < RR ? nrow - i0 : RR);
-#pragma unroll 4
-          for (int rr = 0; rr < cnt; rr++) {
+          // this chunk's rows through chunk-base pointers (immediate offsets in the unrolled body)
+          const double* pe = ee + i0;
+          const double* pd = dd + i0 + 1;
+          double* pFL = FL + i0 * 32 + lane;
+          double* pFR = FR + i0 * 32 + lane;
+          double* pFB = FB + i0 * 32 + lane;
+          double* pFC = FC + i0 * 32 + lane;
+          double* pX = X + i0 * 32 + lane;
+          int8_t* pFP = FPv + i0 * 32 + lane;
+          auto row = [&](int rr) {
             const int64_t i = i0 + rr;
-            const double sub = ee[i];
-            const double anext = dd[i + 1] - shift;
-            const double enext = stage_de ? ee[i + 1] : ((i + 1 < n - 1) ? ee[i + 1] : 0.0);
+            const double sub = pe[rr];
+            const double anext = pd[rr] - shift;
+            const double enext = stage_de ? pe[rr + 1] : ((i + 1 < n - 1) ? pe[rr + 1] : 0.0);
             const double bn = rb[rr * 32 + lane];
             double u0, u1, u2, l, y;
             int8_t sw;
@@ -214,13 +223,19 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
                 c = bn - l * c;
                 sw = 0;
             }
-            const int64_t o = i * 32 + lane;   // dead lanes store too: their slots are unused
-            __stcg(FL + o, l);
-            FPv[o] = sw;
-            __stcg(FR + o, r);
-            __stcg(FB + o, u1 * r);
-            __stcg(FC + o, u2 * r);
-            __stcg(X + o, y);
+            const int o = rr * 32;   // dead lanes store too: their slots are unused
+            __stcg(pFL + o, l);
+            pFP[o] = sw;
+            __stcg(pFR + o, r);
+            __stcg(pFB + o, u1 * r);
+            __stcg(pFC + o, u2 * r);
+            __stcg(pX + o, y);
+          };
+          if (cnt == RR) {
+#pragma unroll 8
+            for (int rr = 0; rr < RR; rr++) row(rr);
+          } else {
+            for (int rr = 0; rr < cnt; rr++) row(rr);
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(rempty + slot);
@@ -470,14 +485,19 @@ void launch_batched(const BatchedArgs& a, cudaStream_t s, int nsm) {
         const size_t de = (size_t)(((a.n + 1) & ~int64_t(1)) + a.n) * 8;
         size_t sm = smem_fixed<NS_DEEP>();
         b.stage_de = (sm + de <= 200 * 1024) ? 1 : 0;
-        if (b.stage_de) sm += de;
-        cudaFuncSetAttribute(batched_lu_kernel<NS_DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        batched_lu_kernel<NS_DEEP><<<(unsigned)nb, 64, sm, s>>>(b);
+        if (b.stage_de) {
+            sm += de;
+            cudaFuncSetAttribute(batched_lu_kernel<NS_DEEP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            batched_lu_kernel<NS_DEEP, true><<<(unsigned)nb, 64, sm, s>>>(b);
+        } else {
+            cudaFuncSetAttribute(batched_lu_kernel<NS_DEEP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            batched_lu_kernel<NS_DEEP, false><<<(unsigned)nb, 64, sm, s>>>(b);
+        }
     } else {
         b.stage_de = 0;
         const size_t sm = smem_fixed<NS_SHALLOW>();
-        cudaFuncSetAttribute(batched_lu_kernel<NS_SHALLOW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        batched_lu_kernel<NS_SHALLOW><<<(unsigned)nb, 64, sm, s>>>(b);
+        cudaFuncSetAttribute(batched_lu_kernel<NS_SHALLOW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        batched_lu_kernel<NS_SHALLOW, false><<<(unsigned)nb, 64, sm, s>>>(b);
     }
 }
 
