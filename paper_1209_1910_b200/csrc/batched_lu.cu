@@ -291,12 +291,27 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
                 xp2 = xp1;
                 xp1 = xi;
             }
+            if (keep) {
+                double* Xb = X + ib * 32 + lane;   // this stage's rows (the first may be partial)
+                if (ib >= 0) {
+#pragma unroll
+                    for (int rr = 0; rr < RB; rr++) __stcg(Xb + rr * 32, xv[rr]);
+                } else {
+#pragma unroll
+                    for (int rr = 0; rr < RB; rr++)
+                        if (ib + rr >= 0) __stcg(Xb + rr * 32, xv[rr]);
+                }
+            }
+            if (!iter_warp) {   // first-solve warps need no statistics (their iterate goes on)
+                __syncwarp();
+                if (lane == 0 && b + NS < nblk) issue(b + NS);
+                continue;
+            }
             double sa[RB], sq[RB];
             int ia[RB];
 #pragma unroll
             for (int rr = 0; rr < RB; rr++) {
                 const bool valid = ib + rr >= 0;
-                if (keep && valid) __stcg(X + (ib + rr) * 32 + lane, xv[rr]);
                 sa[rr] = valid ? fabs(xv[rr]) : 0.0;
                 sq[rr] = valid ? xv[rr] * xv[rr] : 0.0;
                 ia[rr] = rr;
