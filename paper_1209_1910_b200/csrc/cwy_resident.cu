@@ -260,12 +260,16 @@ __device__ __forceinline__ double colacc(const L& sm, const YSw& ys, int r0, int
 // U of the chained solve), in place over t.  The recurrence stays sequential: expanding it
 // over blocks of rows multiplies the b, c of neighbouring rows, which for nearly decoupled
 // blocks (pivots ~ eps ||T||, |b| ~ 1e11 in glued Wilkinson matrices) cancels catastrophically.
-// All threads of CTA 0 first stage (b, c) of every row into shared memory (back_stage); then
+// All threads of CTA 0 stage (b, c) of every row into shared memory (back_stage_async); then
 // one thread runs the chain from shared memory in 16-row batches (back_sweep_smem).
-__device__ void back_stage(const double* __restrict__ F, double* bc, int64_t n) {
-#pragma unroll 8
+// Staged asynchronously (cp.async, 16 bytes per row) when the vector starts, so the copy is
+// off the critical path by the time of its first solve; the sweep waits for the group.
+__device__ void back_stage_async(const double* __restrict__ F, double* bc, int64_t n) {
+#pragma unroll 4
     for (int64_t i = threadIdx.x; i < n; i += NT)
-        reinterpret_cast<double2*>(bc)[i] = __ldg(reinterpret_cast<const double2*>(F + i * 4 + 2));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(bc + 2 * i)), "l"(F + i * 4 + 2)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 __device__ void back_sweep_smem(const double* __restrict__ bc, double* tf, int64_t n64) {
     const double2* BC = reinterpret_cast<const double2*>(bc);
@@ -460,8 +464,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
     const int fta = s0 + min(max(s1 - s0, 0), tid * FLn), ftb = s0 + min(max(s1 - s0, 0), (tid + 1) * FLn);
     // the back sweep in CTA 0 (all its threads stage, thread 0 sweeps)
     auto sweep = [&](const double* Fj) {
+        (void)Fj;
         if (crank == 0) {
-            back_stage(Fj, sm.bc, n);
+            asm volatile("cp.async.wait_group 0;" ::: "memory");   // this vector's (b, c) rows
             __syncthreads();
             PH(9);
             if (tid == 0) back_sweep_smem(sm.bc, sm.tf, n);
@@ -484,6 +489,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
             const int8_t* FPj = a.FP + j * n;
             if (crank == 0 && tid == 0)
                 for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
+            if (crank == 0) back_stage_async(Fj, sm.bc, n);
             {
                 const double* x1 = a.X1c + j * n2v;
                 #pragma unroll 4
@@ -606,6 +612,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
             bool first = true;
             if (crank == 0 && tid == 0)   // this vector's factor records for the chained solve
                 for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
+            if (crank == 0) back_stage_async(Fj, sm.bc, n);   // (b, c) for its back sweeps
             if (a.mgs) {
                 // ===== Alg. 1 (classical inverse iteration):
                 // after every solve, modified Gram-Schmidt against the cluster's accepted
