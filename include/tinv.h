@@ -89,8 +89,11 @@ int tinv_eigvals(tinv_t h, int64_t n, const double* d, const double* e, double* 
 int tinv_eig(tinv_t h, int64_t n, const double* d, const double* e, double* w, double* Z, int64_t ldz,
              uint64_t seed);
 
-/* Same operation with HOST buffers (pinned host memory recommended): the library copies
- * d, e, w to the device, runs tinv_eigvecs and copies Z back (end-to-end path). */
+/* Same operation with HOST buffers (end-to-end path): the library copies d, e, w to the
+ * device and runs tinv_eigvecs.  When Z is page-locked host memory mapped into the device
+ * address space (cudaHostAlloc / cudaMallocHost under UVA) and nranks == 1, the kernels write
+ * the finished columns straight into Z over PCIe, overlapped with the remaining compute;
+ * otherwise Z is computed in a device buffer and copied back after the last kernel. */
 int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
                       double* Z, int64_t ldz, uint64_t seed);
 

@@ -1056,6 +1056,24 @@ int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, con
     CK(cudaMemcpyAsync(dd, d, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     if (n > 1) CK(cudaMemcpyAsync(de, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dw, w, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    // Z in page-locked host memory mapped into the device's address space (cudaHostAlloc /
+    // cudaMallocHost / torch pin_memory under UVA): the kernels write every finished column
+    // straight into it over PCIe while later clusters are still computing, instead of one
+    // 8 n^2-byte copy after the last kernel.  Single-rank only (the multi-rank column exchange
+    // runs on device buffers).
+    double* zmap = nullptr;
+    if (h->nranks == 1) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, Z) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+            zmap = static_cast<double*>(pa.devicePointer);
+        cudaGetLastError();   // unregistered pageable memory: not an error here
+    }
+    if (zmap) {
+        int rc = tinv_eigvecs(h, n, dd, n > 1 ? de : nullptr, dw, zmap, ldz, seed);
+        if (rc < 0) return rc;
+        CK(cudaStreamSynchronize(st));
+        return rc;
+    }
     int rc = tinv_eigvecs(h, n, dd, n > 1 ? de : nullptr, dw, dZ, ldz, seed);
     if (rc < 0) return rc;
     CK(cudaMemcpyAsync(Z, dZ, sizeof(double) * (size_t)ldz * n, cudaMemcpyDeviceToHost, st));

@@ -241,6 +241,19 @@ def test_host_path_equals_device_path(handle, torch):
     assert np.array_equal(Zh.T, Zd.cpu().numpy())
 
 
+def test_host_path_pinned_mapped_z(handle, torch):
+    """Pinned (mapped) Z: the kernels write the columns straight into host memory; the result
+    equals the device path bit for bit, on a resident-kernel config and a persistent one."""
+    for cfg, n in (("cfg2", 800), ("cfg3", 630)):
+        d, e, w = W.problem(cfg, n)
+        Zd, _ = run_gpu(handle, torch, d, e, w)
+        hd, he, hw = (torch.tensor(a, dtype=torch.float64).pin_memory() for a in (d, e, w))
+        hZ = torch.full((n, n), float("nan"), dtype=torch.float64).pin_memory()
+        Zh, rc = handle.eigvecs_host(hd, he, hw, Z=hZ, seed=1)
+        assert rc == 0
+        assert torch.equal(hZ, Zd.cpu().t())   # hZ row j = column j (column-major Z)
+
+
 def test_stats_report_native_launches(handle, torch):
     d, e, w = W.problem("cfg2", 400)
     run_gpu(handle, torch, d, e, w)
