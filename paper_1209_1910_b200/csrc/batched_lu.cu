@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
                 xp2 = xp1;
                 xp1 = xi;
             }
-            if (keep) {
+            if (keep && iter_warp) {
                 double* Xb = X + ib * 32 + lane;   // this stage's rows (the first may be partial)
                 if (ib >= 0) {
 #pragma unroll
@@ -300,6 +300,17 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
 #pragma unroll
                     for (int rr = 0; rr < RB; rr++)
                         if (ib + rr >= 0) __stcg(Xb + rr * 32, xv[rr]);
+                }
+            } else if (keep && live) {   // first-solve vector: x^(1) straight into its X1c row
+                double* xr = a.X1c + j * ((n + 1) & ~int64_t(1)) + ib;
+                if (ib >= 0 && !(ib & 1)) {
+#pragma unroll
+                    for (int rr = 0; rr < RB; rr += 2)
+                        __stcg(reinterpret_cast<double2*>(xr + rr), make_double2(xv[rr], xv[rr + 1]));
+                } else {
+#pragma unroll
+                    for (int rr = 0; rr < RB; rr++)
+                        if (ib + rr >= 0) __stcg(xr + rr, xv[rr]);
                 }
             }
             if (!iter_warp) {   // first-solve warps need no statistics (their iterate goes on)
@@ -424,11 +435,11 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
 
 // Per-vector contiguous copy of the factors of the first-solve vectors (slots >= nc_pad: j_c >= 1
 // and handed-over leaders) for the chained solves of the compact-WY kernels:
-// F[j][i] = (l_i, 1/u0_i, u1_i/u0_i, u2_i/u0_i), the pivot byte, and the first iterate x^(1)
-// (contiguous per vector, so the compact-WY passes can bulk-copy it), via 32x32 shared-memory
-// tiles (coalesced on both sides).
+// F[j][i] = (l_i, 1/u0_i, u1_i/u0_i, u2_i/u0_i) and the pivot byte, via 32x32 shared-memory
+// tiles (coalesced on both sides).  (Their first iterates x^(1) are written per vector by the
+// batched kernel's back sweep directly.)
 __global__ void pack_factors_kernel(PackArgs a) {
-    __shared__ double tile[5][32][33];
+    __shared__ double tile[4][32][33];
     __shared__ int8_t ptile[32][33];
     __shared__ int vec[32];
     const int64_t s0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
@@ -437,11 +448,11 @@ __global__ void pack_factors_kernel(PackArgs a) {
     if (ty == 0) vec[tx] = a.perm[s0 + tx];
     __syncthreads();
     if (vec[0] < 0 && !__syncthreads_or(vec[tx] >= 0)) return;
-    const double* src[5] = {a.fl, a.fr, a.fb, a.fc, a.X};
+    const double* src[4] = {a.fl, a.fr, a.fb, a.fc};
     for (int r = ty; r < 32; r += 8) {
         const int64_t i = i0 + r;
         const bool ok = i < a.n;
-        for (int c = 0; c < 5; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + bix(i, s0 + tx, a.n)) : 0.0;
+        for (int c = 0; c < 4; c++) tile[c][r][tx] = ok ? __ldcg(src[c] + bix(i, s0 + tx, a.n)) : 0.0;
         ptile[r][tx] = ok ? a.fp[bix(i, s0 + tx, a.n)] : (int8_t)0;
     }
     __syncthreads();
@@ -455,7 +466,6 @@ __global__ void pack_factors_kernel(PackArgs a) {
             __stcg(reinterpret_cast<double2*>(dst), make_double2(tile[0][tx][r], tile[1][tx][r]));
             __stcg(reinterpret_cast<double2*>(dst + 2), make_double2(tile[2][tx][r], tile[3][tx][r]));
             a.FP[j * a.n + i] = ptile[tx][r];
-            __stcg(a.X1c + j * ((a.n + 1) & ~int64_t(1)) + i, tile[4][tx][r]);
         }
     }
 }

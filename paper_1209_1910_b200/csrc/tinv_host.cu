@@ -516,10 +516,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     CK(cudaMemcpyAsync(h->h_cstart, h->cstart, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, h->side));
     ev_record(h, 2);
     BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, h->perm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
-                   h->X, h->unn, h->zscale, h->iters, h->out,
+                   h->X, h->X1c, h->unn, h->zscale, h->iters, h->out,
                    h->profiling ? reinterpret_cast<unsigned long long*>(h->bnd + 24) : nullptr, 0, 0};
     FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->perm, Z, ldz, h->out};
-    PackArgs pk{n, h->ldv, h->perm, h->out, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP, h->X, h->X1c};
+    PackArgs pk{n, h->ldv, h->perm, h->out, h->fl, h->fr, h->fb, h->fc, h->fp, h->F, h->FP};
     if (handover) {
         CK(cudaStreamWaitEvent(h->bst, h->ev_prep, 0));
         ba.mode = 2;

@@ -56,7 +56,8 @@ struct BatchedArgs {
     double* fr;         // 1/u0_i
     double* fb;         // u1_i/u0_i
     double* fc;         // u2_i/u0_i
-    double* X;          // iterate / solution, [i][j]
+    double* X;          // iterate / solution, [i][j] (iterating warps)
+    double* X1c;        // x^(1) of first-solve vectors, [j][i], vector stride roundup(n, 2)
     double* unn;        // |u_{n-1,n-1}| per vector
     double* zscale;     // sign/||x||_2 of finished (j_c == 0) vectors
     int* iters;         // iteration count per vector
@@ -79,8 +80,6 @@ struct PackArgs {
     const int8_t* fp;
     double* F;          // [j][i][4]: l, 1/u0, u1/u0, u2/u0
     int8_t* FP;         // [j][i] pivot bits
-    const double* X;    // x^(1), [i][j]
-    double* X1c;        // x^(1) of clustered vectors, [j][i], vector stride roundup(n, 2)
 };
 
 struct FinalizeArgs {
