@@ -700,37 +700,74 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             for (size_t q = 1; q < rgroups.size(); q++)
                 want_units[q] = std::max(1, (int)((double)std::max(budget, 0) * wg[q] / std::max(wrest, 1.0)));
         }
+        // Units of every group (co-resident SM shares as above), then one LPT over all
+        // clusters: a cluster may run in any unit whose CTAs hold its rows (CS at least its own
+        // group's) and whose Y row fits its columns, so the larger-CS units that finish their
+        // long chains early absorb smaller clusters.  Load = weight x per-vector cost of the
+        // unit's CS (relative; TINV_CS_COST="cs:f,..." overrides).
+        double csf[9] = {1.0, 1.5, 1.25, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0};   // tuned on cfg2
+        if (const char* v = getenv("TINV_CS_COST")) {
+            int k; double f; const char* q = v;
+            while (sscanf(q, "%d:%lf", &k, &f) == 2) {
+                if (k >= 1 && k <= 8) csf[k] = f;
+                const char* comma = strchr(q, ',');
+                if (!comma) break;
+                q = comma + 1;
+            }
+        }
+        struct Unit { int q; double load; std::vector<int> cl; };
+        std::vector<Unit> all;
+        std::vector<int> nus(rgroups.size());
         for (size_t q = 0; q < rgroups.size(); q++) {
             ResGroup& rg = rgroups[q];
             const int maxc = std::max(1, resident_max_clusters(rg.cs, rg.smem));
-            const int share = want_units[q];
-            const int nu = std::max(1, std::min<int>({(int)rg.cl.size(), maxc, share}));
-            std::vector<int> order = rg.cl;
-            std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-                return (cs[x + 1] - cs[x]) > (cs[y + 1] - cs[y]);
-            });
-            std::vector<std::vector<int>> lists(nu);
-            std::vector<double> load(nu, 0.0);
-            for (int c : order) {
-                const double m = cs[c + 1] - cs[c];
-                const int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-                lists[b].push_back(c);
-                // per-vector cost is dominated by the m-independent chained solve: weight by
-                // the number of vectors (m - 1), with a small m term for the passes
-                load[b] += (m - 1) * (1.0 + h->lpt_m * m / 32.0) + (handover ? h->leader_w : 0.0);
+            nus[q] = std::max(1, std::min<int>({(int)rg.cl.size(), maxc, want_units[q]}));
+            for (int u = 0; u < nus[q]; u++) all.push_back(Unit{(int)q, 0.0, {}});
+        }
+        std::vector<std::pair<int, int>> order;   // (cluster, its own group)
+        for (size_t q = 0; q < rgroups.size(); q++)
+            for (int c : rgroups[q].cl) order.push_back({c, (int)q});
+        auto weight = [&](int c) {
+            const double m = cs[c + 1] - cs[c];
+            // per-vector cost is dominated by the m-independent chained solve: weight by the
+            // number of vectors (m - 1), with a small m term for the passes
+            return (m - 1) * (1.0 + h->lpt_m * m / 32.0) + (handover ? h->leader_w : 0.0);
+        };
+        std::stable_sort(order.begin(), order.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+            return weight(x.first) > weight(y.first);
+        });
+        for (auto& [c, q0] : order) {
+            const int m2 = (cs[c + 1] - cs[c] + 1) & ~1;
+            int best = -1;
+            double bl = 0.0;
+            for (size_t u = 0; u < all.size(); u++) {
+                const ResGroup& rg = rgroups[all[u].q];
+                if (rg.cs < rgroups[q0].cs || rg.M2 < m2) continue;
+                const double l = all[u].load + weight(c) * csf[rg.cs];
+                if (best < 0 || l < bl) { best = (int)u; bl = l; }
             }
+            all[best].load = bl;
+            all[best].cl.push_back(c);
+        }
+        for (size_t q = 0; q < rgroups.size(); q++) {
+            ResGroup& rg = rgroups[q];
+            std::vector<const Unit*> mine;
+            for (const Unit& un : all)
+                if (un.q == (int)q && !un.cl.empty()) mine.push_back(&un);
+            const int nu = (int)mine.size();
             units[q] = nu;
             if (getenv("TINV_DEBUG")) {
                 double mx = 0.0;
-                for (double v : load) mx = std::max(mx, v);
-                fprintf(stderr, "[tinv] resident group cs=%d clusters=%zu units=%d (maxc %d share %d) M2=%d smem=%zu max-load %.0f\n",
-                        rg.cs, rg.cl.size(), nu, maxc, share, rg.M2, rg.smem, mx);
+                size_t ncl = 0;
+                for (const Unit* un : mine) { mx = std::max(mx, un->load); ncl += un->cl.size(); }
+                fprintf(stderr, "[tinv] resident group cs=%d clusters=%zu (own %zu) units=%d (share %d) M2=%d smem=%zu max-load %.0f\n",
+                        rg.cs, ncl, rg.cl.size(), nu, want_units[q], rg.M2, rg.smem, mx);
             }
             offs[q] = (int)img.size();
             int acc = 0;
             img.push_back(0);
-            for (int u = 0; u < nu; u++) { acc += (int)lists[u].size(); img.push_back(acc); }
-            for (int u = 0; u < nu; u++) for (int c : lists[u]) img.push_back(c);
+            for (int u = 0; u < nu; u++) { acc += (int)mine[u]->cl.size(); img.push_back(acc); }
+            for (int u = 0; u < nu; u++) for (int c : mine[u]->cl) img.push_back(c);
         }
         if (img.size() > h->res_cap) {
             if (h->res_buf) cudaFree(h->res_buf);
@@ -762,8 +799,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             // phase timers of unit 0 of one group (the first; TINV_PROF_GROUP picks another)
             const int pg = getenv("TINV_PROF_GROUP") ? atoi(getenv("TINV_PROF_GROUP")) : 0;
             ra.prof = (h->profiling && (int)q == pg) ? reinterpret_cast<unsigned long long*>(h->bnd + 8) : nullptr;
-            CK(launch_resident(ra, rg.cs, units[q], rg.smem, sq));
-            launches++;
+            if (units[q] > 0) {   // a group may have lent all its clusters to larger units
+                CK(launch_resident(ra, rg.cs, units[q], rg.smem, sq));
+                launches++;
+            }
             CK(cudaEventRecord(h->rev[q], sq));
             if (getenv("TINV_DEBUG") && q < 4) CK(cudaEventRecord(h->ev[10 + q], sq));
         }
