@@ -156,6 +156,31 @@ def cpu_baseline(d, e, w, budget_s=12.0, mgs=False):
             "sample": f"first {k} of {n} eigenvectors (start of the single cluster; later vectors cost more), {dt:.1f} s"}
 
 
+def e2e_leg(h, d, e, w, n, args, ws, dev, barrier):
+    """The same metric through tinv_eigvecs_host with pinned host buffers: H2D of d, e, w and
+    the columns of Z landing in host memory inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    hd, he, hw = (torch.tensor(a, dtype=torch.float64).pin_memory() for a in (d, e, w))
+    hZ = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    h.eigvecs_host(hd, he, hw, Z=hZ, seed=args.seed)
+    barrier()
+    e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        h.eigvecs_host(hd, he, hw, Z=hZ, seed=args.seed)
+    barrier()
+    e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+    if ws > 1:
+        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = {"value": n / (e_ms * 1e-3), "unit": "eigenvectors/s", "ms_per_step": e_ms,
+           "h2d_bytes_per_step": 8 * (3 * n - 1), "d2h_bytes_per_step": 8 * n * n}
+    return e2e
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -165,6 +190,7 @@ def main():
     ap.add_argument("--impl", default="tinv", choices=["tinv", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiler runs)")
     ap.add_argument("--reorth", default="cwy", choices=["cwy", "mgs"],
                     help="cwy: compact WY (Alg. 4, the method); mgs: classical MGS (Alg. 1), the paper's comparison")
     ap.add_argument("--verbose", action="store_true")
@@ -272,22 +298,10 @@ def main():
             "share_of_step": avg[dom] / ms_per_step if ms_per_step > 0 else None}
 
     # ---- e2e through the public API with host buffers (pinned)
-    hd, he, hw = (torch.tensor(a, dtype=torch.float64).pin_memory() for a in (d, e, w))
-    hZ = torch.empty((n, n), dtype=torch.float64).pin_memory()
-    h.eigvecs_host(hd, he, hw, Z=hZ, seed=args.seed)
-    barrier()
-    e_steps = max(1, min(args.steps, 5))
-    t0 = time.perf_counter()
-    for _ in range(e_steps):
-        h.eigvecs_host(hd, he, hw, Z=hZ, seed=args.seed)
-    barrier()
-    e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
-    if ws > 1:
-        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
-    e2e = {"value": n / (e_ms * 1e-3), "unit": "eigenvectors/s", "ms_per_step": e_ms,
-           "h2d_bytes_per_step": 8 * (3 * n - 1), "d2h_bytes_per_step": 8 * n * n}
+    if args.no_e2e:
+        e2e = None
+    else:
+        e2e = e2e_leg(h, d, e, w, n, args, ws, dev, barrier)
 
     # one wide cluster holds all the clustered vectors -> the library row-splits it over the
     # ranks; otherwise clusters are sharded by columns
