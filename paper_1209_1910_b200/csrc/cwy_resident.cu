@@ -610,7 +610,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
             bool la_done = false;
             la_have = false;
             bool first = true;
-            if (crank == 0 && tid == 0)   // this vector's factor records for the chained solve
+            if (crank == 0 && tid == 0 && p + 1 < m) {   // the next vector's factor records into L2
+                const double* Fn = Fj + n * 4;             // (this one's were prefetched a vector ago)
+                for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fn + o, min64(8192, n * 4 - o));
+            }
+            if (crank == 0 && tid == 0 && p == 1)
                 for (int64_t o = 0; o < n * 4; o += 8192) l2_prefetch_(Fj + o, min64(8192, n * 4 - o));
             if (crank == 0) back_stage_async(Fj, sm.bc, n);   // (b, c) for its back sweeps
             if (a.mgs) {

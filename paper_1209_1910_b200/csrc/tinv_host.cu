@@ -90,7 +90,7 @@ struct tinv_s {
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
     int mgs = 0;                      // 1: classical MGS reorthogonalisation (Alg. 1)
-    int res_cs2 = 1000, res_cs4 = 1000;   // m from which a cluster gets >= 2 / 4 CTAs
+    int res_cs2 = 1000, res_cs4 = 1000, res_cs8 = 1000;   // m from which a cluster gets >= 2 / 4 / 8 CTAs
     int handover = 1;                 // narrow leaders finish in the resident kernel (n <= 2048)
     double leader_w = 1.0;            // LPT weight of a handed-over leader (vector equivalents)
     double lpt_m = 1.0;               // LPT weight per vector: 1 + lpt_m m / 32
@@ -385,6 +385,7 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     CK(cudaMallocHost(&h->h_out, sizeof(PrepOut)));
     if (const char* v = getenv("TINV_RES_CS2")) h->res_cs2 = atoi(v);
     if (const char* v = getenv("TINV_RES_CS4")) h->res_cs4 = atoi(v);
+    if (const char* v = getenv("TINV_RES_CS8")) h->res_cs8 = atoi(v);
     if (const char* v = getenv("TINV_HANDOVER")) h->handover = atoi(v);
     if (const char* v = getenv("TINV_LEADER_W")) h->leader_w = atof(v);
     if (const char* v = getenv("TINV_LPT_M")) h->lpt_m = atof(v);
@@ -615,7 +616,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             if (m < 2 || m > cwy_narrow_max()) continue;
             const int m2 = (m + 1) & ~1;
             // the longest chains get more CTAs (shorter passes) beyond what their rows need
-            const int want = (m >= h->res_cs4) ? 4 : (m >= h->res_cs2 ? 2 : 1);
+            const int want = (m >= h->res_cs8) ? 8 : (m >= h->res_cs4) ? 4 : (m >= h->res_cs2 ? 2 : 1);
             for (int q = 0; q < 4; q++) {
                 const int RL = (int)(((n + css[q] - 1) / css[q] + 1) & ~int64_t(1));
                 if (css[q] >= want && resident_smem_bytes(n, RL, m2, css[q]) <= 232448) {
