@@ -191,8 +191,9 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiler runs)")
-    ap.add_argument("--reorth", default="cwy", choices=["cwy", "mgs"],
-                    help="cwy: compact WY (Alg. 4, the method); mgs: classical MGS (Alg. 1), the paper's comparison")
+    ap.add_argument("--reorth", default="cwy", choices=["cwy", "mgs", "ordinary"],
+                    help="cwy: compact WY (Alg. 4, reduced §3.3.2 sequence, the method); mgs: classical MGS "
+                         "(Alg. 1), the paper's comparison; ordinary: compact WY in the §3.3.1 sequence")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

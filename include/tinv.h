@@ -165,13 +165,16 @@ int tinv_set_virtual_ranks(tinv_t h, int nranks);
 int tinv_set_resident(tinv_t h, int enable);
 
 /* Reorthogonalisation of clustered vectors: mode 0 (default) = compact WY, Alg. 4
- * (PAPER.md:681-716); mode 1 = the classical inverse iteration's modified Gram-Schmidt,
- * Alg. 1, the paper's comparison method: after every
- * solve, x <- x - <x, z_i> z_i for the cluster's accepted vectors in order, one cluster-wide
- * reduction per z_i.  Same factorization, start vectors, stopping rule and restarts; the
- * vectors agree with mode 0 up to rounding.  Mode 1 runs in the resident kernel only:
- * tinv_eigvecs returns TINV_ERR_UNSUPPORTED when a cluster does not fit it (m > 64 or
- * n > 4096).  Returns 0, -2 for another mode, TINV_ERR_HANDLE. */
+ * in the reduced BLAS sequence of §3.3.2; mode 1 = the classical inverse
+ * iteration's modified Gram-Schmidt, Alg. 1, the
+ * paper's comparison method: after every solve, x <- x - <x, z_i> z_i for the cluster's
+ * accepted vectors in order, one cluster-wide reduction per z_i; mode 2 = compact WY in the
+ * ordinary sequence of §3.3.1 (with the T_j erratum fixed; SURVEY §8(f)
+ * row 4): Y^T y_j by a pass of its own instead of the reduced sequence's reuse of the BC pass.
+ * Same factorization, start vectors, stopping rule and restarts; the vectors agree with mode 0
+ * up to rounding.  Modes 1 and 2 run in the resident kernel only: tinv_eigvecs returns
+ * TINV_ERR_UNSUPPORTED when a cluster does not fit it (m > 64 or n > 4096).  Returns 0, -2
+ * for another mode, TINV_ERR_HANDLE. */
 int tinv_set_reorth(tinv_t h, int mode);
 int tinv_get_stats(tinv_t h, tinv_stats_t* out);
 

@@ -837,7 +837,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                     __syncthreads();
                     PH(12);
                     const int b = pxb;
-                    const double u2s = colacc(sm, ys, r0, ia, nl, p, [&](int i) { return sm.ul[i]; },
+                    // (the ordinary sequence of §3.3.1 forms Y^T y in a pass of its own after R2)
+                    const double u2s = colacc(sm, ys, r0, ia, nl, a.ordinary ? 0 : p, [&](int i) { return sm.ul[i]; },
                                               [&](int k, double v, int c) { pub1(b, k, v, c); }, CS, u2, 0, NT, bsync);
                     PH(15);
                     {
@@ -896,11 +897,29 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
                 const double tt = 1.0 / (c * c - u0 * c);
                 const double y0 = u0 - c;
-                for (int k = tid; k < p; k += NT) {
-                    double v = 0.0;
-                    if (!zero_u)
+                if (a.ordinary) {
+                    // §3.3.1: y_j from u_j, then
+                    // s = Y_{j-1}^T y_j by its own pass over Y (the DGEMV before `that`) instead of
+                    // the reduced sequence's s' - c Y[p,:] from the BC pass
+                    pxb ^= 1;
+                    const int b = pxb;
+                    const int ia = max(0, p - r0);
+                    colacc(sm, ys, r0, ia, nl, p,
+                           [&](int i) { return (r0 + i == p) ? y0 : (zero_u ? 0.0 : sm.ul[i]); },
+                           [&](int k, double v, int cc) { pub1(b, k, v, cc); }, CS, 0.0, 0, NT, bsync);
+                    csync();
+                    for (int k = tid; k < p; k += NT) {
+                        double v = 0.0;
                         for (int cc = 0; cc < CS; cc++) v += PXo(cc, pxb)[k];
-                    sm.s[k] = v - c * sm.yrow[k];
+                        sm.s[k] = v;
+                    }
+                } else {
+                    for (int k = tid; k < p; k += NT) {
+                        double v = 0.0;
+                        if (!zero_u)
+                            for (int cc = 0; cc < CS; cc++) v += PXo(cc, pxb)[k];
+                        sm.s[k] = v - c * sm.yrow[k];
+                    }
                 }
                 pxb ^= 1;
                 __syncthreads();

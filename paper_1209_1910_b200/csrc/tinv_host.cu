@@ -89,7 +89,8 @@ struct tinv_s {
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
-    int mgs = 0;                      // 1: classical MGS reorthogonalisation (Alg. 1)
+    int mgs = 0;                      // reorthogonalisation: 0 reduced cWY (§3.3.2), 1 classical MGS
+                                      // (Alg. 1), 2 ordinary cWY (§3.3.1)
     int res_cs2 = 1000, res_cs4 = 1000, res_cs8 = 1000;   // m from which a cluster gets >= 2 / 4 / 8 CTAs
     int handover = 1;                 // narrow leaders finish in the resident kernel (n <= 2048)
     double leader_w = 1.0;            // LPT weight of a handed-over leader (vector equivalents)
@@ -450,7 +451,7 @@ int tinv_set_resident(tinv_t h, int enable) {
 
 int tinv_set_reorth(tinv_t h, int mode) {
     if (!h) return TINV_ERR_HANDLE;
-    if (mode != 0 && mode != 1) return -2;
+    if (mode < 0 || mode > 2) return -2;
     h->mgs = mode;
     return 0;
 }
@@ -648,7 +649,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         // the largest clusters first (longest dependent chains)
         std::sort(rgroups.begin(), rgroups.end(), [](const ResGroup& a, const ResGroup& b) { return a.cs > b.cs; });
     }
-    if (h->mgs) {   // MGS (Alg. 1) runs in the resident kernel only
+    if (h->mgs) {   // MGS (Alg. 1) and the ordinary sequence run in the resident kernel only
         for (int c = 0; c < nclus; c++)
             if (cs[c + 1] - cs[c] >= 2 && (rs_real || !resident[c]) && (rs_real || (c >= rlo[h->rank] && c < rhi[h->rank]))) {
                 join_b2();
@@ -795,7 +796,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             ra.u_off = h->res_buf + offs[q];
             ra.u_list = h->res_buf + offs[q] + units[q] + 1;
             ra.X1c = h->X1c; ra.F = h->F; ra.FP = h->FP; ra.unn = h->unn; ra.Z = Z; ra.ldz = ldz;
-            ra.iters = h->iters; ra.out = h->out; ra.handover = handover; ra.mgs = h->mgs;
+            ra.iters = h->iters; ra.out = h->out; ra.handover = handover; ra.mgs = h->mgs == 1; ra.ordinary = h->mgs == 2;
             if (const char* v = getenv("TINV_RES_FLAGS")) ra.flags = atoi(v);
             // phase timers of unit 0 of one group (the first; TINV_PROF_GROUP picks another)
             const int pg = getenv("TINV_PROF_GROUP") ? atoi(getenv("TINV_PROF_GROUP")) : 0;

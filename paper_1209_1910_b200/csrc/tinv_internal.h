@@ -181,6 +181,7 @@ struct ResArgs {
                             // x^(1), iterate it here (0: none)
     int flags;              // experiments: bit 0 disables the look-ahead pass
     int mgs;                // 1: classical MGS reorthogonalisation (Alg. 1) instead of compact WY
+    int ordinary;           // 1: the ordinary compact-WY sequence of §3.3.1 (separate Y^T y pass)
 };
 size_t resident_smem_bytes(int64_t n, int RL, int M2, int cs);
 cudaError_t launch_resident(const ResArgs& a, int cs, int nunits, size_t smem, cudaStream_t s);

@@ -172,8 +172,9 @@ class Tinv:
             raise TinvError(f"tinv_set_resident failed: {rc}")
 
     def set_reorth(self, mode: str):
-        """'cwy' (Alg. 4, default) or 'mgs' (Alg. 1, classical modified Gram-Schmidt)."""
-        code = {"cwy": 0, "mgs": 1}[mode]
+        """'cwy' (Alg. 4, reduced sequence §3.3.2, default), 'mgs' (Alg. 1, classical modified
+        Gram-Schmidt) or 'ordinary' (Alg. 4 in the ordinary sequence of §3.3.1)."""
+        code = {"cwy": 0, "mgs": 1, "ordinary": 2}[mode]
         rc = self._L.tinv_set_reorth(self._h, code)
         if rc:
             raise TinvError(f"tinv_set_reorth failed: {rc}")

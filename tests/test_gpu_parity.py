@@ -454,3 +454,24 @@ def test_mgs_unsupported_for_wide_clusters(handle, torch):
         handle.set_reorth("cwy")
     Z, rc = run_gpu(handle, torch, d, e, w)   # the handle still works in cWY mode
     assert rc == 0
+
+
+# ------------------------------------------------------------------ §3.3.1 ordinary sequence
+# tinv_set_reorth(h, 2) -- the same compact-WY step in the ordinary BLAS
+# sequence (Y^T y by its own pass); equals the compact-WY oracle within tolerance.
+
+@pytest.mark.parametrize("cfg,n,sizes", [("cfg2", 1200, None), ("clustered", 2000, [60, 33, 17, 9, 2]),
+                                         ("type3", 420, None)])
+def test_ordinary_cwy_path_parity(handle, torch, cfg, n, sizes):
+    d, e, w = _clustered(n, sizes) if sizes else W.problem(cfg, n)
+    handle.set_reorth("ordinary")
+    try:
+        Zg, rc = run_gpu(handle, torch, d, e, w)
+    finally:
+        handle.set_reorth("cwy")
+    assert rc == 0
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
+    Zo, info = O.eigvecs(d, e, w, seed=1)
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zg.cpu().numpy(), Zo)
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
