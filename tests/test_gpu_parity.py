@@ -475,3 +475,22 @@ def test_ordinary_cwy_path_parity(handle, torch, cfg, n, sizes):
     Zo, info = O.eigvecs(d, e, w, seed=1)
     wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zg.cpu().numpy(), Zo)
     assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+
+
+@pytest.mark.parametrize("mode", ["mgs", "ordinary"])
+def test_reorth_modes_without_handover(handle, torch, mode):
+    """n > 2048: the batched LU iterates every leader (no handover); the resident kernel reads
+    them from Z.  Both comparison modes against their oracle."""
+    d, e, w = _clustered(3000, [20, 12, 7])   # clusters that fit the resident kernel at n = 3000
+    handle.set_reorth(mode)
+    try:
+        Zg, rc = run_gpu(handle, torch, d, e, w)
+        assert handle.stats()["resident_groups"] >= 1
+    finally:
+        handle.set_reorth("cwy")
+    assert rc == 0
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
+    Zo, info = O.eigvecs(d, e, w, seed=1, mgs=(mode == "mgs"))
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zg.cpu().numpy(), Zo)
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
