@@ -441,7 +441,7 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
         const int64_t lo = c * CH, hi = (lo + CH < n) ? lo + CH : n;
         const int cnt = (int)(hi - lo);
         // top remainder (only in the first chunk): scalar rows
-        int top = cnt & ~7;
+        const int top = cnt & ~15;
         for (int u = cnt - 1; u >= top; u--) {
             const double2 bc = *reinterpret_cast<const double2*>(Fs + u * 4 + 2);
             const double xi = fma(-bc.x, x1, fma(-bc.y, x2, Ts[u]));
@@ -449,35 +449,25 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
             x2 = x1;
             x1 = xi;
         }
-        // 8-row batches, loads of the next batch issued before the current chain (measured
-        // 13 cycles/row on B200 vs 20-30 for per-row forms; DFMA latency is 8)
-        if (top > 0) {
-            double b[8], c[8], t[8];
+        // 16-row batches: the batch's loads first (independent), then the dependent chain
+        // (~15 cycles/row in the kernels; the 8-row form with the next batch's loads in
+        // flight measured ~19-23; tools/micro/sweep_var.cu)
+        for (int u0 = top - 16; u0 >= 0; u0 -= 16) {
+            double b[16], c[16], t[16], xv[16];
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const double2 bc = *reinterpret_cast<const double2*>(Fs + (top - 8 + u) * 4 + 2);
-                b[u] = bc.x; c[u] = bc.y; t[u] = Ts[top - 8 + u];
+            for (int u = 0; u < 16; u++) {
+                const double2 bc = *reinterpret_cast<const double2*>(Fs + (u0 + u) * 4 + 2);
+                b[u] = bc.x; c[u] = bc.y; t[u] = Ts[u0 + u];
             }
-            for (int u0 = top - 8; u0 >= 0; u0 -= 8) {
-                double bn[8], cn[8], tn[8], xv[8];
-                const int nx = u0 >= 8 ? u0 - 8 : 0;
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const double2 bc = *reinterpret_cast<const double2*>(Fs + (nx + u) * 4 + 2);
-                    bn[u] = bc.x; cn[u] = bc.y; tn[u] = Ts[nx + u];
-                }
-#pragma unroll
-                for (int u = 7; u >= 0; u--) {
-                    xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u]));
-                    x2 = x1;
-                    x1 = xv[u];
-                }
-#pragma unroll
-                for (int u = 0; u < 8; u += 2)
-                    __stcg(reinterpret_cast<double2*>(x + lo + u0 + u), make_double2(xv[u], xv[u + 1]));
-#pragma unroll
-                for (int u = 0; u < 8; u++) { b[u] = bn[u]; c[u] = cn[u]; t[u] = tn[u]; }
+            for (int u = 15; u >= 0; u--) {
+                xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u]));
+                x2 = x1;
+                x1 = xv[u];
             }
+#pragma unroll
+            for (int u = 0; u < 16; u += 2)
+                __stcg(reinterpret_cast<double2*>(x + lo + u0 + u), make_double2(xv[u], xv[u + 1]));
         }
         if (k + kRing < C) issue(k + kRing);
     }
