@@ -37,6 +37,7 @@ namespace res {
 
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
+static_assert(NT >= 4 * kNarrowM, "TT / TN use four threads per column of a cluster of up to kNarrowM vectors");
 constexpr int kXS = 16;          // scalar slots of the exchange area
 enum { U2 = 0, X2 = 1, U0 = 2, Q2 = 3, QINF = 4, QARG = 5, Q1 = 6, FA = 7, FB = 8, X2N = 9, GPN = 10, QSGN = 11, Q0 = 12 };
 
@@ -800,11 +801,15 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 first = false;
                 use_la = false;
                 PH(0);
-                // ---------------- TT: g' = T_p^T g (replicated)
-                for (int k = tid; k < p; k += NT) {
+                // ---------------- TT: g' = T_p^T g (replicated); four threads per column (p <= 64)
+                {
+                    const int k = tid >> 2, sub = tid & 3;
                     double v = 0.0;
-                    for (int l = 0; l <= k; l++) v = fma(sm.T[l * TS + k], sm.g[l], v);
-                    sm.gp[k] = v;
+                    if (k < p)
+                        for (int l = sub; l <= k; l += 4) v = fma(sm.T[l * TS + k], sm.g[l], v);
+                    v += __shfl_xor_sync(0xffffffffu, v, 1);
+                    v += __shfl_xor_sync(0xffffffffu, v, 2);
+                    if (k < p && sub == 0) sm.gp[k] = v;
                 }
                 __syncthreads();
                 PH(1);
@@ -924,17 +929,27 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                 pxb ^= 1;
                 __syncthreads();
                 PH(3);
-                // ---------------- TN (replicated): that, x', column p of T; column p of local Y
-                for (int l = tid; l < p; l += NT) {
+                // ---------------- TN (replicated): that, x', column p of T; column p of local Y;
+                // four threads per row of T (p <= 64)
+                {
+                    const int l = tid >> 2, sub = tid & 3;
                     double a1 = 0.0, a2 = 0.0;
-                    const double* tr = sm.T + (size_t)l * TS;
-                    for (int k = l; k < p; k++) {
-                        a1 = fma(tr[k], sm.s[k], a1);
-                        a2 = fma(tr[k], sm.yrow[k], a2);
+                    if (l < p) {
+                        const double* tr = sm.T + (size_t)l * TS;
+                        for (int k = l + sub; k < p; k += 4) {
+                            a1 = fma(tr[k], sm.s[k], a1);
+                            a2 = fma(tr[k], sm.yrow[k], a2);
+                        }
                     }
-                    const double that = -tt * a1;
-                    sm.xp[l] = a2 + y0 * that;
-                    sm.T[(size_t)l * TS + p] = that;
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, 1);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, 2);
+                    if (l < p && sub == 0) {
+                        const double that = -tt * a1;
+                        sm.xp[l] = a2 + y0 * that;
+                        sm.T[(size_t)l * TS + p] = that;
+                    }
                 }
                 if (tid == 0) {
                     sm.xp[p] = tt * y0;
