@@ -62,8 +62,8 @@ struct L {        // shared-memory carve-up (doubles unless noted)
     double* Y;    // RL x M2, local rows; the 16-byte column pairs of row i are XOR-swizzled
                   // (yo) so that a warp's loads of one pair from consecutive rows hit distinct banks
     double* xl;   // RL: current iterate
-    double* ul;   // RL: uhat
-    double* ql;   // RL: q
+    double* ul;   // RL: uhat (BC .. TN)
+    double* ql;   // RL: q (D .. the solve's forward pass / z); shares ul's storage (disjoint lives)
     double* x1l;  // RL: x^(1) of the next vector (look-ahead)
     double* T;    // M2 x TS row-major, T[l][k] (odd stride TS = M2 + 1: threads walking rows do not collide)
     double* g;    // M2 + 2
@@ -83,7 +83,7 @@ struct L {        // shared-memory carve-up (doubles unless noted)
 __host__ __device__ inline size_t smem_doubles(int64_t n, int RL, int M2, int CS) {
     const size_t XW = (size_t)M2 + kXS;
     const size_t TS = M2 + 1;
-    return (size_t)RL * (M2 + 4) + (size_t)M2 * TS + 1 + 5 * (size_t)(M2 + 2) + 3 * CS * XW + (n + 2) + 2 * (size_t)n +
+    return (size_t)RL * (M2 + 3) + (size_t)M2 * TS + 1 + 5 * (size_t)(M2 + 2) + 3 * CS * XW + (n + 2) + 2 * (size_t)n +
            4 + 2 * NW * 6 + NW + 2 * NT + 8;
 }
 
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
         sm.Y = p; p += (size_t)RL * M2;
         sm.xl = p; p += RL;
         sm.ul = p; p += RL;
-        sm.ql = p; p += RL;
+        sm.ql = sm.ul;
         sm.x1l = p; p += RL;
         sm.T = p; p += (size_t)M2 * TS;
         sm.g = p; p += M2 + 2;
