@@ -692,8 +692,20 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 for (int c : rgroups[q].cl) vec += (double)(cs[c + 1] - cs[c] - 1) + (handover ? h->leader_w : 0.0);
                 // measured: a unit spends about the same time per vector whatever its CTA
                 // count (fewer rows per CTA but more exchange), so SM-time ~ vectors x CTAs
-                wg[q] = vec;
-                if (q > 0) wrest += vec * rgroups[q].cs;
+                // a group's share scale (measured on cfg2: the 2-CTA units are the critical ones);
+                // TINV_SPLIT="cs:f,..." overrides
+                double sf = (rgroups[q].cs == 2) ? 1.15 : 1.0;
+                if (const char* v = getenv("TINV_SPLIT")) {
+                    int k; double f; const char* qq = v;
+                    while (sscanf(qq, "%d:%lf", &k, &f) == 2) {
+                        if (k == rgroups[q].cs) sf = f;
+                        const char* comma = strchr(qq, ',');
+                        if (!comma) break;
+                        qq = comma + 1;
+                    }
+                }
+                wg[q] = vec * sf;
+                if (q > 0) wrest += vec * sf * rgroups[q].cs;
             }
             // SMs still held by the iterating batched-LU warps (handover: they run concurrently)
             int budget = h->nsm - (handover ? po.nc_pad / 32 : 0);
