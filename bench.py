@@ -297,6 +297,10 @@ def main():
             "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": src,
             "alg_bytes_per_launch": alg_bytes, "kernel_ms": avg[dom],
             "share_of_step": avg[dom] / ms_per_step if ms_per_step > 0 else None}
+    if dom == "cwy" and st.get("resident_groups", 0) > 0:
+        roof["note"] = ("resident cWY kernel: Y stays in shared memory, so DRAM traffic is far below the "
+                        "algorithmic bytes; the step is bound by the dependent chains and phase latencies "
+                        "(DESIGN.md section 8), not by HBM")
 
     # ---- e2e through the public API with host buffers (pinned)
     if args.no_e2e:
