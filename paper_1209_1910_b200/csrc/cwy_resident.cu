@@ -840,12 +840,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_resident_kernel(ResArgs a) {
                             st_cl(cl_addr(sm.yrow + k, c), sm.Y[ys.at(p - r0, k)]);
                         }
                     __syncthreads();
-                    PH(12);
                     const int b = pxb;
                     // (the ordinary sequence of §3.3.1 forms Y^T y in a pass of its own after R2)
                     const double u2s = colacc(sm, ys, r0, ia, nl, a.ordinary ? 0 : p, [&](int i) { return sm.ul[i]; },
                                               [&](int k, double v, int c) { pub1(b, k, v, c); }, CS, u2, 0, NT, bsync);
-                    PH(15);
                     {
                         const double u0v = (p >= r0 && p < r1) ? sm.ul[p - r0] : 0.0;
                         pubs(pxb, 2, [&](int k, int& slot) {
