@@ -60,10 +60,10 @@ constexpr size_t smem_fixed() { return sizeof(Stage) * NS + ((8 * kBars<NS> + 15
 __device__ __forceinline__ double rcp_pivot(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
+    // one third-order step r (1 + e + e^2), e = 1 - x r: relative error delta -> delta^3
+    // (three dependent FMAs instead of the four of two Newton steps)
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);
 }
 
 // SDE: d and e staged in shared memory (compile-time, so their loads are LDS, not generic)
