@@ -117,6 +117,7 @@ struct tinv_s {
     cudaEvent_t ev_prep = nullptr;
     cudaStream_t bst = nullptr;       // handover: the iterating batched-LU warps + finalize
     cudaEvent_t ev_b2 = nullptr;
+    cudaEvent_t ev_img = nullptr;     // resident unit lists copied (side stream)
     tinv_stats_t stats{};
 };
 
@@ -398,6 +399,7 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     CK(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&h->bst, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_b2, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_img, cudaEventDisableTiming));
     if (h->nranks > 1) {
         if (!cfg->nccl_id || !g_nccl.load()) { delete h; return TINV_ERR_NCCL; }
         ncclUniqueId id;
@@ -430,6 +432,7 @@ int tinv_destroy(tinv_t h) {
     if (h->side) cudaStreamDestroy(h->side);
     if (h->bst) cudaStreamDestroy(h->bst);
     if (h->ev_b2) cudaEventDestroy(h->ev_b2);
+    if (h->ev_img) cudaEventDestroy(h->ev_img);
     for (auto& q : h->rs) if (q) cudaStreamDestroy(q);
     for (auto& q : h->rev) if (q) cudaEventDestroy(q);
     delete h;
@@ -796,7 +799,11 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             h->h_res_cap = img.size();
         }
         memcpy(h->h_res, img.data(), sizeof(int) * img.size());
-        CK(cudaMemcpyAsync(h->res_buf, h->h_res, sizeof(int) * img.size(), cudaMemcpyHostToDevice, st));
+        // on the side stream (ordered after this call's prep, hence after the previous call), so
+        // the copy's latency overlaps the batched LU instead of following it
+        CK(cudaMemcpyAsync(h->res_buf, h->h_res, sizeof(int) * img.size(), cudaMemcpyHostToDevice, h->side));
+        CK(cudaEventRecord(h->ev_img, h->side));
+        CK(cudaStreamWaitEvent(st, h->ev_img, 0));
         // fork: every cluster size on its own stream (independent eigen-clusters), join below
         CK(cudaEventRecord(h->rev[4], st));
         for (size_t q = 0; q < rgroups.size(); q++) {
