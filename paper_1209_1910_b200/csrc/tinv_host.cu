@@ -86,6 +86,7 @@ struct tinv_s {
     int* h_cstart = nullptr;
     int* h_iters = nullptr;
     int64_t h_cap = 0;
+    int64_t iters_n = 0;              // > 0: the last call's iteration counts not yet read back
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
@@ -468,6 +469,14 @@ int tinv_set_profiling(tinv_t h, int enable) {
 int tinv_get_stats(tinv_t h, tinv_stats_t* out) {
     if (!h) return TINV_ERR_HANDLE;
     if (!out) return -2;
+    if (h->iters_n > 0) {   // the last call's iteration histogram, read back on first request
+        CK(cudaSetDevice(h->device));
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaMemcpy(h->h_iters, h->iters, sizeof(int) * h->iters_n, cudaMemcpyDeviceToHost));
+        for (int k = 0; k < 8; k++) h->stats.iters_hist[k] = 0;
+        for (int64_t j = 0; j < h->iters_n; j++) h->stats.iters_hist[std::min(7, std::max(0, h->h_iters[j]))]++;
+        h->iters_n = 0;
+    }
     *out = h->stats;
     return 0;
 }
@@ -486,6 +495,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     cudaStream_t st = h->stream;
     tinv_stats_t& S = h->stats;
     memset(&S, 0, sizeof(S));
+    h->iters_n = 0;
     S.n = n;
     int launches = 0;
 
@@ -1032,10 +1042,9 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     // ---------------- status
     ev_record(h, 7);
     CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h->h_iters, h->iters, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
-    for (int64_t j = 0; j < n; j++) S.iters_hist[std::min(7, std::max(0, h->h_iters[j]))]++;
+    h->iters_n = n;   // iters_hist: read back lazily by tinv_get_stats
     // algorithmic bytes of the compact-WY work (paper kernel sequence
     // PAPER.md:530-623): one cWY step of vector j_c = p reads 8 (4 p n - 1.5 p^2) bytes;
     // every iteration of a clustered vector runs one step.
