@@ -20,7 +20,11 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
     __shared__ int s_bad;
     const int64_t n = a.n;
     const int tid = threadIdx.x;
-    if (tid == 0) { s_bad = 0; s_carry = 0; }
+    if (tid == 0) {
+        s_bad = 0;
+        s_carry = 0;
+        *a.out = PrepOut{};   // the call's summary starts from zero (the later kernels accumulate)
+    }
     __syncthreads();
 
     // ---- R1 + validation

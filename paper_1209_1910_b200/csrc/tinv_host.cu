@@ -519,7 +519,6 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         return 0;
     };
     ev_record(h, 0);
-    CK(cudaMemsetAsync(h->out, 0, sizeof(PrepOut), st));
     PrepArgs pa{n, d, e, w, h->wt, h->cstart, h->cid, h->jc, h->slot, h->perm, batched_slot_cap(n), handover, h->out};
     launch_prep(pa, st);
     launches++;
