@@ -9,6 +9,7 @@
 // With nranks > 1 the clusters are sharded over the ranks in contiguous column ranges and
 // each rank's columns are broadcast with NCCL at the end (no data-path collective).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -492,6 +493,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     if (ldz < n) return -7;
     CK(cudaSetDevice(h->device));
     if (int r = ensure_base(h, n)) return r;
+    const auto t_host0 = std::chrono::steady_clock::now();   // TINV_DEBUG: host-side timeline
     cudaStream_t st = h->stream;
     tinv_stats_t& S = h->stats;
     memset(&S, 0, sizeof(S));
@@ -807,6 +809,9 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             CK(cudaMallocHost(&h->h_res, sizeof(int) * img.size()));
             h->h_res_cap = img.size();
         }
+        if (getenv("TINV_DEBUG"))
+            fprintf(stderr, "[tinv] host: resident schedule ready %.3f ms after the call started\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count());
         memcpy(h->h_res, img.data(), sizeof(int) * img.size());
         // on the side stream (ordered after this call's prep, hence after the previous call), so
         // the copy's latency overlaps the batched LU instead of following it
