@@ -78,9 +78,26 @@ __device__ __forceinline__ int64_t bsearch_cum(int64_t lo, int64_t hi, int64_t t
     }
     return lo;
 }
-// rows of A / D weighted by their length min(i+1, P)
-__device__ __forceinline__ void part_rows_weighted(int64_t n, int64_t P, int r, int G, int64_t& a, int64_t& b) {
-    auto cum = [P](int64_t i) -> int64_t { return i <= P ? i * (i + 1) / 2 : P * (P + 1) / 2 + (i - P) * P; };
+// Static partitions of the passes over the group's CTAs.  A wide pass (P > kNarrowM) costs
+// a CTA its elements plus a fixed consumer cost per row piece (one TMA copy and one warp's
+// dot / accumulate per piece of <= kPieceW columns), measured at several thousand elements
+// (CwyArgs::piece_cost): the rows of the triangles (short rows, one or two pieces each) are
+// weighted accordingly, or the CTA holding them sets the phase time.
+constexpr int kPieceW = 2 * (NW - 1) * 32;   // = PW below
+// sum_{i < l} floor(i / kPieceW)
+__device__ __forceinline__ int64_t sum_floor_pw(int64_t l) {
+    const int64_t q = l / kPieceW, rem = l - q * kPieceW;
+    return (int64_t)kPieceW * q * (q - 1) / 2 + rem * q;
+}
+// rows of A / D: row i has min(i+1, P) elements in min(floor(i / kPieceW) + 1, nblk) pieces
+__device__ __forceinline__ void part_rows_weighted(int64_t n, int64_t P, int r, int G, int64_t& a, int64_t& b,
+                                                   int64_t C) {
+    if (P <= kNarrowM) C = 0;
+    const int64_t NB = (P + kPieceW - 1) / kPieceW;
+    auto cum = [P, C, NB](int64_t i) -> int64_t {
+        if (i <= P) return i * (i + 1) / 2 + C * (sum_floor_pw(i) + i);
+        return P * (P + 1) / 2 + C * (sum_floor_pw(P) + P) + (i - P) * (P + C * NB);
+    };
     int64_t W = cum(n);
     a = (r == 0) ? 0 : bsearch_cum(0, n, (W * r) / G, cum);
     b = (r == G - 1) ? n : bsearch_cum(0, n, (W * (r + 1)) / G, cum);
@@ -90,16 +107,19 @@ __device__ __forceinline__ void part_uniform(int64_t lo, int64_t hi, int r, int 
     a = lo + (len * r) / G;
     b = lo + (len * (r + 1)) / G;
 }
-// k in [0,p) weighted by k+1 (packed columns of T)
-__device__ __forceinline__ void part_tt(int64_t p, int r, int G, int64_t& a, int64_t& b) {
-    auto cum = [](int64_t k) -> int64_t { return k * (k + 1) / 2; };
+// k in [0,p): packed column k of T has k+1 elements in floor(k / kPieceW) + 1 pieces
+__device__ __forceinline__ void part_tt(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C) {
+    if (p <= kNarrowM) C = 0;
+    auto cum = [C](int64_t k) -> int64_t { return k * (k + 1) / 2 + C * (sum_floor_pw(k) + k); };
     int64_t W = cum(p);
     a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
     b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
 }
-// l in [0,p) weighted by p-l (rows of T)
-__device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int64_t& b) {
-    auto cum = [p](int64_t l) -> int64_t { return l * p - l * (l - 1) / 2; };
+// l in [0,p): row l of T has p-l elements in nblk - floor(l / kPieceW) pieces
+__device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C) {
+    if (p <= kNarrowM) C = 0;
+    const int64_t NB = (p + kPieceW - 1) / kPieceW;
+    auto cum = [p, C, NB](int64_t l) -> int64_t { return l * p - l * (l - 1) / 2 + C * (l * NB - sum_floor_pw(l)); };
     int64_t W = cum(p);
     a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
     b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
@@ -736,6 +756,7 @@ __device__ __forceinline__ void narrow_colacc_finish(const Smem& sm, int CPT, in
 constexpr int NCW = NW - 1;              // consumer warps
 constexpr int NCT = NCW * 32;            // consumer threads
 constexpr int PW = 2 * NCT;              // column block / piece width (doubles) = 448
+static_assert(PW == kPieceW, "piece width of the partitions");
 constexpr int PPS = NCW;                 // pieces per stage = consumer warps
 constexpr int RCH = 1024;                // rows per chunk (row accumulators; coefficients in Smem::cf)
 constexpr int kWStgD = PPS * PW;         // doubles per wide ring slot
@@ -1135,11 +1156,13 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     __syncthreads();
     uint32_t mbph = 0;   // back-sweep ring phase bits (thread 0)
     uint32_t rph = 0;    // pass ring phase bits (every thread)
-    const bool timing0 = (a.prof != nullptr) && threadIdx.x == 0 && (int)blockIdx.x == a.g_cta0[0];
+    // pass timers: the first consumer thread of the first group's first CTA
+    const bool timing0 = (a.prof != nullptr) && threadIdx.x == 32 && (int)blockIdx.x == a.g_cta0[0] + a.prof_sel;
     uint64_t ntim[4] = {0, 0, 0, 0};
+    uint64_t ntim_sink[4] = {0, 0, 0, 0};
     const Ring rg{ring_base, sm.mbar + kRing, &rph, timing0 ? ntim : nullptr};
     uint32_t wiss = 0, wuse = 0;   // wide ring stage counters (issued: warp 0; used: all)
-    const WRing wr{ring_base, wfull, wempty, &wiss, &wuse, timing0 ? ntim : nullptr};
+    WRing wr{ring_base, wfull, wempty, &wiss, &wuse, timing0 ? ntim : nullptr};
     const int tid = threadIdx.x;
     int g = 0;
     for (int t = 0; t < a.ngroups; t++)
@@ -1156,10 +1179,16 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     const bool own_out = !(ws.vrt && RK != 0);   // virtual ranks share the caller's outputs
     long long nsync = 0;
     unsigned int bar_epoch = 0;
+    // debug (TINV_PROF_CTA): this CTA's busy time before each barrier, attributed to the
+    // phase that the next mark() closes
+    const bool ctime = (a.prof_cta != nullptr) && tid == 0;
+    uint64_t c_last = ctime ? gtime() : 0, c_busy = 0;
     auto gsync = [&]() {
+        if (ctime) c_busy += gtime() - c_last;
         if (NR == 1) group_sync(ws.bar, G, bar_epoch);
         else group_sync_ranks(ws.bar, ws.delta, NR, Gt, bar_epoch);
         nsync++;
+        if (ctime) c_last = gtime();
     };
     // mirrored store: every rank's replica of the group workspace
     auto mst = [&](double* ptr, double v) {
@@ -1171,21 +1200,19 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     const bool timing = (a.prof != nullptr) && r == 0 && tid == 0;
     uint64_t tacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     uint64_t tmark = timing ? gtime() : 0;
+    bool inwin = true;   // the current vector is inside the timed window [prof_p0, prof_p1)
     auto mark = [&](int k) {
+        if (ctime) {
+            if (inwin) a.prof_cta[(int64_t)blockIdx.x * 16 + k] += c_busy;
+            c_busy = 0;
+        }
         if (timing) {
             uint64_t _t = gtime();
-            tacc[k] += _t - tmark;
+            if (inwin) tacc[k] += _t - tmark;
             tmark = _t;
         }
     };
-#define PH(k)                                         \
-    do {                                              \
-        if (timing) {                                 \
-            uint64_t _t = gtime();                    \
-            tacc[k] += _t - tmark;                    \
-            tmark = _t;                               \
-        }                                             \
-    } while (0)
+#define PH(k) mark(k)
 
     const int64_t n = a.n;
     const int64_t n2v = (n + 1) & ~int64_t(1);   // vector stride of X1c
@@ -1234,6 +1261,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         bool la_have = false;   // look-ahead of this vector's first pass A is ready
         for (int64_t p = 1; p < m; p++) {
             const int64_t j = j1 + p;
+            inwin = p >= a.prof_p0 && p < a.prof_p1;
+            if (timing0) wr.tacc = inwin ? ntim : ntim_sink;
             const double* xcur = a.X1c + j * n2v;   // x^(1), contiguous copy
             int64_t xs = 1;
             int its = 1, kin = 1, passes = 0, restart = 0;
@@ -1246,7 +1275,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     // ---------------- A: partial g = Y_p^T x, ||x||^2
                     {
                         int64_t i0, i1;
-                        part_rows_weighted(n, p, cg, Gt, i0, i1);
+                        part_rows_weighted(n, p, cg, Gt, i0, i1, a.piece_cost);
                         double x2 = 0.0;
                         if (narrow) {
                             const int CPT = pow2ceil((int)((p + 1) / 2));
@@ -1287,7 +1316,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // ---------------- TT: g' = T_p^T g
                 {
                     int64_t k0, k1;
-                    part_tt(p, cg, Gt, k0, k1);
+                    part_tt(p, cg, Gt, k0, k1, a.piece_cost);
                     if (p > kNarrowM) {
                         wide_rowdots<false>(sm, wr, SrcTc{Tc, (int)p}, (int)k0, (int)k1, ws.g, nullptr, p,
                                             [&](int64_t k, double v, double) { mst(ws.gp + k, v); });
@@ -1395,7 +1424,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // ---------------- TN: [Ts, h] = T_p [s, yrow]; column p of T and Y; x'
                 {
                     int64_t l0, l1;
-                    part_tn(p, cg, Gt, l0, l1);
+                    part_tn(p, cg, Gt, l0, l1, a.piece_cost);
                     if (p > kNarrowM) {
                         wide_rowdots<true>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, yrow, p,
                                            [&](int64_t l, double a1, double a2) {
@@ -1461,7 +1490,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 bool flast = false;
                 {
                     int64_t i0, i1;
-                    part_rows_weighted(n, p + 1, cg, Gt, i0, i1);
+                    part_rows_weighted(n, p + 1, cg, Gt, i0, i1, a.piece_cost);
                     double q2 = 0.0, q1 = 0.0, qinf = -1.0;
                     int64_t qarg = 0;
                     if (tid == 0) {   // this CTA's factor rows (forward sweep below, back sweep)
@@ -1677,7 +1706,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         // (every rank's CTA 0 solves; the others split the rows over all ranks)
                         const int Gl = Gt - NR, rl = RK * (G - 1) + (r - 1);
                         int64_t i0, i1;
-                        part_rows_weighted(n, p, rl, Gl, i0, i1);
+                        part_rows_weighted(n, p, rl, Gl, i0, i1, a.piece_cost);
                         double x2n = (p > kNarrowM)
                                          ? wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, a.X1c + (j + 1) * n2v, p,
                                                        ws.P2 + (int64_t)cg * mc, false)

@@ -977,9 +977,35 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.X1c = h->X1c; ca.Z = Z; ca.ldz = ldz; ca.iters = h->iters; ca.out = h->out;
         ca.ngroups = ng; ca.g_cta0 = arrs[0]; ca.g_size = arrs[1]; ca.g_coff = arrs[2]; ca.g_clist = arrs[3];
         ca.ws = dws; ca.syncs = syncs; ca.prof = h->profiling ? prof : nullptr;
+        ca.prof_p0 = getenv("TINV_PROF_P0") ? atoi(getenv("TINV_PROF_P0")) : 0;
+        ca.prof_p1 = getenv("TINV_PROF_P1") ? atoi(getenv("TINV_PROF_P1")) : (1 << 30);
         ca.vcap = vcap;
         ca.nstg = nstg;
+        ca.piece_cost = getenv("TINV_PIECE_COST") ? atoi(getenv("TINV_PIECE_COST")) : 4000;
+        ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
+        unsigned long long* pcta = nullptr;
+        if (getenv("TINV_PROF_CTA")) {   // debug only (not the product path): per-CTA phase busy times
+            CK(cudaMalloc(&pcta, sizeof(unsigned long long) * 16 * sc.nctas));
+            CK(cudaMemsetAsync(pcta, 0, sizeof(unsigned long long) * 16 * sc.nctas, st));
+            ca.prof_cta = pcta;
+        }
         CK(launch_cwy(ca, sc.nctas, smem, st));
+        if (pcta) {
+            std::vector<unsigned long long> hc((size_t)16 * sc.nctas);
+            CK(cudaMemcpyAsync(hc.data(), pcta, sizeof(unsigned long long) * hc.size(), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            CK(cudaFree(pcta));
+            for (int k = 0; k < 12; k++) {
+                std::vector<double> v;
+                for (int c = 0; c < sc.nctas; c++) v.push_back(hc[(size_t)c * 16 + k] * 1e-6);
+                std::vector<double> srt = v;
+                std::sort(srt.begin(), srt.end());
+                if (srt.back() == 0.0) continue;
+                int amax = (int)(std::max_element(v.begin(), v.end()) - v.begin());
+                fprintf(stderr, "[tinv] cta busy phase %2d (ms): min %.3f med %.3f max %.3f (cta %d) cta0 %.3f\n", k,
+                        srt.front(), srt[srt.size() / 2], srt.back(), amax, v[0]);
+            }
+        }
         launches++;
         S.ngroups = ng;
         S.cwy_ctas = sc.nctas;

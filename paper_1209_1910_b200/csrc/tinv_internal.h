@@ -155,6 +155,10 @@ struct CwyArgs {
     unsigned long long* prof;  // optional per-group phase times [g*16 + phase] (ns), or NULL
     int64_t vcap;            // largest vector staged in shared memory (max mcap over groups)
     int nstg;                // TMA ring stages for narrow clusters (0 = ring not allocated)
+    int prof_p0, prof_p1;    // phase timers count only vectors with prof_p0 <= j_c < prof_p1
+    int piece_cost;          // partition cost of one wide row piece, in elements (cwy.cu part_*)
+    int prof_sel;            // debug: CTA whose thread 32 runs the pass timers (default: the first group's first)
+    unsigned long long* prof_cta;   // debug: per-CTA busy time before each phase's barrier [cta*16 + phase], or NULL
 };
 
 // Resident compact-WY kernel for narrow clusters (cwy_resident.cu): one thread-block cluster
