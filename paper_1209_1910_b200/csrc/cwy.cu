@@ -86,7 +86,7 @@ __device__ __forceinline__ int64_t bsearch_cum(int64_t lo, int64_t hi, int64_t t
 constexpr int kPieceW = 2 * (NW - 1) * 32;   // = PW below
 // sum_{i < l} floor(i / kPieceW)
 __device__ __forceinline__ int64_t sum_floor_pw(int64_t l) {
-    const int64_t q = l / kPieceW, rem = l - q * kPieceW;
+    const int64_t q = (int64_t)((uint32_t)l / (uint32_t)kPieceW), rem = l - q * kPieceW;   // l < 2^31
     return (int64_t)kPieceW * q * (q - 1) / 2 + rem * q;
 }
 // rows of A / D: row i has min(i+1, P) elements in min(floor(i / kPieceW) + 1, nblk) pieces
@@ -1156,13 +1156,13 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     __syncthreads();
     uint32_t mbph = 0;   // back-sweep ring phase bits (thread 0)
     uint32_t rph = 0;    // pass ring phase bits (every thread)
-    // pass timers: the first consumer thread of the first group's first CTA
+    // pass timers (whole launch, not windowed): the first consumer thread of the first
+    // group's first CTA (+ prof_sel)
     const bool timing0 = (a.prof != nullptr) && threadIdx.x == 32 && (int)blockIdx.x == a.g_cta0[0] + a.prof_sel;
     uint64_t ntim[4] = {0, 0, 0, 0};
-    uint64_t ntim_sink[4] = {0, 0, 0, 0};
     const Ring rg{ring_base, sm.mbar + kRing, &rph, timing0 ? ntim : nullptr};
     uint32_t wiss = 0, wuse = 0;   // wide ring stage counters (issued: warp 0; used: all)
-    WRing wr{ring_base, wfull, wempty, &wiss, &wuse, timing0 ? ntim : nullptr};
+    const WRing wr{ring_base, wfull, wempty, &wiss, &wuse, timing0 ? ntim : nullptr};
     const int tid = threadIdx.x;
     int g = 0;
     for (int t = 0; t < a.ngroups; t++)
@@ -1262,7 +1262,6 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         for (int64_t p = 1; p < m; p++) {
             const int64_t j = j1 + p;
             inwin = p >= a.prof_p0 && p < a.prof_p1;
-            if (timing0) wr.tacc = inwin ? ntim : ntim_sink;
             const double* xcur = a.X1c + j * n2v;   // x^(1), contiguous copy
             int64_t xs = 1;
             int its = 1, kin = 1, passes = 0, restart = 0;
@@ -1270,12 +1269,18 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             bool use_la = la_have;           // first iteration: A already done in look-ahead
             bool la_done = false;            // look-ahead for vector p+1 issued
             la_have = false;
+            // this CTA's share of every pass of vector p (the same in each iteration)
+            int64_t pa0, pa1, ptt0, ptt1, ptn0, ptn1, pd0, pd1;
+            part_rows_weighted(n, p, cg, Gt, pa0, pa1, a.piece_cost);
+            part_tt(p, cg, Gt, ptt0, ptt1, a.piece_cost);
+            part_tn(p, cg, Gt, ptn0, ptn1, a.piece_cost);
+            part_rows_weighted(n, p + 1, cg, Gt, pd0, pd1, a.piece_cost);
             while (!done) {
                 if (!use_la) {
                     // ---------------- A: partial g = Y_p^T x, ||x||^2
                     {
                         int64_t i0, i1;
-                        part_rows_weighted(n, p, cg, Gt, i0, i1, a.piece_cost);
+                        i0 = pa0; i1 = pa1;
                         double x2 = 0.0;
                         if (narrow) {
                             const int CPT = pow2ceil((int)((p + 1) / 2));
@@ -1316,7 +1321,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // ---------------- TT: g' = T_p^T g
                 {
                     int64_t k0, k1;
-                    part_tt(p, cg, Gt, k0, k1, a.piece_cost);
+                    k0 = ptt0; k1 = ptt1;
                     if (p > kNarrowM) {
                         wide_rowdots<false>(sm, wr, SrcTc{Tc, (int)p}, (int)k0, (int)k1, ws.g, nullptr, p,
                                             [&](int64_t k, double v, double) { mst(ws.gp + k, v); });
@@ -1424,7 +1429,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // ---------------- TN: [Ts, h] = T_p [s, yrow]; column p of T and Y; x'
                 {
                     int64_t l0, l1;
-                    part_tn(p, cg, Gt, l0, l1, a.piece_cost);
+                    l0 = ptn0; l1 = ptn1;
                     if (p > kNarrowM) {
                         wide_rowdots<true>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, yrow, p,
                                            [&](int64_t l, double a1, double a2) {
@@ -1490,7 +1495,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 bool flast = false;
                 {
                     int64_t i0, i1;
-                    part_rows_weighted(n, p + 1, cg, Gt, i0, i1, a.piece_cost);
+                    i0 = pd0; i1 = pd1;
                     double q2 = 0.0, q1 = 0.0, qinf = -1.0;
                     int64_t qarg = 0;
                     if (tid == 0) {   // this CTA's factor rows (forward sweep below, back sweep)
