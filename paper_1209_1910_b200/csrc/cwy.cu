@@ -451,8 +451,14 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
     };
     for (int64_t k = 0; k < C && k < kRing; k++) issue(k);
     double x1 = 0.0, x2 = 0.0;
+    // x leaves through a double-buffered shared staging area and one bulk store per chunk
+    // (per-row global stores on the chain cost ~16 us per 8000 rows)
+    // (the wide row dots' accumulators: no wide pass runs on this CTA during the sweep)
+    double* xbuf = sm.racc;   // 2 CH doubles
     for (int64_t k = 0; k < C; k++) {
         const int slot = (int)(k % kRing);
+        double* xb = xbuf + (k & 1) * CH;
+        bulk_wait_read<1>();   // the store of chunk k-2 has read this buffer
         mbar_wait(sm.mbar + slot, (mbph >> slot) & 1u);
         mbph ^= 1u << slot;
         const double* Fs = ring + (int64_t)slot * 5 * CH;
@@ -465,7 +471,7 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
         for (int u = cnt - 1; u >= top; u--) {
             const double2 bc = *reinterpret_cast<const double2*>(Fs + u * 4 + 2);
             const double xi = fma(-bc.x, x1, fma(-bc.y, x2, Ts[u]));
-            __stcg(x + lo + u, xi);
+            xb[u] = xi;
             x2 = x1;
             x1 = xi;
         }
@@ -487,10 +493,16 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
             }
 #pragma unroll
             for (int u = 0; u < 16; u += 2)
-                __stcg(reinterpret_cast<double2*>(x + lo + u0 + u), make_double2(xv[u], xv[u + 1]));
+                *reinterpret_cast<double2*>(xb + u0 + u) = make_double2(xv[u], xv[u + 1]);
         }
+        if (cnt & 1) xb[cnt] = 0.0;   // x[n] (padding of the last, odd chunk)
+        fence_proxy_async_smem();     // generic smem writes -> the bulk store
+        bulk_s2g(x + lo, xb, (uint32_t)((cnt + 1) & ~1) * 8u);
+        bulk_commit();
         if (k + kRing < C) issue(k + kRing);
     }
+    bulk_wait_all();
+    fence_proxy_async_global();   // the bulk-stored x before the group barrier's release
 }
 
 // Composition of the forward maps of CTAs 0..cnt-1 (S slots FA, FB), applied in CTA order, by
@@ -767,6 +779,7 @@ constexpr int kPfAhead = 0;              // wide stages prefetched into L2 beyon
 constexpr int64_t kRingD = (int64_t)kWStg * kWStgD > (int64_t)kNStg * kStgD ? (int64_t)kWStg * kWStgD
                                                                             : (int64_t)kNStg * kStgD;
 static_assert((int64_t)kNStg * kStgD + kSolveDoubles <= kRingD, "back-sweep ring after the narrow ring");
+static_assert(2 * CH <= 2 * RCH, "x staging of the back sweep in the row accumulators");
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
 
