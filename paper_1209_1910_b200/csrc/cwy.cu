@@ -94,9 +94,10 @@ __device__ __forceinline__ void part_rows_weighted(int64_t n, int64_t P, int r, 
                                                    int64_t C) {
     if (P <= kNarrowM) C = 0;
     const int64_t NB = (P + kPieceW - 1) / kPieceW;
-    auto cum = [P, C, NB](int64_t i) -> int64_t {
-        if (i <= P) return i * (i + 1) / 2 + C * (sum_floor_pw(i) + i);
-        return P * (P + 1) / 2 + C * (sum_floor_pw(P) + P) + (i - P) * (P + C * NB);
+    const int64_t base = P * (P + 1) / 2 + C * ((NB > 1 ? sum_floor_pw(P) : 0) + P);
+    auto cum = [P, C, NB, base](int64_t i) -> int64_t {
+        if (i <= P) return i * (i + 1) / 2 + C * ((NB > 1 ? sum_floor_pw(i) : 0) + i);   // one block: 1 piece per row
+        return base + (i - P) * (P + C * NB);
     };
     int64_t W = cum(n);
     a = (r == 0) ? 0 : bsearch_cum(0, n, (W * r) / G, cum);
@@ -110,7 +111,8 @@ __device__ __forceinline__ void part_uniform(int64_t lo, int64_t hi, int r, int 
 // k in [0,p): packed column k of T has k+1 elements in floor(k / kPieceW) + 1 pieces
 __device__ __forceinline__ void part_tt(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C) {
     if (p <= kNarrowM) C = 0;
-    auto cum = [C](int64_t k) -> int64_t { return k * (k + 1) / 2 + C * (sum_floor_pw(k) + k); };
+    const bool multi = p > kPieceW;
+    auto cum = [C, multi](int64_t k) -> int64_t { return k * (k + 1) / 2 + C * ((multi ? sum_floor_pw(k) : 0) + k); };
     int64_t W = cum(p);
     a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
     b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
@@ -119,7 +121,9 @@ __device__ __forceinline__ void part_tt(int64_t p, int r, int G, int64_t& a, int
 __device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C) {
     if (p <= kNarrowM) C = 0;
     const int64_t NB = (p + kPieceW - 1) / kPieceW;
-    auto cum = [p, C, NB](int64_t l) -> int64_t { return l * p - l * (l - 1) / 2 + C * (l * NB - sum_floor_pw(l)); };
+    auto cum = [p, C, NB](int64_t l) -> int64_t {
+        return l * p - l * (l - 1) / 2 + C * (l * NB - (NB > 1 ? sum_floor_pw(l) : 0));
+    };
     int64_t W = cum(p);
     a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
     b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
