@@ -28,6 +28,14 @@
 
 namespace tinv {
 
+// Debug timers of the wide kernel (per-CTA busy times, vector windows; TINV_PROF_CTA,
+// TINV_PROF_P0/P1): compiled in only with -DTINV_WIDE_DEBUG (`make EXTRA=-DTINV_WIDE_DEBUG`),
+// since even their untaken branches cost ~3% on cfg3's short phases.
+#ifdef TINV_WIDE_DEBUG
+constexpr bool kWideDebug = true;
+#else
+constexpr bool kWideDebug = false;
+#endif
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int CFCH = 2048;   // rows whose coefficients are staged in shared memory at once
@@ -1198,7 +1206,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     unsigned int bar_epoch = 0;
     // debug (TINV_PROF_CTA): this CTA's busy time before each barrier, attributed to the
     // phase that the next mark() closes
-    const bool ctime = (a.prof_cta != nullptr) && tid == 0;
+    const bool ctime = kWideDebug && (a.prof_cta != nullptr) && tid == 0;
     uint64_t c_last = ctime ? gtime() : 0, c_busy = 0;
     auto gsync = [&]() {
         if (ctime) c_busy += gtime() - c_last;
@@ -1278,7 +1286,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         bool la_have = false;   // look-ahead of this vector's first pass A is ready
         for (int64_t p = 1; p < m; p++) {
             const int64_t j = j1 + p;
-            inwin = p >= a.prof_p0 && p < a.prof_p1;
+            inwin = !kWideDebug || (p >= a.prof_p0 && p < a.prof_p1);
             const double* xcur = a.X1c + j * n2v;   // x^(1), contiguous copy
             int64_t xs = 1;
             int its = 1, kin = 1, passes = 0, restart = 0;

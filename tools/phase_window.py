@@ -1,6 +1,7 @@
 """Per-phase cost of the wide compact-WY kernel for the vectors j_c in a window (TINV_PROF_P0/P1):
 microseconds per iteration of each phase next to the rate its paper-sequence bytes imply.
-Usage: python tools/phase_window.py cfg4 [p0:p1 ...]"""
+Usage: python tools/phase_window.py cfg4 [p0:p1 ...]
+The windows and TINV_PROF_CTA need a debug build: make -C paper_1209_1910_b200/csrc -B EXTRA=-DTINV_WIDE_DEBUG"""
 import os
 import sys
 
