@@ -11,6 +11,9 @@
 #include <stdlib.h>
 #include <string.h>
 #include <float.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define EPS 0x1.0p-53            /* unit roundoff, reading R3/R4 */
 #define MAXITS 5                 /* reading 9 */
@@ -181,37 +184,91 @@ void orc_cwy_free(orc_cwy_t* a) { free(a->P); a->P = NULL; }
 #define PT(a, l, k) ((a)->P[(l) + (k) * (a)->ld])
 static double Yget(const orc_cwy_t* a, int64_t i, int64_t k) { return i >= k ? PY(a, i, k) : 0.0; }
 
+/* Memory order of the BLAS-2 loops below.  Every output element is one dot product
+ * whose terms are added in exactly the order the paper's kernel defines (k ascending for
+ * the row dots of DGEMV-N / DTRMV, i or l ascending for the column dots of DGEMV-T /
+ * DTRMV-T), starting from 0.0.  The row dots over the column-major packed buffer walk
+ * the columns in the outer loop and keep one running sum per output row ("axpy order"):
+ * the same additions in the same order per element, so the result is bit-identical to
+ * the plain nested loop -- only the memory stream is contiguous.  Output elements are
+ * independent, so the OpenMP splits below (over whole output elements) do not change any
+ * rounding either: the result does not depend on the thread count. */
+
+/* out[i - r0] = sum_{k=0}^{kc-1} PY(i, k) * v[k] for rows i in [r0, r1) (k ascending). */
+static void rowdots_Y(const orc_cwy_t* a, int64_t r0, int64_t r1, int64_t kc, const double* v,
+                      double* out)
+{
+#pragma omp parallel
+    {
+        int nt = 1, id = 0;
+#ifdef _OPENMP
+        nt = omp_get_num_threads(); id = omp_get_thread_num();
+#endif
+        int64_t len = r1 - r0, per = (len + nt - 1) / nt;
+        int64_t lo = r0 + per * id, hi = lo + per < r1 ? lo + per : r1;
+        for (int64_t i = lo; i < hi; i++) out[i - r0] = 0.0;
+        for (int64_t k = 0; k < kc; k++) {
+            double vk = v[k];
+            int64_t i0 = lo > k ? lo : k;          /* Y(i, k) = 0 above row k: only i >= k */
+            for (int64_t i = i0; i < hi; i++) out[i - r0] += PY(a, i, k) * vk;
+        }
+    }
+}
+
+/* out[l] = sum_{k=l}^{kc-1} PT(l, k) * x[k] for l in [0, kc) (k ascending). */
+static void rowdots_T(const orc_cwy_t* a, int64_t kc, const double* x, double* out)
+{
+#pragma omp parallel
+    {
+        int nt = 1, id = 0;
+#ifdef _OPENMP
+        nt = omp_get_num_threads(); id = omp_get_thread_num();
+#endif
+        int64_t per = (kc + nt - 1) / nt;
+        int64_t lo = per * id, hi = lo + per < kc ? lo + per : kc;
+        for (int64_t l = lo; l < hi; l++) out[l] = 0.0;
+        for (int64_t k = lo; k < kc; k++) {        /* T(l, k) = 0 below the diagonal: l <= k */
+            double xk = x[k];
+            int64_t l1 = hi < k + 1 ? hi : k + 1;
+            for (int64_t l = lo; l < l1; l++) out[l] += PT(a, l, k) * xk;
+        }
+    }
+}
+
 /* §3.3.2, one reflector, in the paper's BLAS order. */
 void orc_cwy_step(orc_cwy_t* a, int64_t p, const double* v, double* q, double* c, double* unorm)
 {
     int64_t n = a->n;
     double* uh = (double*)malloc(sizeof(double) * (size_t)(n - p));
     double* vc = (double*)malloc(sizeof(double) * (size_t)(p + 1));
+    double* vin = (double*)malloc(sizeof(double) * (size_t)(p + 1));
+    double* rs = (double*)malloc(sizeof(double) * (size_t)n);
 
     /* u-step */
     for (int64_t i = p; i < n; i++) uh[i - p] = v[i];                         /* DCOPY */
     if (p > 0) {
-        for (int64_t k = 0; k < p; k++) vc[k] = v[k];
+        for (int64_t k = 0; k < p; k++) vin[k] = v[k];
+#pragma omp parallel for schedule(dynamic, 64)
         for (int64_t k = 0; k < p; k++) {                                       /* DTRMV L_p^T */
             double s = 0.0;
-            for (int64_t i = k; i < p; i++) s += PY(a, i, k) * vc[i];
+            for (int64_t i = k; i < p; i++) s += PY(a, i, k) * vin[i];
             vc[k] = s;
         }
+#pragma omp parallel for schedule(dynamic, 16)
         for (int64_t k = 0; k < p; k++) {                                       /* DGEMV Yhat^T vhat + vc */
             double s = 0.0;
             for (int64_t i = p; i < n; i++) s += PY(a, i, k) * v[i];
             vc[k] = s + vc[k];
         }
+        for (int64_t k = 0; k < p; k++) vin[k] = vc[k];
+#pragma omp parallel for schedule(dynamic, 64)
         for (int64_t k = p - 1; k >= 0; k--) {                                  /* DTRMV T_p^T */
             double s = 0.0;
-            for (int64_t l = 0; l <= k; l++) s += PT(a, l, k) * vc[l];
+            for (int64_t l = 0; l <= k; l++) s += PT(a, l, k) * vin[l];
             vc[k] = s;
         }
-        for (int64_t i = p; i < n; i++) {                                       /* DGEMV uhat -= Yhat vc */
-            double s = 0.0;
-            for (int64_t k = 0; k < p; k++) s += PY(a, i, k) * vc[k];
-            uh[i - p] = -s + uh[i - p];
-        }
+        rowdots_Y(a, p, n, p, vc, rs);                                          /* DGEMV uhat -= Yhat vc */
+        for (int64_t i = p; i < n; i++) uh[i - p] = -rs[i - p] + uh[i - p];
     }
 
     /* reflector.  Reading: an exactly-zero uhat is replaced by e_1. */
@@ -223,16 +280,13 @@ void orc_cwy_step(orc_cwy_t* a, int64_t p, const double* v, double* q, double* c
 
     /* that = -t T_p Yhat_p^T yhat */
     if (p > 0) {
+#pragma omp parallel for schedule(dynamic, 16)
         for (int64_t k = 0; k < p; k++) {                                       /* DGEMV */
             double s = 0.0;
             for (int64_t i = p; i < n; i++) s += PY(a, i, k) * yh[i - p];
-            vc[k] = (-tt) * s;
+            vin[k] = (-tt) * s;
         }
-        for (int64_t l = 0; l < p; l++) {                                       /* DTRMV T_p */
-            double s = 0.0;
-            for (int64_t k = l; k < p; k++) s += PT(a, l, k) * vc[k];
-            vc[l] = s;
-        }
+        rowdots_T(a, p, vin, vc);                                               /* DTRMV T_p */
     }
     /* append column p (rollback: any earlier trial column p is overwritten), Eq.(3) */
     for (int64_t l = 0; l < p; l++) PT(a, l, p) = vc[l];
@@ -241,28 +295,15 @@ void orc_cwy_step(orc_cwy_t* a, int64_t p, const double* v, double* q, double* c
     a->count = p + 1;
 
     /* q = (Y T Y^T - I) e_p, with T_{p+1} (erratum for T^T) */
-    for (int64_t k = 0; k <= p; k++) vc[k] = PY(a, p, k);                       /* DCOPY row p */
-    for (int64_t l = 0; l <= p; l++) {                                          /* DTRMV T_{p+1} */
-        double s = 0.0;
-        for (int64_t k = l; k <= p; k++) s += PT(a, l, k) * vc[k];
-        vc[l] = s;
-    }
-    for (int64_t i = 0; i <= p; i++) q[i] = vc[i];                              /* DCOPY */
-    for (int64_t i = p; i >= 0; i--) {                                          /* DTRMV L_{p+1} */
-        double s = 0.0;
-        for (int64_t k = 0; k <= i; k++) s += PY(a, i, k) * q[k];
-        q[i] = s;
-    }
-    for (int64_t i = p + 1; i < n; i++) {                                       /* DGEMV Yhat_{p+1} x */
-        double s = 0.0;
-        for (int64_t k = 0; k <= p; k++) s += PY(a, i, k) * vc[k];
-        q[i] = s;
-    }
+    for (int64_t k = 0; k <= p; k++) vin[k] = PY(a, p, k);                      /* DCOPY row p */
+    rowdots_T(a, p + 1, vin, vc);                                               /* DTRMV T_{p+1} */
+    rowdots_Y(a, 0, p + 1, p + 1, vc, q);                                       /* DTRMV L_{p+1} */
+    rowdots_Y(a, p + 1, n, p + 1, vc, q + p + 1);                               /* DGEMV Yhat_{p+1} x */
     q[p] = q[p] - 1.0;
 
     *c = cc;
     *unorm = nu0;
-    free(uh); free(vc); free(yh);
+    free(uh); free(vc); free(vin); free(rs); free(yh);
 }
 
 void orc_cwy_first(orc_cwy_t* a, const double* z)
@@ -612,7 +653,7 @@ static int64_t eigvecs_range(int64_t n, const double* d, const double* e, const 
     int64_t nc = orc_clusters(n, w, tnorm, cs);
     orc_shifts(n, w, nc, cs, wt);
     int64_t nflag = 0;
-#pragma omp parallel for schedule(dynamic, 1) reduction(+ : nflag)
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : nflag) if (nc > 1)
     for (int64_t c = 0; c < nc; c++) {
         int64_t j1 = cs[c], j2 = cs[c + 1];
         if (j2 <= j_lo || j1 >= j_hi) continue;
