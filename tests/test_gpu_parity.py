@@ -99,7 +99,29 @@ def test_cfg1_laplacian_full(handle, torch):
             if a[-2] < a[-1] * (1 - 1e-8):
                 assert np.abs(Zg[:, s] - Zo[:, s]).max() <= TOL_VEC
                 nsame += 1
-    assert nsame >= 0
+    # (every Laplacian vector has mirror-image maxima |v_i| = |v_{n+1-i}|, so nsame is 0 here;
+    # the sign rule itself is checked on cfg2 below, where the maxima are unique)
+    assert nsame == 0
+    big = np.abs(Zg).max(axis=0)
+    assert (Zg.max(axis=0) >= big * (1 - 1e-12)).all()       # a largest-|entry| is positive
+
+
+def test_sign_rule_identity_cfg2(handle, torch):
+    """Reading 15: with a unique largest |entry| the canonical sign makes determined vectors
+    identical (no sign freedom): every P3-isolated vector of cfg2 (n = 2000) whose top two
+    |entries| differ by more than 1e-8 relative matches the oracle without a sign flip."""
+    d, e, w = W.problem("cfg2")
+    Zg, Zo, rep = full_parity(handle, torch, d, e, w)
+    tn = O.tnorm(d, e)
+    nsame = niso = 0
+    for s, t in groups(w, 1e-6 * tn):
+        if t - s == 1:
+            niso += 1
+            a = np.sort(np.abs(Zo[:, s]))
+            if a[-2] < a[-1] * (1 - 1e-8):
+                assert np.abs(Zg[:, s] - Zo[:, s]).max() <= TOL_VEC
+                nsame += 1
+    assert niso >= 1900 and nsame >= 0.95 * niso, (niso, nsame)
 
 
 def test_cfg2_random_full(handle, torch):
@@ -182,6 +204,64 @@ def test_exact_duplicates(handle, torch):
     # two identical decoupled W21+ blocks: every eigenvalue exactly duplicated
     d, e = W.glued_wilkinson(2, 0.0)
     full_parity(handle, torch, d, e, W.eigenvalues(d, e))
+
+
+def _iters_of(handle):
+    return handle.stats()["iters_hist"]
+
+
+def test_restart_branch(handle, torch):
+    """Reading 16 on the device: T = diag(1, 2), w = [1, 1] (one cluster of 2).  The second
+    vector's first iterate lies in span(z_0): the compact-WY step restarts it with the start
+    vector of restart 1.  Same Z (= I up to rounding), return code and iteration counts as
+    the oracle (test_oracle.py::test_restart_branch_closed_form pins the oracle)."""
+    d, e, w = np.array([1.0, 2.0]), np.array([0.0]), np.array([1.0, 1.0])
+    Zg, rc = run_gpu(handle, torch, d, e, w)
+    Zo, info, its = O.eigvecs(d, e, w, seed=1, return_iters=True)
+    assert rc == info == 0
+    assert np.abs(Zg.cpu().numpy() - Zo).max() <= 1e-14
+    assert np.abs(Zg.cpu().numpy() - np.eye(2)).max() <= 1e-14
+    hist = _iters_of(handle)
+    assert hist == list(np.bincount(its, minlength=8)[:8]), (hist, its)
+
+
+def test_restart_exhausted_inside_larger_cluster(handle, torch):
+    """Restarts in a wider cluster, run on the resident (narrow) kernel and on the persistent
+    one: T = diag(1, 200, 300, 400, 500, 600) with three shifts on eigenvalue 1.  Vector 1's
+    iterates stay in span(z_0) (the other components are damped by ~1/200 against 1/(10 eps)),
+    so it restarts twice, then is kept and flagged (reading 16: rc = 1); vector 2 is accepted.
+    Same Z, rc and iteration histogram as the oracle."""
+    d = np.array([1.0, 200.0, 300.0, 400.0, 500.0, 600.0])
+    e = np.zeros(5)
+    w = np.array([1.0, 1.0, 1.0, 400.0, 500.0, 600.0])
+    Zo, info, its = O.eigvecs(d, e, w, seed=1, return_iters=True)
+    assert info == 1 and its[1] > 2, (info, its)          # the oracle restarts and flags
+    for resident in (True, False):
+        handle.set_resident(resident)
+        try:
+            Zg, rc = run_gpu(handle, torch, d, e, w)
+            hist = _iters_of(handle)
+        finally:
+            handle.set_resident(True)
+        assert rc == info, (resident, rc, info)
+        assert np.abs(Zg.cpu().numpy() - Zo).max() <= 1e-10, resident
+        assert hist == list(np.bincount(its, minlength=8)[:8]), (resident, hist, its)
+
+
+def test_maxits_flag(handle, torch):
+    """Readings 9/17 on the device: tiny-scale diagonal T with shifts far from every eigenvalue
+    (the oracle pin test_maxits_flag_closed_form proves no iterate can pass the growth test):
+    every vector runs MAXITS = 5 iterations and is counted in the return code; the kept
+    iterates equal the oracle's."""
+    s = 1e-20
+    d = s * np.array([1.0, 3.0, 5.0, 5.002, 5.004])
+    e = np.zeros(4)
+    w = s * np.array([2.0, 3.6, 6.0, 6.0 + 1e-6, 6.0 + 2e-6])
+    Zo, info, its = O.eigvecs(d, e, w, seed=1, return_iters=True)
+    Zg, rc = run_gpu(handle, torch, d, e, w)
+    assert info == 5 and rc == 5, (rc, info)
+    assert _iters_of(handle)[5] == 5
+    assert np.abs(Zg.cpu().numpy() - Zo).max() <= 1e-10
 
 
 def test_invalid_arguments(handle, torch):

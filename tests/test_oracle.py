@@ -106,6 +106,17 @@ def test_start_vector_range_and_independence():
     assert not np.array_equal(b, O.start_vector(1000, 2, 7))
 
 
+def test_start_vector_golden_table():
+    """Reading 7's (seed, n, j, restart, i) -> value mapping, including the counter layout and
+    the top-53-bit conversion, against the table written by tests/golden/make_start_vectors.py
+    (plain Python integers, independent of oracle.c)."""
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "start_vectors.txt")) if l.strip() and not l.startswith("#")]
+    assert len(rows) >= 30
+    for seed, n, j, r, i, v in rows:
+        b = O.start_vector(int(n), int(seed), int(j), restart=int(r))
+        assert b[int(i)] == float.fromhex(v), (seed, n, j, r, i)
+
+
 # ------------------------------------------------------------------ LU (Eq. 1 solver)
 
 def test_lu_spec_examples():
@@ -466,3 +477,41 @@ def test_eigvecs_mgs_invariants_and_range(cfg, n):
     assert residual_units_tridiag(d, e, w, Z) <= 10 and orth_units(Z) <= 10
     Zr, _ = O.eigvecs(d, e, w, seed=1, j_lo=40, j_hi=110, mgs=True)
     assert np.array_equal(Zr, Z[:, 40:110])
+
+
+# ------------------------------------------------------------------ silent branches (readings 9, 16, 17)
+
+def test_restart_branch_closed_form():
+    """Reading 16 (PAPER.md:681-716 is silent on an iterate inside the accepted span): with
+    T = diag(1, 2) and the (wrong) input w = [1, 1], both shifts sit on eigenvalue 1 and form
+    one cluster.  The second vector's first iterate lies in span(e_1) = span(z_1) up to
+    rounding, so ||uhat|| <= n eps ||x|| triggers a restart; the restarted iterate is
+    reorthogonalised to the complement.  Closed form: z_0 = e_1, z_1 = e_2 (the only unit
+    vectors orthogonal to each other with z_0 the eigenvector for shift 1); the restart
+    shows in the iteration count (> 2 = one restart plus 2 passes)."""
+    Z, info, its = O.eigvecs(np.array([1.0, 2.0]), np.array([0.0]), np.array([1.0, 1.0]), seed=1,
+                             return_iters=True)
+    assert info == 0
+    assert np.abs(Z - np.eye(2)).max() <= 1e-15
+    assert its[0] == 2 and its[1] > 2, its
+
+
+def test_maxits_flag_closed_form():
+    """Readings 9 and 17: a vector that never passes the growth test in MAXITS = 5 iterations is
+    kept and counted in the return value.  T = 1e-20 diag(1, 3, 5, 5.002, 5.004) with shifts at
+    distance >= 0.5e-20 from every eigenvalue (a singleton and a 1e-3 ||T||_1 cluster of 3 +
+    one more singleton): for a diagonal T the solve is x_i = sigma b_i / (d_i - w), and
+    sigma = n ||T||_1 max(eps, |u_nn|) / ||b||_1 = n ||T||_1 eps / ||b||_1 since |u_nn| < eps,
+    so ||x||_inf <= n ||T||_1 eps / 0.5e-20 = 5 * 5.004 * 2 eps < sqrt(0.1 / n) on every
+    iteration (the cWY iterate c q has norm <= ||x||): no vector ever counts a pass."""
+    s = 1e-20
+    d = s * np.array([1.0, 3.0, 5.0, 5.002, 5.004])
+    e = np.zeros(4)
+    w = s * np.array([2.0, 3.6, 6.0, 6.0 + 1e-6, 6.0 + 2e-6])
+    cs = O.clusters(w, O.tnorm(d, e))
+    assert list(cs) == [0, 1, 2, 5]                    # singleton, singleton, cluster of 3
+    Z, info, its = O.eigvecs(d, e, w, seed=1, return_iters=True)
+    assert info == 5, info
+    assert (its == 5).all(), its                      # MAXITS, no restart
+    assert np.isfinite(Z).all()
+    assert np.allclose(np.linalg.norm(Z, axis=0), 1.0, atol=1e-14)
