@@ -108,7 +108,10 @@ int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, con
  * memory of nclus + 1 and nranks entries. */
 int tinv_partition(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi);
 
-/* Release the handle and its device workspace. */
+/* Release the handle and its device workspace.  With nranks > 1 and a previous row-split
+ * call (peers hold CUDA IPC mappings of this rank's workspace) it is collective: every rank
+ * must call it, so that all mappings are closed (and a barrier passed) before any rank frees
+ * its exported memory. */
 int tinv_destroy(tinv_t h);
 
 /* Human-readable text of a return code (static storage). */
@@ -131,7 +134,8 @@ typedef struct {
     int64_t ngroups;            /* CTA groups used by the cWY kernel                  */
     int64_t cwy_ctas;           /* CTAs of the cWY kernel                             */
     int64_t resident_groups;    /* launches of the resident (DSMEM) cWY kernel        */
-    double  reorth_bytes;       /* algorithmic bytes of the cWY passes    */
+    double  reorth_bytes;       /* algorithmic bytes of the cWY passes, from the
+                                   call's iteration counts (computed when the stats are read) */
     double  solve_bytes;        /* algorithmic bytes of the batched LU kernel         */
     double  kernel_ms[TINV_NKERNELS];     /* prep, batched_lu, finalize, cwy, misc, total */
     int64_t kernel_launches[TINV_NKERNELS];

@@ -16,6 +16,8 @@
 // fed by a per-warp cp.async pipeline: NS stages of RB rows x 256 B per array in shared
 // memory, so ~NS*RB rows are in flight per lane while the lane runs its serial recurrence
 // (one FMA per row on the dependent chain: row-normalised U, alpha/beta forward form).
+#include <type_traits>
+
 #include "common.cuh"
 #include "tinv_internal.h"
 
@@ -98,6 +100,10 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
     double tiny = kEps * tnorm;
     if (tiny == 0.0) tiny = 2.2250738585072014e-308;
     const double thr = sqrt(0.1 / (double)n);
+    // rcp.approx.ftz flushes subnormal arguments and results: the pivots lie in
+    // [eps ||T||_1, ~2 ||T||_1], so outside this range of ||T||_1 the factor sweep takes the
+    // IEEE division instead (uniform over the grid)
+    const bool exact_rcp = !(tnorm > 0x1p-960 && tnorm < 0x1p1000);
     // this warp's block of rows (block-row layout over slots, common.cuh bix)
     const int64_t boff = (int64_t)blockIdx.x * n * 32;
     double* __restrict__ X = a.X + boff;
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
           double* pFC = FC + i0 * 32 + lane;
           double* pX = X + i0 * 32 + lane;
           int8_t* pFP = FPv + i0 * 32 + lane;
-          auto row = [&](int rr) {
+          auto row = [&](int rr, auto exact) {
             const int64_t i = i0 + rr;
             const double sub = pe[rr];
             const double anext = pd[rr] - shift;
@@ -204,7 +210,9 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
             // one reciprocal per row on the dependent chain (l = other * (1/pivot))
             const bool swp = fabs(sub) > fabs(pp);
             u0 = pivot_floor(swp ? sub : pp, tiny);
-            const double r = rcp_pivot(u0);
+            double r;
+            if constexpr (decltype(exact)::value) r = 1.0 / u0;   // IEEE (subnormal-safe)
+            else r = rcp_pivot(u0);
             l = (swp ? pp : sub) * r;
             if (swp) {
                 u1 = anext;
@@ -231,11 +239,13 @@ __global__ void __launch_bounds__(64) batched_lu_kernel(BatchedArgs a) {
             __stcg(pFC + o, u2 * r);
             __stcg(pX + o, y);
           };
-          if (cnt == RR) {
+          if (exact_rcp) {   // ||T||_1 outside [2^-960, 2^1000]: pivots may leave the normal range
+            for (int rr = 0; rr < cnt; rr++) row(rr, std::true_type{});
+          } else if (cnt == RR) {
 #pragma unroll 8
-            for (int rr = 0; rr < RR; rr++) row(rr);
+            for (int rr = 0; rr < RR; rr++) row(rr, std::false_type{});
           } else {
-            for (int rr = 0; rr < cnt; rr++) row(rr);
+            for (int rr = 0; rr < cnt; rr++) row(rr, std::false_type{});
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(rempty + slot);

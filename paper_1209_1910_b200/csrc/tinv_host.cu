@@ -88,6 +88,7 @@ struct tinv_s {
     int* h_iters = nullptr;
     int64_t h_cap = 0;
     int64_t iters_n = 0;              // > 0: the last call's iteration counts not yet read back
+    int rb_clo = 0, rb_chi = 0;       // cluster range whose cWY bytes the stats report (this rank's)
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
@@ -105,6 +106,7 @@ struct tinv_s {
     std::vector<void*> peer_cw;       // per rank (nullptr for self)
     std::vector<char> peer_hdl;       // the IPC handles the mappings were opened from
     void* ipc_buf = nullptr;          // device staging for the handle allgather / barrier
+    bool exported = false;            // peers hold IPC mappings of our cw (a row-split call ran)
     // pinned image of the cWY schedule header
     void* h_hdr = nullptr;
     size_t h_hdr_bytes = 0;
@@ -153,6 +155,10 @@ struct Carve {
 
 int ensure_base(tinv_s* h, int64_t n) {
     if (n <= h->ncap) return 0;
+    // the capacity is zero until the new allocation succeeded: a failed cudaMalloc leaves no
+    // handle state that a later, smaller call could mistake for a valid workspace
+    h->ncap = 0;
+    h->ldv = 0;
     if (h->base) { cudaFree(h->base); h->base = nullptr; }
     int64_t ldv = (n + 31) / 32 * 32;
     auto layout = [&](char* p) {
@@ -322,6 +328,23 @@ int map_peers(tinv_s* h, cudaStream_t st) {
     return 0;
 }
 
+// Close every peer mapping, then a collective barrier (an NCCL all-reduce, completed on the
+// host): on return no rank holds a mapping of any other rank's workspace, so each may free its
+// own (CUDA IPC: an exported allocation must not be freed while an importer has it open).
+// Collective: every rank calls it at the same point (tinv_eigvecs calls are collective and the
+// decision to call it depends only on the identical cluster table).
+int unmap_peers_collective(tinv_s* h, cudaStream_t st) {
+    for (auto& pp : h->peer_cw)
+        if (pp) { cudaIpcCloseMemHandle(pp); pp = nullptr; }
+    std::fill(h->peer_hdl.begin(), h->peer_hdl.end(), 0);
+    if (h->comm && h->ipc_buf) {
+        if (g_nccl.allReduce(h->ipc_buf, h->ipc_buf, 1, ncclUint8, ncclSum, h->comm, st)) return TINV_ERR_NCCL;
+        CK(cudaStreamSynchronize(st));
+    }
+    h->exported = false;
+    return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -416,6 +439,9 @@ int tinv_destroy(tinv_t h) {
     if (!h) return TINV_ERR_HANDLE;
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
+    // collective with nranks > 1 (include/tinv.h): no rank frees an exported workspace while a
+    // peer still has it mapped
+    if (h->nranks > 1 && h->exported) unmap_peers_collective(h, h->stream);
     if (h->comm) g_nccl.commDestroy(h->comm);
     if (h->base) cudaFree(h->base);
     if (h->cw) cudaFree(h->cw);
@@ -476,6 +502,19 @@ int tinv_get_stats(tinv_t h, tinv_stats_t* out) {
         CK(cudaMemcpy(h->h_iters, h->iters, sizeof(int) * h->iters_n, cudaMemcpyDeviceToHost));
         for (int k = 0; k < 8; k++) h->stats.iters_hist[k] = 0;
         for (int64_t j = 0; j < h->iters_n; j++) h->stats.iters_hist[std::min(7, std::max(0, h->h_iters[j]))]++;
+        // algorithmic bytes of the compact-WY work (paper kernel sequence
+        // PAPER.md:530-623): one cWY step of vector j_c = p reads 8 (4 p n - 1.5 p^2) bytes;
+        // every iteration of a clustered vector runs one step.  Needs this call's iteration
+        // counts, hence computed here, after the read-back (h_cstart still holds this call's
+        // cluster table: it is only rewritten by the next call).
+        const double nd = (double)h->stats.n;
+        double rb = 0.0;
+        for (int c = h->rb_clo; c < h->rb_chi; c++)
+            for (int64_t j = h->h_cstart[c] + 1; j < h->h_cstart[c + 1]; j++) {
+                const double p = (double)(j - h->h_cstart[c]);
+                rb += (double)h->h_iters[j] * 8.0 * (4.0 * p * nd - 1.5 * p * p);
+            }
+        h->stats.reorth_bytes = rb;
         h->iters_n = 0;
     }
     *out = h->stats;
@@ -618,6 +657,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const bool rs_real = h->nranks > 1 && wide1;
     const int NRK = rs_real ? h->nranks : ((h->nranks == 1 && h->vranks > 1 && wide1) ? h->vranks : 1);
     const bool rs_virtual = !rs_real && NRK > 1;
+    // a previous call row-split (peers mapped our workspace); this one shards by columns, so the
+    // ranks' workspace sizes may diverge: release the mappings collectively first
+    if (h->nranks > 1 && h->exported && !rs_real)
+        if (int rc = unmap_peers_collective(h, st)) { join_b2(); return rc; }
     // Narrow clusters whose rows fit in the shared memory of 1..8 CTAs run in the resident
     // kernel (one thread-block cluster per eigen-cluster, Y in distributed shared memory);
     // the rest in the persistent kernel.
@@ -673,7 +716,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     Schedule sc = rs_real ? make_schedule(cs, 0, nclus, n, nctas_max)
                           : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max, &resident);
     if (rs_virtual && sc.size.size() == 1) {   // split the group into NRK equal virtual ranks
-        const int Gv = sc.size[0] / NRK;
+        const int Gv = std::max(1, sc.size[0] / NRK);   // >= 1 CTA per virtual rank (small clusters)
         const int cl = sc.clist[0];
         const int64_t mc = sc.mcap[0];
         sc = Schedule{};
@@ -920,6 +963,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         GroupWS* dws;
         size_t need = layout(nullptr, ws, arrs, &syncs, &dws);
         if (need > h->cw_bytes) {
+            // row split: every rank grows here at the same call (identical schedules); peers'
+            // mappings of the old allocation are closed collectively before it is freed
+            if (rs_real && h->exported)
+                if (int rc = unmap_peers_collective(h, st)) return rc;
             if (h->cw) cudaFree(h->cw);
             h->cw = nullptr;
             h->cw_bytes = 0;
@@ -956,6 +1003,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                         for (int k = 0; k < RG; k++) dv[(size_t)g * RG + k] = ws[k].Y - ws[g].Y;
                 } else {
                     if (int rc = map_peers(h, st)) return rc;
+                    h->exported = true;
                     for (int k = 0; k < RG; k++)
                         dv[k] = (k == h->rank) ? 0 : ((char*)h->peer_cw[k] - (char*)h->cw) / 8;
                 }
@@ -1074,21 +1122,9 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
-    h->iters_n = n;   // iters_hist: read back lazily by tinv_get_stats
-    // algorithmic bytes of the compact-WY work (paper kernel sequence
-    // PAPER.md:530-623): one cWY step of vector j_c = p reads 8 (4 p n - 1.5 p^2) bytes;
-    // every iteration of a clustered vector runs one step.
-    {
-        double rb = 0.0;
-        const int c_lo = rs_real ? 0 : rlo[h->rank], c_hi = rs_real ? nclus : rhi[h->rank];
-        for (int c = c_lo; c < c_hi; c++) {
-            for (int64_t j = cs[c] + 1; j < cs[c + 1]; j++) {
-                double p = (double)(j - cs[c]);
-                rb += (double)h->h_iters[j] * 8.0 * (4.0 * p * (double)n - 1.5 * p * p);
-            }
-        }
-        S.reorth_bytes = rb;
-    }
+    h->iters_n = n;   // iters_hist and reorth_bytes: computed by tinv_get_stats after its read-back
+    h->rb_clo = rs_real ? 0 : rlo[h->rank];
+    h->rb_chi = rs_real ? nclus : rhi[h->rank];
     S.launches = launches;
     if (h->profiling) {
         float ms = 0.f;

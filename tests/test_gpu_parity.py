@@ -264,6 +264,26 @@ def test_maxits_flag(handle, torch):
     assert np.abs(Zg.cpu().numpy() - Zo).max() <= 1e-10
 
 
+@pytest.mark.parametrize("k", [-1000, -500, 300])
+@pytest.mark.parametrize("cfg,n", [("cfg2", 300), ("cfg3", 210), ("cfg4", 200)])
+def test_scaled_matrices(handle, torch, cfg, n, k):
+    """T, w scaled by 2^k (exact): the eigenvectors of 2^k T are those of T.  At 2^-1000 the
+    pivot floor eps ||T||_1 is subnormal (the factor sweep's approximate reciprocal flushes
+    subnormals, so it switches to IEEE division there).  Gates: the GPU returns the oracle's
+    code, the vectors satisfy the P0 invariants of the UNSCALED problem, and match the
+    oracle's run on the scaled input per vector / per subspace (P1-P3)."""
+    d, e, w = W.problem(cfg, n)
+    s = 2.0 ** k
+    ds, es, ws_ = d * s, e * s, w * s
+    Zg, rc = run_gpu(handle, torch, ds, es, ws_)
+    Zo, info = O.eigvecs(ds, es, ws_, seed=1)
+    assert rc == info == 0, (rc, info)
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0, (res, orth)
+    wv, wsig, _, _ = parity_report(w, O.tnorm(d, e), Zg.cpu().numpy(), Zo)
+    assert wv <= TOL_VEC and wsig >= 1 - TOL_SUB, (wv, wsig)
+
+
 def test_invalid_arguments(handle, torch):
     import ctypes as C
 
