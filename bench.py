@@ -2,15 +2,21 @@
 """Benchmark of the hot path: all n eigenvectors of a symmetric tridiagonal T by inverse
 iteration with compact-WY reorthogonalisation (DSTEIN-cWY, Alg. 4), fp64.
 
-Metric (BASELINE.json): eigenvectors/s (all n, fp64); one step = one tinv_eigvecs call on
-one synthetic input resident in HBM.  Default workload: configs[1] (cfg2, n = 2000 random
-tridiagonal).  Other configs: --config cfg1..cfg5.
+Metric (BASELINE.json): eigenvectors/s (all n, fp64) at n = 2000-16000; reorth HBM GB/s vs
+peak.  One step = one tinv_eigvecs call on one synthetic input resident in HBM.  Default
+workload: configs[3] (cfg4, n = 8000, one giant cluster): the HBM-bound regime the metric's
+"reorth HBM GB/s vs peak" half refers to.  Other configs: --config cfg1..cfg5 (cfg2 = the
+n = 2000 many-small-clusters, latency-bound case).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl tinv|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl tinv|reference]
 
-N > 1 is launched with torch.distributed.run (one process per GPU, NCCL): the clusters are
-sharded over the ranks (contiguous column ranges, no data-path collective) and each rank's
-columns are broadcast at the end, so the whole job computes one problem (strong scaling).
+--gpus N > 1 without a torch.distributed environment re-executes itself under
+torch.distributed.run (one process per GPU, NCCL, 127.0.0.1).  Multi-rank: a single giant
+cluster (cfg4, cfg5) is row-split over the ranks (in-kernel reductions over NVLink peer
+memory); otherwise the clusters are sharded by columns and each rank's columns broadcast at
+the end.  Either way the whole job computes one problem (strong scaling).
+The timed Z is checked on the device after the timed region (P0 invariants of
+BASELINE.json north_star); a violation prints the line with "parity.ok": false and exits 1.
 """
 from __future__ import annotations
 
@@ -36,6 +42,16 @@ WORKLOAD_DESC = {
     "cfg4": "n=8000 single giant cluster d=1+1e-7U, e=1e-9U (configs[3])",
     "cfg5": "n=16000 perturbed Laplacian 2+1e-6U(-1,1), -1 (configs[4])",
 }
+
+
+BIG = ("cfg4", "cfg5")          # one giant cluster: row split at N > 1, seconds per step
+
+
+def config_dict(args, n, ws):
+    """The workload description -- identical in both arms (no run-dependent keys)."""
+    par = "single GPU" if ws == 1 else (f"row-split x{ws}" if args.config in BIG else f"cluster-shard x{ws}")
+    return {"workload": WORKLOAD_DESC[args.config], "name": args.config, "n": n, "parallelism": par,
+            "reorth": args.reorth, "l2": "flushed between timed steps (256 MB write)", "seed": args.seed}
 
 
 def measured_peaks():
@@ -103,6 +119,8 @@ def reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
+    if ws > 1:   # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 alone works here: all host cores
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     import oracle as O
 
     d, e, w = W.problem(args.config)
@@ -124,7 +142,7 @@ def reference_arm(args):
         "impl": "reference", "metric": "eigenvectors/s (all n, fp64)", "value": value, "unit": "eigenvectors/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.config], "n": n, "name": args.config},
+        "config": config_dict(args, n, ws),
         "cpu_baseline": {"value": value, "unit": "eigenvectors/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "eigenvectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -156,6 +174,31 @@ def cpu_baseline(d, e, w, budget_s=12.0, mgs=False):
             "sample": f"first {k} of {n} eigenvectors (start of the single cluster; later vectors cost more), {dt:.1f} s"}
 
 
+def p0_check(torch, d, e, w, Zt, dev):
+    """P0 invariants (BASELINE.json north_star) of the timed result, on the device:
+    max_j ||T z_j - w_j z_j||_2 <= 10 n eps ||T||_1 and max |Z^T Z - I| <= 10 n eps.
+    Zt's row j is eigenvector j (column-major Z).  fp64 throughout (cuBLAS DGEMM for Z^T Z)."""
+    n = len(d)
+    eps = 2.0 ** -53
+    dt, wt = (torch.tensor(a, dtype=torch.float64, device=dev) for a in (d, w))
+    TZ = Zt * dt[None, :]
+    if n > 1:
+        et = torch.tensor(e, dtype=torch.float64, device=dev)
+        TZ[:, :-1] += Zt[:, 1:] * et[None, :]
+        TZ[:, 1:] += Zt[:, :-1] * et[None, :]
+    TZ -= Zt * wt[:, None]
+    tn = float(np.max(np.abs(d) + np.concatenate([[0.0], np.abs(e)]) + np.concatenate([np.abs(e), [0.0]])))
+    res = torch.linalg.vector_norm(TZ, dim=1).max().item() / (n * eps * tn)
+    del TZ
+    G = Zt @ Zt.t()
+    G.diagonal().sub_(1.0)
+    orth = G.abs().max().item() / (n * eps)
+    del G
+    ok = bool(res <= 10.0 and orth <= 10.0)
+    return {"ok": ok, "residual_n_eps_tnorm": res, "orth_n_eps": orth, "bound": 10.0,
+            "what": "P0 invariants of the last timed step's Z, on the device"}
+
+
 def e2e_leg(h, d, e, w, n, args, ws, dev, barrier):
     """The same metric through tinv_eigvecs_host with pinned host buffers: H2D of d, e, w and
     the columns of Z landing in host memory inside the timed region."""
@@ -166,7 +209,7 @@ def e2e_leg(h, d, e, w, n, args, ws, dev, barrier):
     hZ = torch.empty((n, n), dtype=torch.float64).pin_memory()
     h.eigvecs_host(hd, he, hw, Z=hZ, seed=args.seed)
     barrier()
-    e_steps = max(1, min(args.steps, 5))
+    e_steps = max(1, min(args.steps, 2 if args.config in BIG else 5))
     t0 = time.perf_counter()
     for _ in range(e_steps):
         h.eigvecs_host(hd, he, hw, Z=hZ, seed=args.seed)
@@ -185,9 +228,9 @@ def e2e_leg(h, d, e, w, n, args, ws, dev, barrier):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 5 for cfg4/cfg5, else 30)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=list(WORKLOAD_DESC))
+    ap.add_argument("--config", default="cfg4", choices=list(WORKLOAD_DESC))
     ap.add_argument("--impl", default="tinv", choices=["tinv", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -197,6 +240,23 @@ def main():
                          "(Alg. 1), the paper's comparison; ordinary: compact WY in the §3.3.1 sequence")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 5 if args.config in BIG else 30
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # honour --gpus N: one process per GPU under torch.distributed.run (127.0.0.1)
+        import socket
+        import subprocess
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return reference_arm(args)
     args.warmup = max(args.warmup, 3)
@@ -258,10 +318,11 @@ def main():
             launches += h.stats()["launches"]
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    parity = p0_check(torch, d, e, w, Zt, dev)     # the Z of the last timed step (untimed)
     # per-kernel breakdown and phase timers from separate profiled calls (the library's events
     # and host synchronisation would otherwise sit inside the timed steps)
     h.set_profiling(True)
-    for k in range(min(3, args.steps)):
+    for k in range(min(1 if args.config in BIG else 3, args.steps)):
         flush.fill_(float(k))
         h.eigvecs(dd, de, dw, Z=Zt, seed=args.seed)
         for kk, v in h.stats()["kernel_ms"].items():
@@ -294,14 +355,21 @@ def main():
             traffic = float(tr["bytes"])
     except Exception:
         traffic = None
-    roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": src,
-            "alg_bytes_per_launch": alg_bytes, "kernel_ms": avg[dom],
+    resident = dom == "cwy" and st.get("resident_groups", 0) > 0
+    kernel_name = {"cwy": "cwy_resident_kernel" if resident else "cwy_kernel (persistent, wide clusters)",
+                   "batched_lu": "batched_lu_kernel"}[dom]
+    roof = {"kernel": kernel_name, "bound": "latency" if resident else "hbm", "achieved": achieved,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+            "peak_source": src, "alg_bytes_per_launch": alg_bytes, "kernel_ms": avg[dom],
             "share_of_step": avg[dom] / ms_per_step if ms_per_step > 0 else None}
-    if dom == "cwy" and st.get("resident_groups", 0) > 0:
+    if traffic:
+        # measured DRAM bytes of the same kernel (committed ncu capture) over the same kernel time
+        roof["traffic_gbs"] = traffic / (avg[dom] * 1e-3) / 1e9
+        roof["traffic_frac"] = roof["traffic_gbs"] / peaks["hbm_gbs"]
+    if resident:
         roof["note"] = ("resident cWY kernel: Y stays in shared memory, so DRAM traffic is far below the "
                         "algorithmic bytes; the step is bound by the dependent chains and phase latencies "
-                        "(DESIGN.md section 8), not by HBM")
+                        "(DESIGN.md section 8), not by HBM: 'frac' is the algorithmic-byte rate over the HBM peak")
 
     # ---- e2e through the public API with host buffers (pinned)
     if args.no_e2e:
@@ -309,18 +377,13 @@ def main():
     else:
         e2e = e2e_leg(h, d, e, w, n, args, ws, dev, barrier)
 
-    # one wide cluster holds all the clustered vectors -> the library row-splits it over the
-    # ranks; otherwise clusters are sharded by columns
-    row_split = st["max_cluster"] > 64 and st["n_clustered"] == st["max_cluster"] - 1
-    parallelism = "single GPU" if ws == 1 else (f"row-split x{ws}" if row_split else f"cluster-shard x{ws}")
     line = {
         "metric": "eigenvectors/s (all n, fp64)", "value": value, "unit": "eigenvectors/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.config], "name": args.config, "n": n,
-                   "parallelism": parallelism, "reorth": args.reorth,
-                   "l2": "flushed between timed steps (256 MB write)", "seed": args.seed},
+        "config": config_dict(args, n, ws),
         "roofline": roof,
+        "parity": parity,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -331,12 +394,19 @@ def main():
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(d, e, w, mgs=args.reorth == "mgs")
+    ok = parity["ok"]
+    if ws > 1:
+        t = torch.tensor([0.0 if ok else 1.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ok = t.item() == 0.0
     if rank == 0:
         print(json.dumps(line))
+        if not ok:
+            print("bench.py: PARITY FAILURE (P0 invariants violated on the timed Z)", file=sys.stderr)
     h.close()
     if ws > 1:
         dist.destroy_process_group()
-    return 0
+    return 0 if ok else 1
 
 
 if __name__ == "__main__":
