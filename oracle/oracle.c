@@ -648,6 +648,23 @@ static int64_t eigvecs_range(int64_t n, const double* d, const double* e, const 
         }
         return 0;
     }
+    /* R0 (reading 21; the paper is silent on scaling): if ||T||_1 lies outside
+     * [2^-200, 2^200], T and w are multiplied by the power of two 2^k that brings ||T||_1 into
+     * [1, 2) -- exact, and 2^k T has the eigenvectors of T -- so that sigma (reading 8), the
+     * pivot floor and the iterates' norms stay in the normal floating-point range. */
+    double *dsc = NULL, *esc = NULL, *wsc = NULL;
+    if (!(tnorm >= 0x1p-200 && tnorm <= 0x1p200)) {
+        int ex;
+        frexp(tnorm, &ex);
+        const int k = 1 - ex;
+        dsc = (double*)malloc(sizeof(double) * (size_t)n);
+        esc = (double*)malloc(sizeof(double) * (size_t)n);
+        wsc = (double*)malloc(sizeof(double) * (size_t)n);
+        for (int64_t i = 0; i < n; i++) { dsc[i] = ldexp(d[i], k); wsc[i] = ldexp(w[i], k); }
+        for (int64_t i = 0; i + 1 < n; i++) esc[i] = ldexp(e[i], k);
+        d = dsc; e = esc; w = wsc;
+        tnorm = orc_tnorm(n, d, e);
+    }
     int64_t* cs = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
     double* wt = (double*)malloc(sizeof(double) * (size_t)n);
     int64_t nc = orc_clusters(n, w, tnorm, cs);
@@ -661,6 +678,7 @@ static int64_t eigvecs_range(int64_t n, const double* d, const double* e, const 
         nflag += do_cluster(n, d, e, wt, tnorm, seed, j1, j2, jstop, j_lo, j_hi, Z, ldz, iters, mgs);
     }
     free(cs); free(wt);
+    free(dsc); free(esc); free(wsc);
     return nflag;
 }
 

@@ -59,6 +59,7 @@ __device__ __forceinline__ void l2_prefetch(const double* p, int64_t ndoubles) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 constexpr int64_t kPfDist = 2048;   // doubles prefetched ahead inside a row (16 KB)
+constexpr double kL2KeepBytes = 48e6;   // Y_p beyond this: single-use streams are evict_first
 
 struct SSlots {  // scalar partial slots per CTA (ws.S[r*SST + slot])
     enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4, GPN = 5, X2N = 6, Q1 = 7, FA = 8, FB = 9 };
@@ -365,14 +366,21 @@ __device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P,
         double acc = 0.0;
         if (tg < TG && kk < K) {
             const double* col = P + kb + kk;
-            int t = tg;
             auto at = [&](int u) { return col + (int64_t)u * mc + rks.off(u); };
-            for (; t + 3 * TG < G; t += 4 * TG) {
-                const double v0 = ld(at(t)), v1 = ld(at(t + TG));
-                const double v2 = ld(at(t + 2 * TG)), v3 = ld(at(t + 3 * TG));
-                acc += v0; acc += v1; acc += v2; acc += v3;
+            // up to 16 independent loads in flight per thread (one L2 round trip per batch
+            // instead of one per 4 partials), added in the fixed order t = tg, tg + TG, ...
+            constexpr int RB = 16;
+            for (int t0 = tg; t0 < G; t0 += RB * TG) {
+                double v[RB];
+#pragma unroll
+                for (int u = 0; u < RB; u++) {
+                    const int t = t0 + u * TG;
+                    v[u] = (t < G) ? ld(at(t)) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < RB; u++)
+                    if (t0 + u * TG < G) acc += v[u];
             }
-            for (; t < G; t += TG) acc += ld(at(t));
         }
         if (TG > 1) {
             __syncthreads();
@@ -865,7 +873,7 @@ __device__ __forceinline__ int wide_rps(int pst) { return min(2 * NCW, kWStgD / 
 // __syncthreads.  chunk_begin / chunk_end run on all threads around each chunk (may
 // __syncthreads).
 template <class Src, class Body, class BlkBegin, class BlkEnd, class ChunkBegin, class ChunkEnd>
-__device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, bool reverse_blocks,
+__device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, bool reverse_blocks, uint64_t pol,
                             ChunkBegin chunk_begin, BlkBegin blk_begin, Body body, BlkEnd blk_end,
                             ChunkEnd chunk_end) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -930,8 +938,8 @@ __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, boo
                     if (b > a) {
                         const uint32_t bytes = (uint32_t)(b - a) * 8u;
                         mbar_add_tx(rg.full + slot, bytes);
-                        bulk_g2s(rg.base + (int64_t)slot * kWStgD + (r - ra) * PST + (a - kb * PW), src.base(r) + a,
-                                 bytes, rg.full + slot);
+                        bulk_g2s_hint(rg.base + (int64_t)slot * kWStgD + (r - ra) * PST + (a - kb * PW),
+                                      src.base(r) + a, bytes, rg.full + slot, pol);
                     }
                 }
                 __syncwarp();
@@ -977,7 +985,7 @@ __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, boo
 // vector w when TWO); epi(r, dot, dot2) after all blocks, one thread per row.
 template <bool TWO, class Src, class Epi>
 __device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, int r0, int r1, const double* v,
-                             const double* w, int P, Epi epi) {
+                             const double* w, int P, uint64_t pol, Epi epi) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* racc = sm.racc;           // RCH (x2 when TWO)
     int cb = 0;
@@ -994,7 +1002,7 @@ __device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, in
     const int NB = src.nblk();
     int pre = -1;   // block prefetched into its buffer (thread 32)
     wide_stream(
-        rg, src, r0, r1, false,
+        rg, src, r0, r1, false, pol,
         [&](int c0, int c1) {
             cb = c0;
             pre = -1;
@@ -1089,7 +1097,7 @@ __device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, in
 // [r0, r1); coefficients staged per chunk from coef (global).  Returns sum coef^2.
 template <class Src>
 __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, int r0, int r1, const double* coef,
-                              int P, double* out, bool reverse_blocks) {
+                              int P, double* out, bool reverse_blocks, uint64_t pol) {
     const int tid = threadIdx.x, tc = tid - 32;   // consumer thread index
     double c2 = 0.0;
     double a0 = 0.0, a1 = 0.0;
@@ -1109,7 +1117,7 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
         }
     if (r1 <= r0) return 0.0;
     wide_stream(
-        rg, src, r0, r1, reverse_blocks,
+        rg, src, r0, r1, reverse_blocks, pol,
         [&](int c0, int c1) {
             cb = c0;
             for (int r = c0 + tid; r < c1; r += NT) {
@@ -1189,6 +1197,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     uint32_t wiss = 0, wuse = 0;   // wide ring stage counters (issued: warp 0; used: all)
     const WRing wr{ring_base, wfull, wempty, &wiss, &wuse, timing0 ? ntim : nullptr};
     const int tid = threadIdx.x;
+    const uint64_t pol_first = l2_policy_evict_first(), pol_norm = l2_policy_evict_normal();
     int g = 0;
     for (int t = 0; t < a.ngroups; t++)
         if ((int)blockIdx.x >= a.g_cta0[t]) g = t;
@@ -1294,6 +1303,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             bool use_la = la_have;           // first iteration: A already done in look-ahead
             bool la_done = false;            // look-ahead for vector p+1 issued
             la_have = false;
+            // L2 policy of the streams: once Y_p no longer fits a share of L2, the passes that read
+            // their operand once stream it evict_first (the partial sums, vectors and BC's re-read
+            // stay in L2); BC's first read of Yhat keeps the normal priority for its second read
+            const bool ybig = 8.0 * (double)y_row_off(n, p + 1 < m ? p + 1 : m) > kL2KeepBytes;
+            const uint64_t pol_once = ybig ? pol_first : pol_norm, pol_keep = pol_norm;
             // this CTA's share of every pass of vector p (the same in each iteration)
             int64_t pa0, pa1, ptt0, ptt1, ptn0, ptn1, pd0, pd1;
             part_rows_weighted(n, p, cg, Gt, pa0, pa1, a.piece_cost);
@@ -1316,7 +1330,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                             });
                             narrow_colacc_finish(sm, CPT, p, a0, a1, P_ + (int64_t)cg * mc);
                         } else if (p > kNarrowM) {
-                            x2 = wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, xcur, p, P_ + (int64_t)cg * mc, false);
+                            x2 = wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, xcur, p, P_ + (int64_t)cg * mc, false, pol_once);
                         } else {
                             x2 = colacc(sm, Y, m, i0, i1, p, xcur, xs, P_ + (int64_t)cg * mc);
                         }
@@ -1348,7 +1362,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     int64_t k0, k1;
                     k0 = ptt0; k1 = ptt1;
                     if (p > kNarrowM) {
-                        wide_rowdots<false>(sm, wr, SrcTc{Tc, (int)p}, (int)k0, (int)k1, ws.g, nullptr, p,
+                        wide_rowdots<false>(sm, wr, SrcTc{Tc, (int)p}, (int)k0, (int)k1, ws.g, nullptr, p, pol_once,
                                             [&](int64_t k, double v, double) { mst(ws.gp + k, v); });
                     } else if (k1 > k0) {
                         stage_vec(sm, ws.g, p);
@@ -1387,7 +1401,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         u2 = block_sum<NT>(u2, sm.red);
                         if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
                     } else if (p > kNarrowM) {
-                        wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.gp, nullptr, p,
+                        wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.gp, nullptr, p, pol_keep,
                                             [&](int64_t i, double v, double) {
                                                 const double ui = ld(xcur + i) - v;
                                                 mst(ws.u + i, ui);
@@ -1396,7 +1410,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         u2 = block_sum<NT>(u2, sm.red);
                         if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
                         // second read of Yhat, blocks in reverse order (the last ones are in L2)
-                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)cg * mc, true);
+                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)cg * mc, true, pol_once);
                     } else {
                         stage_vec(sm, ws.gp, p);
                         rowdots(i0, i1, p, sm.vs,
@@ -1456,7 +1470,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     int64_t l0, l1;
                     l0 = ptn0; l1 = ptn1;
                     if (p > kNarrowM) {
-                        wide_rowdots<true>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, yrow, p,
+                        wide_rowdots<true>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, yrow, p, pol_once,
                                            [&](int64_t l, double a1, double a2) {
                                                const double that = -tt * a1;
                                                mst(ws.xp + l, a2 + y0 * that);
@@ -1557,7 +1571,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                             });
                         });
                     } else if (p + 1 > kNarrowM) {
-                        wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p + 1}, (int)i0, (int)i1, ws.xp, nullptr, p + 1,
+                        wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p + 1}, (int)i0, (int)i1, ws.xp, nullptr, p + 1, pol_once,
                                             [&](int64_t i, double v, double) { epiq(i, v); });
                     } else {
                         stage_vec(sm, ws.xp, p + 1);
@@ -1739,7 +1753,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         part_rows_weighted(n, p, rl, Gl, i0, i1, a.piece_cost);
                         double x2n = (p > kNarrowM)
                                          ? wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, a.X1c + (j + 1) * n2v, p,
-                                                       ws.P2 + (int64_t)cg * mc, false)
+                                                       ws.P2 + (int64_t)cg * mc, false, pol_once)
                                          : colacc(sm, Y, m, i0, i1, p, a.X1c + (j + 1) * n2v, 1, ws.P2 + (int64_t)cg * mc);
                         x2n = block_sum<NT>(x2n, sm.red);
                         if (tid == 0) mst(S + cg * SST + SSlots::X2N, x2n);

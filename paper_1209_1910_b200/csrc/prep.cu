@@ -52,19 +52,59 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         if (tid == 0) red[0] = v;
     }
     __syncthreads();
-    const double tnorm = red[0];
+    double tnorm = red[0];
+    if (s_bad) {
+        if (tid == 0) { a.out->tnorm = tnorm; a.out->bad = s_bad; }
+        return;
+    }
+    // ---- R0 (reading 21): ||T||_1 outside [2^-200, 2^200] -> T and w scaled by
+    // the power of two 2^k with 2^k ||T||_1 in [1, 2) (exact; same eigenvectors), so that the
+    // solve's scaling sigma, the pivots' reciprocals and the norms stay in the normal range.
+    // The kernels read d, e through the copies ds, es in either case.
+    int k = 0;
+    if (tnorm > 0.0 && !(tnorm >= 0x1p-200 && tnorm <= 0x1p200)) {
+        int ex;
+        frexp(tnorm, &ex);
+        k = 1 - ex;
+    }
+    for (int64_t i = tid; i < n; i += kPrepThreads) {
+        a.ds[i] = ldexp(a.d[i], k);
+        a.es[i] = (i < n - 1) ? ldexp(a.e[i], k) : 0.0;
+    }
+    if (k != 0) {   // ||T||_1 of the scaled matrix, in the order of R1
+        __syncthreads();
+        tl = 0.0;
+        for (int64_t i = tid; i < n; i += kPrepThreads) {
+            double s = fabs(a.ds[i]);
+            if (i > 0) s = __dadd_rn(s, fabs(a.es[i - 1]));
+            if (i < n - 1) s = __dadd_rn(s, fabs(a.es[i]));
+            tl = fmax(tl, s);
+        }
+        tl = warp_max(tl);
+        __syncthreads();
+        if ((tid & 31) == 0) red[tid >> 5] = tl;
+        __syncthreads();
+        if (tid < 32) {
+            double v = red[tid];
+            v = warp_max(v);
+            if (tid == 0) red[0] = v;
+        }
+        __syncthreads();
+        tnorm = red[0];
+    }
     if (tid == 0) {
         a.out->tnorm = tnorm;
-        a.out->bad = s_bad;
+        a.out->bad = 0;
+        a.out->scale_exp = k;
     }
-    if (s_bad) return;
+    auto wv = [&](int64_t j) -> double { return ldexp(a.w[j], k); };   // exact; k = 0: w itself
     const double thr = __dmul_rn(1e-3, tnorm);
 
     // ---- R2: boundary flags + compaction (chunked block scan)
     for (int64_t base = 0; base < n; base += kPrepThreads) {
         int64_t j = base + tid;
         int flag = 0;
-        if (j < n) flag = (j == 0) || !(__dsub_rn(a.w[j], a.w[j - 1]) <= thr);
+        if (j < n) flag = (j == 0) || !(__dsub_rn(wv(j), wv(j - 1)) <= thr);
         // inclusive warp scan
         int v = flag;
 #pragma unroll
@@ -107,11 +147,11 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         int j1 = a.cstart[c], j2 = a.cstart[c + 1];
         maxm = max(maxm, j2 - j1);
         nclustered += (j2 - j1) - 1;
-        double prev = a.w[j1];
+        double prev = wv(j1);
         a.wt[j1] = prev;
         a.jc[j1] = 0;
         for (int j = j1 + 1; j < j2; j++) {
-            double wj = a.w[j];
+            double wj = wv(j);
             double cand = __dadd_rn(prev, __dmul_rn(10.0 * kEps, fabs(wj)));
             prev = fmax(wj, cand);
             a.wt[j] = prev;

@@ -74,6 +74,7 @@ struct tinv_s {
     int64_t ncap = 0, ldv = 0;
     void* base = nullptr;
     size_t base_bytes = 0;
+    double *ds = nullptr, *es = nullptr;   // d, e as the kernels read them (prep: copies, reading 21)
     double *wt = nullptr, *X = nullptr, *fl = nullptr, *fr = nullptr, *fb = nullptr, *fc = nullptr;
     double *unn = nullptr, *zscale = nullptr, *F = nullptr, *X1c = nullptr;
     int8_t *fp = nullptr, *FP = nullptr;
@@ -165,6 +166,8 @@ int ensure_base(tinv_s* h, int64_t n) {
         Carve c{p};
         const size_t nn = (size_t)n * (size_t)batched_slot_cap(n);   // block-row layout over slots
         h->wt = c.take<double>(n);
+        h->ds = c.take<double>(n + 2);
+        h->es = c.take<double>(n + 2);
         h->unn = c.take<double>(n);
         h->zscale = c.take<double>(n);
         h->cstart = c.take<int>(n + 1);
@@ -560,7 +563,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         return 0;
     };
     ev_record(h, 0);
-    PrepArgs pa{n, d, e, w, h->wt, h->cstart, h->cid, h->jc, h->slot, h->perm, batched_slot_cap(n), handover, h->out};
+    PrepArgs pa{n, d, e, w, h->ds, h->es, h->wt, h->cstart, h->cid, h->jc, h->slot, h->perm, batched_slot_cap(n), handover, h->out};
     launch_prep(pa, st);
     launches++;
     CK(cudaGetLastError());
@@ -570,7 +573,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     CK(cudaMemcpyAsync(h->h_out, h->out, sizeof(PrepOut), cudaMemcpyDeviceToHost, h->side));
     CK(cudaMemcpyAsync(h->h_cstart, h->cstart, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, h->side));
     ev_record(h, 2);
-    BatchedArgs ba{n, h->ldv, d, e, h->wt, h->jc, h->perm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
+    BatchedArgs ba{n, h->ldv, h->ds, h->es, h->wt, h->jc, h->perm, seed, h->fl, h->fp, h->fr, h->fb, h->fc,
                    h->X, h->X1c, h->unn, h->zscale, h->iters, h->out,
                    h->profiling ? reinterpret_cast<unsigned long long*>(h->bnd + 24) : nullptr, 0, 0};
     FinalizeArgs fa{n, h->ldv, h->X, h->zscale, h->perm, Z, ldz, h->out};
@@ -1019,7 +1022,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             }
         }
         CwyArgs ca{};
-        ca.n = n; ca.ldv = h->ldv; ca.d = d; ca.e = e; ca.tnorm = tnorm; ca.seed = seed;
+        ca.n = n; ca.ldv = h->ldv; ca.d = h->ds; ca.e = h->es; ca.tnorm = tnorm; ca.seed = seed;
         ca.wt = h->wt; ca.cstart = h->cstart;
         ca.fl = h->fl; ca.fp = h->fp; ca.fr = h->fr; ca.fb = h->fb; ca.fc = h->fc; ca.unn = h->unn; ca.F = h->F; ca.FP = h->FP;
         ca.X1c = h->X1c; ca.Z = Z; ca.ldz = ldz; ca.iters = h->iters; ca.out = h->out;

@@ -16,7 +16,8 @@ struct PrepOut {
     int n_clustered;
     int nflag;          // vectors that missed the stopping rule
     int nc_pad;         // slots of the vectors the batched LU iterates, rounded up to 32
-    int pad[2];
+    int scale_exp;      // k of the 2^k scaling (reading 21), 0 inside the window
+    int pad;
 };
 
 struct PrepArgs {
@@ -24,6 +25,8 @@ struct PrepArgs {
     const double* d;
     const double* e;
     const double* w;
+    double* ds;         // d and e as the kernels use them (n each): copies, scaled by 2^k when
+    double* es;         // ||T||_1 is outside [2^-200, 2^200] (reading 21); es[n-1] = 0
     double* wt;         // perturbed shifts (n)
     int* cstart;        // cluster starts (n+1)
     int* cid;           // cluster of each vector (n)

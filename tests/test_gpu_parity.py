@@ -264,14 +264,15 @@ def test_maxits_flag(handle, torch):
     assert np.abs(Zg.cpu().numpy() - Zo).max() <= 1e-10
 
 
-@pytest.mark.parametrize("k", [-1000, -500, 300])
+@pytest.mark.parametrize("k", [-1000, -500, -150, 150, 300])
 @pytest.mark.parametrize("cfg,n", [("cfg2", 300), ("cfg3", 210), ("cfg4", 200)])
 def test_scaled_matrices(handle, torch, cfg, n, k):
-    """T, w scaled by 2^k (exact): the eigenvectors of 2^k T are those of T.  At 2^-1000 the
-    pivot floor eps ||T||_1 is subnormal (the factor sweep's approximate reciprocal flushes
-    subnormals, so it switches to IEEE division there).  Gates: the GPU returns the oracle's
-    code, the vectors satisfy the P0 invariants of the UNSCALED problem, and match the
-    oracle's run on the scaled input per vector / per subspace (P1-P3)."""
+    """T, w scaled by 2^k (exact): the eigenvectors of 2^k T are those of T.  Outside
+    [2^-200, 2^200] both sides first rescale to ||T||_1 in [1, 2) (reading 21; at 2^-1000 the
+    pivot floor eps ||T||_1 would be subnormal and sigma would lose its precision); +-150 run
+    unscaled.  Gates: the GPU returns the oracle's code, the vectors satisfy the P0 invariants
+    of the UNSCALED problem, and match the oracle's run on the scaled input per vector / per
+    subspace (P1-P3)."""
     d, e, w = W.problem(cfg, n)
     s = 2.0 ** k
     ds, es, ws_ = d * s, e * s, w * s

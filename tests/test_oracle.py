@@ -515,3 +515,23 @@ def test_maxits_flag_closed_form():
     assert (its == 5).all(), its                      # MAXITS, no restart
     assert np.isfinite(Z).all()
     assert np.allclose(np.linalg.norm(Z, axis=0), 1.0, atol=1e-14)
+
+
+def test_rescaling_reading21_scale_free():
+    """Reading 21: outside ||T||_1 in [2^-200, 2^200] the oracle works on 2^k T (||2^k T||_1 in
+    [1, 2)), so 2^300 T, 2^-500 T and 2^-1000 T (all outside the window) reduce to the SAME
+    scaled matrix and give bit-identical vectors; inside the window (2^150 T) nothing is
+    rescaled.  All of them are eigenvectors of the unscaled T (P0) and agree with the unscaled
+    run within the parity tolerances (P1-P3)."""
+    d, e, w = W.problem("cfg2", 300)
+    Z0, _ = O.eigvecs(d, e, w, seed=1)
+    outs = {}
+    for k in (300, -500, -1000, 150):
+        s = 2.0 ** k
+        Z, info = O.eigvecs(d * s, e * s, w * s, seed=1)
+        assert info == 0
+        assert residual_units(d, e, w, Z) <= 10 and orth_units(Z) <= 10
+        wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Z, Z0)
+        assert wv <= 1e-10 and ws >= 1 - 1e-10
+        outs[k] = Z
+    assert np.array_equal(outs[300], outs[-500]) and np.array_equal(outs[300], outs[-1000])
