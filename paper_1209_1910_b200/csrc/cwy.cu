@@ -112,6 +112,20 @@ __device__ __forceinline__ void part_rows_weighted(int64_t n, int64_t P, int r, 
     a = (r == 0) ? 0 : bsearch_cum(0, n, (W * r) / G, cum);
     b = (r == G - 1) ? n : bsearch_cum(0, n, (W * (r + 1)) / G, cum);
 }
+// rows [b0, b1) of Y_P split over G CTAs by the same weights (rows of one band of the sweep)
+__device__ __forceinline__ void part_band_weighted(int64_t b0, int64_t b1, int64_t P, int r, int G, int64_t& a,
+                                                   int64_t& b, int64_t C) {
+    if (P <= kNarrowM) C = 0;
+    const int64_t NB = (P + kPieceW - 1) / kPieceW;
+    const int64_t base = P * (P + 1) / 2 + C * ((NB > 1 ? sum_floor_pw(P) : 0) + P);
+    auto cum = [P, C, NB, base](int64_t i) -> int64_t {
+        if (i <= P) return i * (i + 1) / 2 + C * ((NB > 1 ? sum_floor_pw(i) : 0) + i);
+        return base + (i - P) * (P + C * NB);
+    };
+    const int64_t w0 = cum(b0), W = cum(b1) - w0;
+    a = (r == 0) ? b0 : bsearch_cum(b0, b1, w0 + (W * r) / G, cum);
+    b = (r == G - 1) ? b1 : bsearch_cum(b0, b1, w0 + (W * (r + 1)) / G, cum);
+}
 __device__ __forceinline__ void part_uniform(int64_t lo, int64_t hi, int r, int G, int64_t& a, int64_t& b) {
     int64_t len = hi - lo;
     a = lo + (len * r) / G;
@@ -451,7 +465,25 @@ __device__ __forceinline__ M block_scan_excl(M f, M* buf, M& total) {
 // bulk copies: per chunk of CH rows the factor records F[i][0..3] (32 B/row) and t_i.  The
 // same thread issues the copies and consumes them (one mbarrier per slot), so the chain only
 // waits for data that was requested kRing chunks earlier.
-__device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const Smem& sm, uint32_t& mbph) {
+// Band progress of the sweep (fused pass A2 behind it): rows are final bottom-up; after every
+// kBandCh chunks the sweep publishes "bands 0..b done" as prog = tag + b + 1 (release), so
+// the other CTAs can stream those rows while the sweep goes on.
+constexpr int kBandCh = 4;
+__host__ __device__ __forceinline__ int sweep_bands(int64_t n) {
+    const int64_t C = (n + 256 - 1) / 256;
+    return (int)((C + kBandCh - 1) / kBandCh);
+}
+__device__ __forceinline__ void publish(unsigned int* prog, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(prog), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int acquire(const unsigned int* prog) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(prog) : "memory");
+    return v;
+}
+
+__device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const Smem& sm, uint32_t& mbph,
+                           unsigned int* prog = nullptr, unsigned int tag = 0) {
     const int64_t n = a.n;
     const double* __restrict__ F = a.F + j * n * 4;
     const double* __restrict__ ts = ws.ysol;
@@ -520,9 +552,18 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
         bulk_s2g(x + lo, xb, (uint32_t)((cnt + 1) & ~1) * 8u);
         bulk_commit();
         if (k + kRing < C) issue(k + kRing);
+        // band b = chunks [b kBandCh, (b+1) kBandCh) complete: its bulk stores are performed once
+        // at most the newest group (this chunk's) is pending -- published one chunk late, so
+        // the wait never stalls the chain
+        if (prog && k % kBandCh == 0 && k > 0) {
+            asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+            fence_proxy_async_global();
+            publish(prog, tag + (unsigned int)(k / kBandCh));
+        }
     }
     bulk_wait_all();
     fence_proxy_async_global();   // the bulk-stored x before the group barrier's release
+    if (prog) publish(prog, tag + (unsigned int)sweep_bands(n));
 }
 
 // Composition of the forward maps of CTAs 0..cnt-1 (S slots FA, FB), applied in CTA order, by
@@ -1094,28 +1135,34 @@ __device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, in
 }
 
 // Column accumulate of a wide pass: out[k] = sum_r row_r[k] coef(r) for k < P over rows
-// [r0, r1); coefficients staged per chunk from coef (global).  Returns sum coef^2.
-template <class Src>
+// [r0, r1); coefficients staged per chunk from coef (global).  Returns sum coef^2.  TWO: a
+// second coefficient vector coef2 -> out2 from the same stream (c2 sum in *c2b).  accum: add
+// into out (and out2) instead of overwriting them (rows of one CTA split over several calls).
+template <bool TWO = false, class Src>
 __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, int r0, int r1, const double* coef,
-                              int P, double* out, bool reverse_blocks, uint64_t pol) {
+                              int P, double* out, bool reverse_blocks, uint64_t pol, bool accum = false,
+                              const double* coef2 = nullptr, double* out2 = nullptr, double* c2b = nullptr) {
     const int tid = threadIdx.x, tc = tid - 32;   // consumer thread index
-    double c2 = 0.0;
-    double a0 = 0.0, a1 = 0.0;
+    double c2 = 0.0, c2x = 0.0;
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
     int cb = 0;
     // The accumulate owns columns 2tc, 2tc+1 of every block.  With one row chunk each block's
     // sums are final at its end (plain store); with several chunks they are added up (zeroed
     // first).  Blocks that no row of this CTA reaches are zero.
-    const bool multi = (r1 - r0) > RCH;
-    if (tc >= 0)
+    const bool multi = accum || (r1 - r0) > RCH;
+    if (tc >= 0 && !accum)
         for (int kb = 0; kb < src.nblk(); kb++) {
             int a, b;
             src.rows(kb, r0, r1, a, b);
-            if (a < b && !multi) continue;   // written by blk_end
+            if (a < b && (r1 - r0) <= RCH) continue;   // written by blk_end
             const int k = kb * PW + 2 * tc;
-            if (k < P) st(out + k, 0.0);
-            if (k + 1 < P) st(out + k + 1, 0.0);
+            if (k < P) { st(out + k, 0.0); if (TWO) st(out2 + k, 0.0); }
+            if (k + 1 < P) { st(out + k + 1, 0.0); if (TWO) st(out2 + k + 1, 0.0); }
         }
+    if (TWO) *c2b = 0.0;
     if (r1 <= r0) return 0.0;
+    double* cf2 = sm.racc;   // second coefficient chunk (the row accumulators are unused here)
+    static_assert(2 * RCH >= CFCH, "second coefficient chunk in the row accumulators");
     wide_stream(
         rg, src, r0, r1, reverse_blocks, pol,
         [&](int c0, int c1) {
@@ -1124,9 +1171,14 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
                 const double c = ld(coef + r);
                 sm.cf[r - c0] = c;
                 c2 = fma(c, c, c2);
+                if (TWO) {
+                    const double cx = ld(coef2 + r);
+                    cf2[r - c0] = cx;
+                    c2x = fma(cx, cx, c2x);
+                }
             }
             __syncthreads();
-            a0 = a1 = 0.0;
+            a0 = a1 = b0 = b1 = 0.0;
         },
         [&](int, int, int) {},
         [&](int kb, int ra, int rb, const double* slot) {
@@ -1137,18 +1189,31 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
                 if (k + 1 >= lo && k < hi) {
                     const double2 y = *reinterpret_cast<const double2*>(slot + (r - ra) * PST + 2 * tc);
                     const double c = sm.cf[r - cb];
-                    if (k >= lo) a0 = fma(y.x, c, a0);
-                    if (k + 1 < hi) a1 = fma(y.y, c, a1);
+                    const double y0 = (k >= lo) ? y.x : 0.0, y1 = (k + 1 < hi) ? y.y : 0.0;
+                    a0 = fma(y0, c, a0);
+                    a1 = fma(y1, c, a1);
+                    if (TWO) {
+                        const double cx = cf2[r - cb];
+                        b0 = fma(y0, cx, b0);
+                        b1 = fma(y1, cx, b1);
+                    }
                 }
             }
         },
         [&](int kb) {
             const int k = kb * PW + 2 * tc;
-            if (k < P) st(out + k, multi ? ld(out + k) + a0 : a0);
-            if (k + 1 < P) st(out + k + 1, multi ? ld(out + k + 1) + a1 : a1);
-            a0 = a1 = 0.0;
+            if (k < P) {
+                st(out + k, multi ? ld(out + k) + a0 : a0);
+                if (TWO) st(out2 + k, multi ? ld(out2 + k) + b0 : b0);
+            }
+            if (k + 1 < P) {
+                st(out + k + 1, multi ? ld(out + k + 1) + a1 : a1);
+                if (TWO) st(out2 + k + 1, multi ? ld(out2 + k + 1) + b1 : b1);
+            }
+            a0 = a1 = b0 = b1 = 0.0;
         },
         [&](int, int) {});
+    if (TWO) *c2b = c2x;
     return c2;
 }
 
@@ -1193,6 +1258,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     // group's first CTA (+ prof_sel)
     const bool timing0 = (a.prof != nullptr) && threadIdx.x == 32 && (int)blockIdx.x == a.g_cta0[0] + a.prof_sel;
     uint64_t ntim[4] = {0, 0, 0, 0};
+    // debug build: SM-clock sub-timers of the reductions on thread 0 of the timed CTA (replace
+    // the stream timers in prof slots 12-15: R1 partials, R1 rest, R2 scalars, R2 partials)
+    const bool dsub = kWideDebug && (a.prof != nullptr) && threadIdx.x == 0 && (int)blockIdx.x == a.g_cta0[0] + a.prof_sel;
+    uint64_t dtim[4] = {0, 0, 0, 0};
+    auto dclk = [&]() -> uint64_t { return dsub ? (uint64_t)clock64() : 0; };
     const Ring rg{ring_base, sm.mbar + kRing, &rph, timing0 ? ntim : nullptr};
     uint32_t wiss = 0, wuse = 0;   // wide ring stage counters (issued: warp 0; used: all)
     const WRing wr{ring_base, wfull, wempty, &wiss, &wuse, timing0 ? ntim : nullptr};
@@ -1293,6 +1363,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
 
         // ================= vectors j_c = 1 .. m-1
         bool la_have = false;   // look-ahead of this vector's first pass A is ready
+        unsigned int* sw_prog = reinterpret_cast<unsigned int*>(S + (int64_t)Gt * SST);   // sweep bands
+        unsigned int sw_ep = 0;   // fused sweeps so far in this cluster (the progress tag's epoch)
+        if (r == 0 && tid == 0) publish(sw_prog, 0u);   // visible after the next group barrier
         for (int64_t p = 1; p < m; p++) {
             const int64_t j = j1 + p;
             inwin = !kWideDebug || (p >= a.prof_p0 && p < a.prof_p1);
@@ -1301,6 +1374,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             int its = 1, kin = 1, passes = 0, restart = 0;
             bool done = false, flagged = false;
             bool use_la = la_have;           // first iteration: A already done in look-ahead
+            bool use_a2 = false;             // pass A of this iteration fused behind the back sweep
             bool la_done = false;            // look-ahead for vector p+1 issued
             la_have = false;
             // L2 policy of the streams: once Y_p no longer fits a share of L2, the passes that read
@@ -1315,7 +1389,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             part_tn(p, cg, Gt, ptn0, ptn1, a.piece_cost);
             part_rows_weighted(n, p + 1, cg, Gt, pd0, pd1, a.piece_cost);
             while (!done) {
-                if (!use_la) {
+                if (!use_la && !use_a2) {
                     // ---------------- A: partial g = Y_p^T x, ||x||^2
                     {
                         int64_t i0, i1;
@@ -1345,14 +1419,19 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 // from the previous vector's last pass D)
                 {
                     int64_t k0, k1;
+                    const uint64_t q0 = dclk();
                     if (use_la) {
                         part_uniform(0, p - 1, cg, Gt, k0, k1);
                         reduce_partials(sm, ws.P2, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
+                        const uint64_t q1 = dclk();
+                        if (dsub) dtim[0] += q1 - q0;
                         const double gl = reduce_slot(sm, S, Gt, SSlots::GPN);
                         if (r == 0 && tid == 0) st(ws.g + p - 1, gl);   // every rank, its own replica
+                        if (dsub) dtim[1] += dclk() - q1;
                     } else {
                         part_uniform(0, p, cg, Gt, k0, k1);
                         reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
+                        if (dsub) dtim[0] += dclk() - q0;
                     }
                 }
                 gsync();
@@ -1429,9 +1508,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 gsync();
                 PH(4);
                 // ---------------- R2: scalars (every CTA, identical), s = s' - c Y[p,:]
+                const uint64_t q2s = dclk();
                 double un = sqrt(reduce_slot(sm, S, Gt, SSlots::U2));
                 const double x2 = reduce_slot(sm, S, Gt, use_la ? SSlots::X2N : SSlots::X2);
                 use_la = false;
+                use_a2 = false;
                 double u0 = ld(ws.u + p);
                 const bool zero_u = (un == 0.0);   // reading: exactly-zero uhat -> e_1
                 if (zero_u) { u0 = 1.0; un = 1.0; }
@@ -1453,6 +1534,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 const double tt = 1.0 / (c * c - u0 * c);
                 const double y0 = u0 - c;
                 const double* yrow = Y + y_row_off(p, m);
+                const uint64_t q2m = dclk();
+                if (dsub) dtim[2] += q2m - q2s;
                 {
                     int64_t k0, k1;
                     part_uniform(0, p, cg, Gt, k0, k1);
@@ -1463,6 +1546,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                         [&](int64_t k, double v) { mst(ws.s + k, v - c * ld(yrow + k)); }, rks);
                     }
                 }
+                if (dsub) dtim[3] += dclk() - q2m;
                 gsync();
                 PH(5);
                 // ---------------- TN: [Ts, h] = T_p [s, yrow]; column p of T and Y; x'
@@ -1670,10 +1754,19 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     // look-ahead only when it can overlap the back sweep (other CTAs of the
                     // group, or warps 1.. of a single-CTA narrow group)
                     const bool la = !la_done && p + 1 < m && la_ok;
+                    // fused A2 (single-rank wide groups): pass A of the next iteration (g = Y_p^T x
+                    // with the solve's x) streams Y_p behind the back sweep, band by band as the
+                    // rows become final, together with the look-ahead Y_p^T x^(1)_{p+1}: one read
+                    // of Y_p for both (PAPER.md:534-535 for both vectors)
+                    const bool a2 = (NR == 1) && (G > 1) && !narrow && p > kNarrowM;
                     if (r == 0) {
                         if (la) {   // CTA 0 of every rank solves; its look-ahead partial is zero
                             for (int64_t k = tid; k < p; k += NT) st(ws.P2 + (int64_t)cg * mc + k, 0.0);
                             if (tid == 0) mst(S + cg * SST + SSlots::X2N, 0.0);
+                        }
+                        if (a2) {   // ... and so is its share of the fused pass A
+                            for (int64_t k = tid; k < p; k += NT) st(P_ + (int64_t)cg * mc + k, 0.0);
+                            if (tid == 0) st(S + cg * SST + SSlots::X2, 0.0);
                         }
                     }
                     {   // forward sweep, pass 2: exact carries from the CTA maps -> t_s = sc y_s / u0_s
@@ -1741,10 +1834,46 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         __syncthreads();
                         rph = *reinterpret_cast<volatile uint32_t*>(sm.red + NW + 7);
                     } else if (r == 0 && tid == 0) {
-                        back_sweep(a, ws, j, sm, mbph);
+                        back_sweep(a, ws, j, sm, mbph, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8);
                     }
                     mark(10);
-                    if (la && r > 0) {   // G > 1: the other CTAs of the group
+                    if (a2 && r > 0) {
+                        // bands bottom-up; this CTA's rows of each band by the pass weights
+                        const unsigned int tag = (sw_ep + 1) << 8;
+                        const int nbands = sweep_bands(n);
+                        const int Gl = G - 1, rl = r - 1;
+                        const double* xn = a.X1c + (j + 1) * n2v;
+                        double x2 = 0.0, x2n = 0.0;
+                        for (int b = 0; b < nbands; b++) {
+                            const int64_t C = (n + 255) / 256;
+                            const int64_t chi = C - (int64_t)b * kBandCh, clo = chi - kBandCh > 0 ? chi - kBandCh : 0;
+                            const int64_t b0 = clo * 256, b1 = chi * 256 < n ? chi * 256 : n;
+                            int64_t i0, i1;
+                            part_band_weighted(b0, b1, p, rl, Gl, i0, i1, a.piece_cost);
+                            if (tid == 0) {
+                                uint32_t spins = 0;
+                                while (acquire(sw_prog) < tag + (unsigned int)b + 1u)
+                                    if (++spins > (1u << 30)) __trap();
+                            }
+                            __syncthreads();
+                            if (la) {
+                                double c2n = 0.0;
+                                x2 += wide_colacc<true>(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.x, p,
+                                                        P_ + (int64_t)cg * mc, false, pol_once, b > 0, xn,
+                                                        ws.P2 + (int64_t)cg * mc, &c2n);
+                                x2n += c2n;
+                            } else {
+                                x2 += wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.x, p,
+                                                  P_ + (int64_t)cg * mc, false, pol_once, b > 0);
+                            }
+                        }
+                        x2 = block_sum<NT>(x2, sm.red);
+                        if (la) x2n = block_sum<NT>(x2n, sm.red);
+                        if (tid == 0) {
+                            st(S + cg * SST + SSlots::X2, x2);
+                            if (la) st(S + cg * SST + SSlots::X2N, x2n);
+                        }
+                    } else if (la && r > 0) {   // G > 1: the other CTAs of the group
                         // look-ahead: Y_{p}^T x^(1)_{p+1} over the accepted columns 0..p-1,
                         // overlapped with the chained solve (PAPER.md:534-535 for vector j+1)
                         // (every rank's CTA 0 solves; the others split the rows over all ranks)
@@ -1759,6 +1888,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         if (tid == 0) mst(S + cg * SST + SSlots::X2N, x2n);
                     }
                     if (la) la_done = true;
+                    if (a2) { sw_ep++; use_a2 = true; }
                     gsync();
                     PH(11);
                     xcur = ws.x;
@@ -1771,8 +1901,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     if (r == 0 && tid == 0) a.syncs[g] = nsync;
     if (timing)
         for (int k = 0; k < 12; k++) a.prof[g * 16 + k] = tacc[k];
-    if (timing0)
+    if (timing0 && !kWideDebug)
         for (int k = 0; k < 4; k++) a.prof[12 + k] = ntim[k];
+    if (dsub)
+        for (int k = 0; k < 4; k++) a.prof[12 + k] = dtim[k];
 #undef PH
 }
 
