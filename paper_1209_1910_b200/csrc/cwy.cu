@@ -468,10 +468,9 @@ __device__ __forceinline__ M block_scan_excl(M f, M* buf, M& total) {
 // Band progress of the sweep (fused pass A2 behind it): rows are final bottom-up; after every
 // kBandCh chunks the sweep publishes "bands 0..b done" as prog = tag + b + 1 (release), so
 // the other CTAs can stream those rows while the sweep goes on.
-constexpr int kBandCh = 4;
-__host__ __device__ __forceinline__ int sweep_bands(int64_t n) {
+__host__ __device__ __forceinline__ int sweep_bands(int64_t n, int bch) {
     const int64_t C = (n + 256 - 1) / 256;
-    return (int)((C + kBandCh - 1) / kBandCh);
+    return (int)((C + bch - 1) / bch);
 }
 __device__ __forceinline__ void publish(unsigned int* prog, unsigned int v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(prog), "r"(v) : "memory");
@@ -555,15 +554,15 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
         // band b = chunks [b kBandCh, (b+1) kBandCh) complete: its bulk stores are performed once
         // at most the newest group (this chunk's) is pending -- published one chunk late, so
         // the wait never stalls the chain
-        if (prog && k % kBandCh == 0 && k > 0) {
+        if (prog && k % a.band_ch == 0 && k > 0) {
             asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
             fence_proxy_async_global();
-            publish(prog, tag + (unsigned int)(k / kBandCh));
+            publish(prog, tag + (unsigned int)(k / a.band_ch));
         }
     }
     bulk_wait_all();
     fence_proxy_async_global();   // the bulk-stored x before the group barrier's release
-    if (prog) publish(prog, tag + (unsigned int)sweep_bands(n));
+    if (prog) publish(prog, tag + (unsigned int)sweep_bands(n, a.band_ch));
 }
 
 // Composition of the forward maps of CTAs 0..cnt-1 (S slots FA, FB), applied in CTA order, by
@@ -1758,7 +1757,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     // with the solve's x) streams Y_p behind the back sweep, band by band as the
                     // rows become final, together with the look-ahead Y_p^T x^(1)_{p+1}: one read
                     // of Y_p for both (PAPER.md:534-535 for both vectors)
-                    const bool a2 = (NR == 1) && (G > 1) && !narrow && p > kNarrowM;
+                    const bool a2 = a.a2 && (NR == 1) && (G > 1) && !narrow && p > kNarrowM;
                     if (r == 0) {
                         if (la) {   // CTA 0 of every rank solves; its look-ahead partial is zero
                             for (int64_t k = tid; k < p; k += NT) st(ws.P2 + (int64_t)cg * mc + k, 0.0);
@@ -1840,20 +1839,23 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     if (a2 && r > 0) {
                         // bands bottom-up; this CTA's rows of each band by the pass weights
                         const unsigned int tag = (sw_ep + 1) << 8;
-                        const int nbands = sweep_bands(n);
+                        const int nbands = sweep_bands(n, a.band_ch);
+                        const int bch = a.band_ch;
                         const int Gl = G - 1, rl = r - 1;
                         const double* xn = a.X1c + (j + 1) * n2v;
                         double x2 = 0.0, x2n = 0.0;
                         for (int b = 0; b < nbands; b++) {
                             const int64_t C = (n + 255) / 256;
-                            const int64_t chi = C - (int64_t)b * kBandCh, clo = chi - kBandCh > 0 ? chi - kBandCh : 0;
+                            const int64_t chi = C - (int64_t)b * bch, clo = chi - bch > 0 ? chi - bch : 0;
                             const int64_t b0 = clo * 256, b1 = chi * 256 < n ? chi * 256 : n;
                             int64_t i0, i1;
                             part_band_weighted(b0, b1, p, rl, Gl, i0, i1, a.piece_cost);
                             if (tid == 0) {
                                 uint32_t spins = 0;
-                                while (acquire(sw_prog) < tag + (unsigned int)b + 1u)
+                                while (acquire(sw_prog) < tag + (unsigned int)b + 1u) {
+                                    if (a.poll_ns) __nanosleep(a.poll_ns);
                                     if (++spins > (1u << 30)) __trap();
+                                }
                             }
                             __syncthreads();
                             if (la) {

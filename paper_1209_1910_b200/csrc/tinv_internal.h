@@ -161,6 +161,9 @@ struct CwyArgs {
     int prof_p0, prof_p1;    // phase timers count only vectors with prof_p0 <= j_c < prof_p1
     int piece_cost;          // partition cost of one wide row piece, in elements (cwy.cu part_*)
     int prof_sel;            // debug: CTA whose thread 32 runs the pass timers (default: the first group's first)
+    int a2;                  // fuse iteration 2's pass A behind the back sweep (TINV_A2, default 1)
+    int band_ch;             // sweep chunks (256 rows) per published band (TINV_BANDCH)
+    int poll_ns;             // back-off of the band polls in ns (TINV_POLLNS)
     unsigned long long* prof_cta;   // debug: per-CTA busy time before each phase's barrier [cta*16 + phase], or NULL
 };
 
