@@ -370,9 +370,11 @@ struct Ranks {
 };
 template <class Post>
 __device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P, int64_t mc, int G, int64_t k0,
-                                                int64_t k1, Post post, const Ranks& rks = Ranks{1, 1, nullptr}) {
+                                                int64_t k1, Post post, const Ranks& rks = Ranks{1, 1, nullptr},
+                                                uint64_t* dt = nullptr) {
     const int tid = threadIdx.x;
     for (int64_t kb = k0; kb < k1; kb += NT) {
+        const uint64_t c0 = dt ? (uint64_t)clock64() : 0;
         const int64_t K = (k1 - kb < NT) ? (k1 - kb) : NT;
         const int KP = (int)((K + 31) & ~int64_t(31));
         const int TG = NT / KP;
@@ -395,6 +397,11 @@ __device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P,
                 for (int u = 0; u < RB; u++)
                     if (t0 + u * TG < G) acc += v[u];
             }
+        }
+        if (dt) {
+            asm volatile("" ::"d"(acc));
+            const uint64_t c1 = (uint64_t)clock64();
+            dt[0] += c1 - c0;
         }
         if (TG > 1) {
             __syncthreads();
@@ -1423,14 +1430,21 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         part_uniform(0, p - 1, cg, Gt, k0, k1);
                         reduce_partials(sm, ws.P2, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
                         const uint64_t q1 = dclk();
-                        if (dsub) dtim[0] += q1 - q0;
+                        const bool dla = dsub && !(a.dbg & 1);
+                        if (dla) dtim[0] += q1 - q0;
                         const double gl = reduce_slot(sm, S, Gt, SSlots::GPN);
                         if (r == 0 && tid == 0) st(ws.g + p - 1, gl);   // every rank, its own replica
-                        if (dsub) dtim[1] += dclk() - q1;
+                        if (dla) dtim[1] += dclk() - q1;
                     } else {
                         part_uniform(0, p, cg, Gt, k0, k1);
                         reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
-                        if (dsub) dtim[0] += dclk() - q0;
+                        const uint64_t q1 = dclk();
+                        if (dsub) dtim[0] += q1 - q0;
+                        if (kWideDebug && (a.dbg & 1)) {   // experiment: the same reduction again
+                            reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks,
+                                            dsub ? dtim + 2 : nullptr);
+                            if (dsub) dtim[1] += dclk() - q1;
+                        }
                     }
                 }
                 gsync();
@@ -1534,7 +1548,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 const double y0 = u0 - c;
                 const double* yrow = Y + y_row_off(p, m);
                 const uint64_t q2m = dclk();
-                if (dsub) dtim[2] += q2m - q2s;
+                if (dsub && !(a.dbg & 1)) dtim[2] += q2m - q2s;
                 {
                     int64_t k0, k1;
                     part_uniform(0, p, cg, Gt, k0, k1);

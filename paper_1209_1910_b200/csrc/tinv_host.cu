@@ -1035,8 +1035,9 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.piece_cost = getenv("TINV_PIECE_COST") ? atoi(getenv("TINV_PIECE_COST")) : 4000;
         ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
         ca.a2 = getenv("TINV_A2") ? atoi(getenv("TINV_A2")) : 1;
-        ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 4;
+        ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 16;
         ca.poll_ns = getenv("TINV_POLLNS") ? atoi(getenv("TINV_POLLNS")) : 0;
+        ca.dbg = getenv("TINV_DBG") ? atoi(getenv("TINV_DBG")) : 0;
         unsigned long long* pcta = nullptr;
         if (getenv("TINV_PROF_CTA")) {   // debug only (not the product path): per-CTA phase busy times
             CK(cudaMalloc(&pcta, sizeof(unsigned long long) * 16 * sc.nctas));

@@ -164,6 +164,7 @@ struct CwyArgs {
     int a2;                  // fuse iteration 2's pass A behind the back sweep (TINV_A2, default 1)
     int band_ch;             // sweep chunks (256 rows) per published band (TINV_BANDCH)
     int poll_ns;             // back-off of the band polls in ns (TINV_POLLNS)
+    int dbg;                 // debug build experiments (TINV_DBG bits)
     unsigned long long* prof_cta;   // debug: per-CTA busy time before each phase's barrier [cta*16 + phase], or NULL
 };
 

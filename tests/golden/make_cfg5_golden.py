@@ -10,7 +10,9 @@ Stored columns (VERDICT r01 "cfg5 golden columns"; parity classes of SURVEY.md Â
   * j in {2000, 6000, 10000, 14000} +- 2: isolated at tau_v = 1e-6 ||T||_1, per-vector gate;
   * the top tau_v run [15948, 16000) (gaps <= tau_v): subspace gate.
 The bottom run [0, 52) is cheap for the oracle's range mode and is recomputed by the test.
-Also stored: info, the iteration count of every vector, and a hash of the input w.
+Also stored: the input w itself (the GPU test feeds this exact w, so the columns do not
+depend on the LAPACK build that produced it), info, the iteration count of every vector,
+and a hash of w.
 
 Usage: OMP_NUM_THREADS=6 python tests/golden/make_cfg5_golden.py [--full-out PATH]
 """
@@ -45,7 +47,7 @@ def main():
         np.save(a.full_out, Z)
     cols = np.array(COLS, dtype=np.int64)
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cfg5_oracle_cols.npz")
-    np.savez(out, cols=cols, Z=np.ascontiguousarray(Z[:, cols]), info=np.int64(info),
+    np.savez(out, cols=cols, w=w, Z=np.ascontiguousarray(Z[:, cols]), info=np.int64(info),
              iters=iters.astype(np.int8), seed=np.int64(SEED), oracle_seconds=np.float64(dt),
              w_sha=np.bytes_(hashlib.sha256(np.ascontiguousarray(w).tobytes()).hexdigest()))
     print("wrote", out)
