@@ -164,6 +164,9 @@ struct Smem {
     double2* acc;    // NT
     double* red;     // NW + 8
     uint64_t* mbar;  // kRing mbarriers (back-sweep ring)
+    double* rbuf;    // partial-sum staging of reduce_partials (aliases the pass rings)
+    uint64_t* rbar;  // its mbarrier
+    uint32_t* rcnt;  // its use counter (phase parity)
 };
 
 // copy len doubles of a global vector into sm.vs (zero padded by 2), then barrier
@@ -368,11 +371,53 @@ struct Ranks {
     const int64_t* delta;
     __device__ __forceinline__ int64_t off(int t) const { return nrk == 1 ? 0 : __ldg(delta + t / Gl); }
 };
+constexpr int64_t kRBufD = 21952;   // doubles of Smem::rbuf (= the wide ring, static_assert below)
 template <class Post>
 __device__ __forceinline__ void reduce_partials(const Smem& sm, const double* P, int64_t mc, int G, int64_t k0,
                                                 int64_t k1, Post post, const Ranks& rks = Ranks{1, 1, nullptr},
                                                 uint64_t* dt = nullptr) {
     const int tid = threadIdx.x;
+    // Single-rank groups: the G partial slices [k0, k1) come into shared memory by TMA bulk
+    // copies (one per partial, all in flight on one mbarrier), then every column is summed in
+    // the fixed order t = tg, tg + TG, ... and the TG groups in order (deterministic).  Plain
+    // global loads of the same slices measured ~10 us per reduction inside the kernel.
+    const int64_t ka = k0 & ~int64_t(1), kw = (k1 - ka + 1) & ~int64_t(1);
+    if (rks.nrk == 1 && k1 > k0 && (int64_t)G * kw <= kRBufD && G <= NT && (mc & 1) == 0) {
+        const uint32_t use = *sm.rcnt;
+        if (tid < G) {
+            fence_proxy_async_global();   // partials stored by other CTAs (generic proxy) -> bulk copy
+            const uint32_t bytes = (uint32_t)(kw * 8);
+            mbar_add_tx(sm.rbar, bytes);
+            bulk_g2s(sm.rbuf + (int64_t)tid * kw, P + (int64_t)tid * mc + ka, bytes, sm.rbar);
+        }
+        __syncthreads();
+        if (tid == 0) mbar_arrive(sm.rbar);
+        mbar_wait(sm.rbar, use & 1u);
+        const int64_t off = k0 - ka;
+        for (int64_t kb = k0; kb < k1; kb += NT) {
+            const int64_t K = (k1 - kb < NT) ? (k1 - kb) : NT;
+            const int KP = (int)((K + 31) & ~int64_t(31));
+            const int TG = NT / KP;
+            const int kk = tid % KP, tg = tid / KP;
+            double acc = 0.0;
+            if (tg < TG && kk < K) {
+                const double* col = sm.rbuf + off + (kb - k0) + kk;
+                for (int t = tg; t < G; t += TG) acc += col[(int64_t)t * kw];
+            }
+            if (TG > 1) {
+                __syncthreads();
+                sm.cf[tid] = acc;
+                __syncthreads();
+                if (tg == 0 && kk < K)
+                    for (int u = 1; u < TG; u++) acc += sm.cf[kk + u * KP];
+            }
+            if (tg == 0 && kk < K) post(kb + kk, acc);
+        }
+        __syncthreads();   // rbuf (the pass ring) and cf free again
+        if (tid == 0) *sm.rcnt = use + 1;
+        __syncthreads();
+        return;
+    }
     for (int64_t kb = k0; kb < k1; kb += NT) {
         const uint64_t c0 = dt ? (uint64_t)clock64() : 0;
         const int64_t K = (k1 - kb < NT) ? (k1 - kb) : NT;
@@ -847,6 +892,7 @@ constexpr int64_t kRingD = (int64_t)kWStg * kWStgD > (int64_t)kNStg * kStgD ? (i
                                                                             : (int64_t)kNStg * kStgD;
 static_assert((int64_t)kNStg * kStgD + kSolveDoubles <= kRingD, "back-sweep ring after the narrow ring");
 static_assert(2 * CH <= 2 * RCH, "x staging of the back sweep in the row accumulators");
+static_assert(kRBufD <= kRingD, "reduce_partials staging inside the pass rings");
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
 
@@ -1190,6 +1236,30 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
         [&](int kb, int ra, int rb, const double* slot) {
             const int k = kb * PW + 2 * tc;
             const int PST = wide_pst(src);
+            // every row of the stage covers the block's valid columns (SrcY: row r has
+            // columns [0, min(r + 1, P))): no per-row masks
+            if (src.cs(ra) == 0 && src.ce(ra) >= min(kb * PW + PW, P)) {
+                if (k < P) {
+                    const bool two = (k + 1 < P);
+                    const double* sp = slot + 2 * tc;
+                    const double* cp = sm.cf + (ra - cb);
+                    const double* cp2 = cf2 + (ra - cb);
+#pragma unroll 7
+                    for (int q = 0; q < rb - ra; q++) {
+                        const double2 y = *reinterpret_cast<const double2*>(sp + q * PST);
+                        const double c = cp[q];
+                        const double y1 = two ? y.y : 0.0;
+                        a0 = fma(y.x, c, a0);
+                        a1 = fma(y1, c, a1);
+                        if (TWO) {
+                            const double cx = cp2[q];
+                            b0 = fma(y.x, cx, b0);
+                            b1 = fma(y1, cx, b1);
+                        }
+                    }
+                }
+                return;
+            }
             for (int r = ra; r < rb; r++) {
                 const int lo = src.cs(r), hi = src.ce(r);
                 if (k + 1 >= lo && k < hi) {
@@ -1246,6 +1316,9 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     // the back-sweep ring sits after the narrow ring (the single-CTA look-ahead streams the
     // narrow ring while the back sweep runs) and aliases the wide ring (never in use together)
     sm.bring = ring_base + (int64_t)kNStg * kStgD;
+    sm.rbuf = ring_base;
+    sm.rbar = sm.mbar + 26;
+    sm.rcnt = reinterpret_cast<uint32_t*>(sm.mbar + 25);
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing + kNStg; k++) mbar_init(sm.mbar + k, 1);
         for (int k = 0; k < kWStg; k++) {
@@ -1255,6 +1328,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         mbar_init(sm.vbar, 1);
         mbar_init(sm.vbar + 1, 1);
         sm.vuse[0] = sm.vuse[1] = 0;
+        mbar_init(sm.mbar + 26, 1);
+        *reinterpret_cast<uint32_t*>(sm.mbar + 25) = 0;
         fence_mbar_init();
     }
     __syncthreads();
@@ -1268,6 +1343,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     // the stream timers in prof slots 12-15: R1 partials, R1 rest, R2 scalars, R2 partials)
     const bool dsub = kWideDebug && (a.prof != nullptr) && threadIdx.x == 0 && (int)blockIdx.x == a.g_cta0[0] + a.prof_sel;
     uint64_t dtim[4] = {0, 0, 0, 0};
+    uint64_t dA = 0;   // debug (TINV_DBG bit 1): SM clock at the exit of pass A's barrier
     auto dclk = [&]() -> uint64_t { return dsub ? (uint64_t)clock64() : 0; };
     const Ring rg{ring_base, sm.mbar + kRing, &rph, timing0 ? ntim : nullptr};
     uint32_t wiss = 0, wuse = 0;   // wide ring stage counters (issued: warp 0; used: all)
@@ -1418,6 +1494,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         if (tid == 0) mst(S + cg * SST + SSlots::X2, x2);
                     }
                     gsync();
+                    if (kWideDebug && (a.dbg & 2)) dA = dclk();
                     PH(1);
                 }
                 // ---------------- R1: g = sum_r partials (look-ahead: columns < p from the
@@ -1430,7 +1507,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         part_uniform(0, p - 1, cg, Gt, k0, k1);
                         reduce_partials(sm, ws.P2, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
                         const uint64_t q1 = dclk();
-                        const bool dla = dsub && !(a.dbg & 1);
+                        const bool dla = dsub && !(a.dbg & 3);
                         if (dla) dtim[0] += q1 - q0;
                         const double gl = reduce_slot(sm, S, Gt, SSlots::GPN);
                         if (r == 0 && tid == 0) st(ws.g + p - 1, gl);   // every rank, its own replica
@@ -1439,7 +1516,18 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         part_uniform(0, p, cg, Gt, k0, k1);
                         reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
                         const uint64_t q1 = dclk();
-                        if (dsub) dtim[0] += q1 - q0;
+                        if (kWideDebug && (a.dbg & 2)) {   // entry, reduce, rest, an extra barrier (every CTA)
+                            __syncthreads();
+                            const uint64_t q2 = dclk();
+                            gsync();
+                            if (dsub && dA) {
+                                dtim[0] += q0 - dA;
+                                dtim[1] += q1 - q0;
+                                dtim[2] += q2 - q1;
+                                dtim[3] += dclk() - q2;
+                            }
+                            dA = 0;
+                        } else if (dsub) dtim[0] += q1 - q0;
                         if (kWideDebug && (a.dbg & 1)) {   // experiment: the same reduction again
                             reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks,
                                             dsub ? dtim + 2 : nullptr);
@@ -1548,7 +1636,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 const double y0 = u0 - c;
                 const double* yrow = Y + y_row_off(p, m);
                 const uint64_t q2m = dclk();
-                if (dsub && !(a.dbg & 1)) dtim[2] += q2m - q2s;
+                if (dsub && !(a.dbg & 3)) dtim[2] += q2m - q2s;
                 {
                     int64_t k0, k1;
                     part_uniform(0, p, cg, Gt, k0, k1);
@@ -1559,7 +1647,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                         [&](int64_t k, double v) { mst(ws.s + k, v - c * ld(yrow + k)); }, rks);
                     }
                 }
-                if (dsub) dtim[3] += dclk() - q2m;
+                if (dsub && !(a.dbg & 2)) dtim[3] += dclk() - q2m;
                 gsync();
                 PH(5);
                 // ---------------- TN: [Ts, h] = T_p [s, yrow]; column p of T and Y; x'

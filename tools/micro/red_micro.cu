@@ -70,10 +70,13 @@ __global__ void __launch_bounds__(NT, 1) kern(double* P, int64_t mc, int p, doub
         for (int k = threadIdx.x; k < p; k += NT) st(P + (int64_t)r * mc + k, (double)(k + r + it));
         uint64_t t1 = gt();
         if (evict) {
-            int64_t per = nbig / G;
-            const double2* b = reinterpret_cast<const double2*>(big + per * r);
+            // touch 200 MB per rep spread over the whole buffer: 64 KB from every page-sized stride
+            const int64_t npg = nbig / (1 << 18);   // 2 MB pages
             double s = 0;
-            for (int64_t i = threadIdx.x; i < per / 2; i += NT) { double2 v = __ldcs(b + i); s += v.x + v.y; }
+            for (int64_t pg = r; pg < npg; pg += G) {
+                const double2* b = reinterpret_cast<const double2*>(big + pg * (1 << 18) + ((it * 8192) & ((1 << 18) - 1)));
+                for (int64_t i = threadIdx.x; i < 4096; i += NT) { double2 v = __ldcs(b + i); s += v.x + v.y; }
+            }
             sink += s;
         }
         uint64_t t2 = gt();
@@ -93,11 +96,11 @@ __global__ void __launch_bounds__(NT, 1) kern(double* P, int64_t mc, int p, doub
     if (sink == 12345.678) g[0] = sink;
 }
 
-int main() {
+int main(int argc, char** argv) {
     const int G = 148, reps = 200;
     int64_t mc = 8000;
     double *P, *g, *big;
-    int64_t nbig = 200ll << 20 >> 3;   // 200 MB
+    int64_t nbig = (argc > 1 ? atoll(argv[1]) : 200ll) << 20 >> 3;   // MB
     unsigned int* cnt;
     unsigned long long* tm;
     cudaMalloc(&P, sizeof(double) * G * mc);

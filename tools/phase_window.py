@@ -13,7 +13,7 @@ from paper_1209_1910_b200.tinv import Tinv  # noqa: E402
 
 cfg = sys.argv[1]
 wins = [tuple(int(x) for x in a.split(":")) for a in sys.argv[2:]] or [(500, 600), (3950, 4050), (7400, 7500)]
-d, e, w = W.problem(cfg, None)
+d, e, w = W.problem(cfg, int(os.environ["PW_N"]) if os.environ.get("PW_N") else None)
 n = len(d)
 dev = torch.device("cuda:0")
 args = [torch.tensor(a, dtype=torch.float64, device=dev) for a in (d, e, w)]
