@@ -62,7 +62,7 @@ constexpr int64_t kPfDist = 2048;   // doubles prefetched ahead inside a row (16
 constexpr double kL2KeepBytes = 48e6;   // Y_p beyond this: single-use streams are evict_first
 
 struct SSlots {  // scalar partial slots per CTA (ws.S[r*SST + slot])
-    enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4, GPN = 5, X2N = 6, Q1 = 7, FA = 8, FB = 9 };
+    enum { U2 = 0, X2 = 1, Q2 = 2, QINF = 3, QARG = 4, GPN = 5, X2N = 6, Q1 = 7, FA = 8, FB = 9, MG0 = 10, MG1 = 11 };
 };
 constexpr int SST = 16;   // scalar slots per CTA
 
@@ -259,7 +259,7 @@ __device__ __forceinline__ void rowdots(int64_t i0, int64_t i1, int64_t P, const
 // Thread t owns a column pair (2 doubles, 16-byte loads) and a subset of the rows; the
 // coefficients of a row chunk are staged in shared memory.  Returns sum coef(i)^2.
 __device__ double colacc(const Smem& sm, const double* __restrict__ Y, int64_t m, int64_t i0, int64_t i1,
-                         int64_t P, const double* cp, int64_t cs, double* out) {
+                         int64_t P, const double* cp, int64_t cs, double* out, int64_t ovr = -1, double ovv = 0.0) {
     const int tid = threadIdx.x;
     const int CPT = (P > 0) ? min(NT, pow2ceil((int)((P + 1) / 2))) : NT;
     const int RS = NT / CPT;
@@ -273,7 +273,7 @@ __device__ double colacc(const Smem& sm, const double* __restrict__ Y, int64_t m
     for (int64_t rc0 = i0; rc0 < i1; rc0 += CFCH) {
         const int64_t rc1 = (i1 - rc0 > CFCH) ? rc0 + CFCH : i1;
         for (int64_t i = rc0 + tid; i < rc1; i += NT) {
-            const double c = ld(cp + i * cs);
+            const double c = (i == ovr) ? ovv : ld(cp + i * cs);   // ovr: coefficient of one row replaced
             sm.cf[i - rc0] = c;
             c2 = fma(c, c, c2);
         }
@@ -1193,7 +1193,8 @@ __device__ void wide_rowdots(const Smem& sm, const WRing& rg, const Src& src, in
 template <bool TWO = false, class Src>
 __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, int r0, int r1, const double* coef,
                               int P, double* out, bool reverse_blocks, uint64_t pol, bool accum = false,
-                              const double* coef2 = nullptr, double* out2 = nullptr, double* c2b = nullptr) {
+                              const double* coef2 = nullptr, double* out2 = nullptr, double* c2b = nullptr,
+                              int ovr = -1, double ovv = 0.0) {
     const int tid = threadIdx.x, tc = tid - 32;   // consumer thread index
     double c2 = 0.0, c2x = 0.0;
     double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
@@ -1220,7 +1221,7 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
         [&](int c0, int c1) {
             cb = c0;
             for (int r = c0 + tid; r < c1; r += NT) {
-                const double c = ld(coef + r);
+                const double c = (r == ovr) ? ovv : ld(coef + r);   // ovr: coefficient of one row replaced
                 sm.cf[r - c0] = c;
                 c2 = fma(c, c, c2);
                 if (TWO) {
@@ -1402,6 +1403,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
 
     const int64_t n = a.n;
     const int64_t n2v = (n + 1) & ~int64_t(1);   // vector stride of X1c
+    // reorthogonalisation (tinv_set_reorth): 0 the reduced compact-WY step of §3.3.2, 1 classical
+    // MGS (Alg. 1; single-rank groups), 2 the ordinary compact-WY sequence of
+    // §3.3.1 (Y^T y by a pass of its own)
+    const int mode = a.reorth;
     const double thr = sqrt(0.1 / (double)n);
     double* __restrict__ Y = ws.Y;
     double* __restrict__ S = ws.S;
@@ -1414,12 +1419,12 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         const int64_t m = a.cstart[cl + 1] - j1;
         const int64_t m2 = (m + 1) & ~int64_t(1);
         const bool narrow = (m <= kNarrowM) && a.nstg > 0;
-        const bool la_ok = (G > 1) || narrow;   // look-ahead can overlap the back sweep
+        const bool la_ok = ((G > 1) || narrow) && mode != 1;   // look-ahead can overlap the back sweep
         double* __restrict__ Tc = ws.Tc;
         double* __restrict__ Tr = ws.Tr;
 
         // ================= first reflector from the accepted z_{j1} (p = 0)
-        {
+        if (mode != 1) {
             const double* z = a.Z + j1 * a.ldz;
             int64_t i0, i1;
             part_uniform(0, n, r, G, i0, i1);
@@ -1471,6 +1476,53 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             part_tn(p, cg, Gt, ptn0, ptn1, a.piece_cost);
             part_rows_weighted(n, p + 1, cg, Gt, pd0, pd1, a.piece_cost);
             while (!done) {
+                double c = 1.0;   // the reflector's c (reduced / ordinary); 1 for MGS (r = q)
+                int64_t dq0 = pd0, dq1 = pd1;   // rows of q that this CTA holds after the step
+                if (mode == 1) {
+                    // ---------------- MGS (Alg. 1 l.10-12): x <- x - <x, z_i> z_i
+                    // for the cluster's accepted z_{j1} .. z_{j-1} in order; one group barrier per
+                    // z_i (the O(m) synchronisations per vector of Table 1).  The
+                    // partial dot of z_{i+1} is fused into the update with z_i; slots MG0/MG1
+                    // alternate so a fast CTA never overwrites a partial still being summed.
+                    part_uniform(0, n, cg, Gt, dq0, dq1);
+                    const int R = (int)(dq1 - dq0);
+                    double* xv = (R <= CFCH) ? sm.cf : ws.q + dq0;   // this CTA's rows of x
+                    double x2 = 0.0, dp = 0.0;
+                    const double* z0 = a.Z + j1 * a.ldz + dq0;
+                    for (int q = tid; q < R; q += NT) {
+                        const double xi = ld(xcur + (dq0 + q) * xs);
+                        xv[q] = xi;
+                        x2 = fma(xi, xi, x2);
+                        dp = fma(xi, ld(z0 + q), dp);
+                    }
+                    x2 = block_sum<NT>(x2, sm.red);
+                    dp = block_sum<NT>(dp, sm.red);
+                    if (tid == 0) {
+                        st(S + cg * SST + SSlots::X2, x2);
+                        st(S + cg * SST + SSlots::MG0, dp);
+                    }
+                    for (int64_t i = 0; i < p; i++) {
+                        gsync();
+                        const double dot = reduce_slot(sm, S, Gt, (i & 1) ? SSlots::MG1 : SSlots::MG0);
+                        const double* zi = a.Z + (j1 + i) * a.ldz + dq0;
+                        const double* zn = a.Z + (j1 + i + 1) * a.ldz + dq0;
+                        const bool nxt = i + 1 < p;
+                        double dn = 0.0;
+                        for (int q = tid; q < R; q += NT) {
+                            const double xi = fma(-dot, ld(zi + q), xv[q]);
+                            xv[q] = xi;
+                            if (nxt) dn = fma(xi, ld(zn + q), dn);
+                        }
+                        if (nxt) {
+                            dn = block_sum<NT>(dn, sm.red);
+                            if (tid == 0) st(S + cg * SST + ((i & 1) ? SSlots::MG0 : SSlots::MG1), dn);
+                        }
+                    }
+                    if (xv == sm.cf)
+                        for (int q = tid; q < R; q += NT) st(ws.q + dq0 + q, xv[q]);
+                    __syncthreads();
+                    PH(4);
+                } else {
                 if (!use_la && !use_a2) {
                     // ---------------- A: partial g = Y_p^T x, ||x||^2
                     {
@@ -1589,8 +1641,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                             });
                         u2 = block_sum<NT>(u2, sm.red);
                         if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
-                        // second read of Yhat, blocks in reverse order (the last ones are in L2)
-                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)cg * mc, true, pol_once);
+                        // second read of Yhat, blocks in reverse order (the last ones are in L2);
+                        // the ordinary sequence forms Y^T y in a pass of its own after R2
+                        if (mode != 2)
+                            wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)cg * mc, true, pol_once);
                     } else {
                         stage_vec(sm, ws.gp, p);
                         rowdots(i0, i1, p, sm.vs,
@@ -1603,7 +1657,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                 });
                         u2 = block_sum<NT>(u2, sm.red);
                         if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
-                        colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)cg * mc);
+                        if (mode != 2) colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)cg * mc);
                     }
                 }
                 gsync();
@@ -1631,13 +1685,26 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     continue;
                 }
                 if (un <= (double)n * kEps * sqrt(x2)) flagged = true;
-                const double c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
+                c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
                 const double tt = 1.0 / (c * c - u0 * c);
                 const double y0 = u0 - c;
                 const double* yrow = Y + y_row_off(p, m);
                 const uint64_t q2m = dclk();
                 if (dsub && !(a.dbg & 3)) dtim[2] += q2m - q2s;
-                {
+                if (mode == 2) {
+                    // ordinary sequence (§3.3.1): s = Y_p^T y_p by a pass of its
+                    // own over rows p..n-1 (y_p = uhat with its first entry y_0), then reduced
+                    int64_t i0, i1, k0, k1;
+                    part_uniform(p, n, cg, Gt, i0, i1);
+                    if (p > kNarrowM)
+                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)cg * mc, false,
+                                    pol_once, false, nullptr, nullptr, nullptr, (int)p, y0);
+                    else
+                        colacc(sm, Y, m, i0, i1, p, ws.u, 1, P_ + (int64_t)cg * mc, p, y0);
+                    gsync();
+                    part_uniform(0, p, cg, Gt, k0, k1);
+                    reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.s + k, v); }, rks);
+                } else {
                     int64_t k0, k1;
                     part_uniform(0, p, cg, Gt, k0, k1);
                     if (zero_u) {
@@ -1713,13 +1780,14 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 }
                 gsync();
                 PH(6);
+                }   // reduced / ordinary compact-WY step
                 // ---------------- D: q = Y_{p+1} x' - e_p, norms and argmax
                 Aff1 fex{1.0, 0.0};   // forward-sweep state kept from D to the solve
                 int64_t fs0 = 0, fta = 0, ftb = 0;
                 bool flast = false;
                 {
                     int64_t i0, i1;
-                    i0 = pd0; i1 = pd1;
+                    i0 = dq0; i1 = dq1;   // D's rows (MGS: the rows of the projection)
                     double q2 = 0.0, q1 = 0.0, qinf = -1.0;
                     int64_t qarg = 0;
                     if (tid == 0) {   // this CTA's factor rows (forward sweep below, back sweep)
@@ -1743,7 +1811,15 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         if (aq > qinf || (aq == qinf && i < qarg)) { qinf = aq; qarg = i; }
                     };
                     auto lend = [&](int64_t i) -> int64_t { return (i + 1 < p + 1) ? i + 1 : p + 1; };
-                    if (narrow) {
+                    if (mode == 1) {   // MGS: q (the projected x) is in place; norms and argmax
+                        for (int64_t i = i0 + tid; i < i1; i += NT) {
+                            const double qi = ld(ws.q + i);
+                            q2 = fma(qi, qi, q2);
+                            const double aq = fabs(qi);
+                            q1 += aq;
+                            if (aq > qinf || (aq == qinf && i < qarg)) { qinf = aq; qarg = i; }
+                        }
+                    } else if (narrow) {
                         stage_vec(sm, ws.xp, p + 1);
                         auto lendn = [&](int i) -> int { return (i + 1 < p + 1) ? i + 1 : (int)p + 1; };
                         // with the look-ahead, the next vector's x^(1) rides along as the stage's
@@ -1830,6 +1906,24 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 double qinf;
                 int64_t qarg;
                 reduce_argmax(sm, S, Gt, qinf, qarg);
+                if (mode == 1) {   // MGS: degenerate projection (reading 16) -> restart
+                    const double x2 = reduce_slot(sm, S, Gt, SSlots::X2);
+                    if (sqrt(q2) <= (double)n * kEps * sqrt(x2)) {
+                        if (restart < kMaxRestart) {
+                            restart++;
+                            its++;
+                            kin = 1;
+                            passes = 0;
+                            if (r == 0) cta_solve(a, ws, j, 1, restart, sm, mark, mbph);
+                            gsync();
+                            PH(10);
+                            xcur = ws.x;
+                            xs = 1;
+                            continue;
+                        }
+                        flagged = true;
+                    }
+                }
                 if (fabs(c) * qinf >= thr) passes++;
                 if (passes >= kPasses) done = true;
                 else if (kin >= kMaxIts) { done = true; flagged = true; }
@@ -1859,7 +1953,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     // with the solve's x) streams Y_p behind the back sweep, band by band as the
                     // rows become final, together with the look-ahead Y_p^T x^(1)_{p+1}: one read
                     // of Y_p for both (PAPER.md:534-535 for both vectors)
-                    const bool a2 = a.a2 && (NR == 1) && (G > 1) && !narrow && p > kNarrowM;
+                    const bool a2 = a.a2 && (NR == 1) && (G > 1) && !narrow && p > kNarrowM && mode != 1;
                     if (r == 0) {
                         if (la) {   // CTA 0 of every rank solves; its look-ahead partial is zero
                             for (int64_t k = tid; k < p; k += NT) st(ws.P2 + (int64_t)cg * mc + k, 0.0);

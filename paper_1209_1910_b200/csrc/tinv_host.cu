@@ -216,7 +216,8 @@ struct Schedule {
 // Clusters [c_lo, c_hi) with m >= 2 -> CTA groups.  Many clusters: one CTA per group and
 // LPT over groups by cost m^2 n.  Few clusters: one group per cluster, CTAs shared in
 // proportion to cost, capped so a CTA keeps >= 256 KB of Y per pass.
-Schedule make_schedule(const int* cs, int c_lo, int c_hi, int64_t n, int nctas, const std::vector<char>* skip = nullptr) {
+Schedule make_schedule(const int* cs, int c_lo, int c_hi, int64_t n, int nctas, const std::vector<char>* skip = nullptr,
+                       int gmax = 1 << 30) {
     Schedule s;
     std::vector<int> cl;
     for (int c = c_lo; c < c_hi; c++)
@@ -253,7 +254,7 @@ Schedule make_schedule(const int* cs, int c_lo, int c_hi, int64_t n, int nctas, 
     for (int i = 0; i < nc; i++) {
         int c = cl[i];
         double m = cs[c + 1] - cs[c];
-        int cap = (int)std::max(1.0, std::min((double)nctas, std::ceil(m * (double)n * 8.0 / (256.0 * 1024.0))));
+        int cap = (int)std::max(1.0, std::min((double)std::min(nctas, gmax), std::ceil(m * (double)n * 8.0 / (256.0 * 1024.0))));
         int want = (int)std::floor(cost(c) / tot * nctas);
         sz[i] = std::max(1, std::min(cap, want));
         used += sz[i];
@@ -709,15 +710,14 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         // the largest clusters first (longest dependent chains)
         std::sort(rgroups.begin(), rgroups.end(), [](const ResGroup& a, const ResGroup& b) { return a.cs > b.cs; });
     }
-    if (h->mgs) {   // MGS (Alg. 1) and the ordinary sequence run in the resident kernel only
-        for (int c = 0; c < nclus; c++)
-            if (cs[c + 1] - cs[c] >= 2 && (rs_real || !resident[c]) && (rs_real || (c >= rlo[h->rank] && c < rhi[h->rank]))) {
-                join_b2();
-                return TINV_ERR_UNSUPPORTED;
-            }
+    if (h->mgs && NRK > 1) {   // MGS / the ordinary sequence: clusters of one rank (no row split)
+        join_b2();
+        return TINV_ERR_UNSUPPORTED;
     }
+    // MGS pays one group barrier per accepted vector: its groups are kept small (TINV_MGS_G CTAs)
+    const int gmax = (h->mgs == 1) ? std::max(1, getenv("TINV_MGS_G") ? atoi(getenv("TINV_MGS_G")) : 16) : (1 << 30);
     Schedule sc = rs_real ? make_schedule(cs, 0, nclus, n, nctas_max)
-                          : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max, &resident);
+                          : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max, &resident, gmax);
     if (rs_virtual && sc.size.size() == 1) {   // split the group into NRK equal virtual ranks
         const int Gv = std::max(1, sc.size[0] / NRK);   // >= 1 CTA per virtual rank (small clusters)
         const int cl = sc.clist[0];
@@ -1038,6 +1038,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 16;
         ca.poll_ns = getenv("TINV_POLLNS") ? atoi(getenv("TINV_POLLNS")) : 0;
         ca.dbg = getenv("TINV_DBG") ? atoi(getenv("TINV_DBG")) : 0;
+        ca.reorth = h->mgs;
         unsigned long long* pcta = nullptr;
         if (getenv("TINV_PROF_CTA")) {   // debug only (not the product path): per-CTA phase busy times
             CK(cudaMalloc(&pcta, sizeof(unsigned long long) * 16 * sc.nctas));

@@ -165,6 +165,7 @@ struct CwyArgs {
     int band_ch;             // sweep chunks (256 rows) per published band (TINV_BANDCH)
     int poll_ns;             // back-off of the band polls in ns (TINV_POLLNS)
     int dbg;                 // debug build experiments (TINV_DBG bits)
+    int reorth;              // 0 reduced compact WY (§3.3.2), 1 classical MGS (Alg. 1), 2 ordinary compact WY (§3.3.1)
     unsigned long long* prof_cta;   // debug: per-CTA busy time before each phase's barrier [cta*16 + phase], or NULL
 };
 

@@ -576,16 +576,87 @@ def test_mgs_cluster_sizes(handle, torch, n, sizes):
     assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
 
 
-def test_mgs_unsupported_for_wide_clusters(handle, torch):
-    from paper_1209_1910_b200.tinv import TinvError
+@pytest.mark.parametrize("cfg,n", [("cfg4", 600), ("type2", 700), ("cfg3", 1050), ("type1", 2100)])
+def test_mgs_wide_clusters(handle, torch, cfg, n):
+    """Clusters too wide for the resident kernel run MGS in the persistent kernel (one group
+    barrier per accepted vector, small CTA groups): parity with the MGS oracle (Alg. 1) and,
+    where the vectors are determined, with the compact-WY path."""
+    d, e, w = W.problem(cfg, n)
+    Zm = _mgs_parity(handle, torch, d, e, w)
+    Zc, rc = run_gpu(handle, torch, d, e, w)
+    assert rc == 0
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zm, Zc.cpu().numpy())
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
 
-    d, e, w = W.problem("cfg4", 600)      # one cluster of 600 vectors: not resident
-    handle.set_reorth("mgs")
+
+@pytest.mark.parametrize("mode", ["mgs", "ordinary"])
+def test_reorth_modes_restart_persistent(handle, torch, mode):
+    """Reading 16 in the persistent kernel's comparison modes (set_resident(False) puts the
+    narrow cluster there): T = diag(1, 200, .., 600) with three shifts on eigenvalue 1 --
+    vector 1 restarts twice and is flagged on both sides (rc = 1), the same Z and iteration
+    histogram as the oracle of that mode (MGS: Alg. 1; ordinary: the compact-WY oracle)."""
+    d = np.array([1.0, 200.0, 300.0, 400.0, 500.0, 600.0])
+    e = np.zeros(5)
+    w = np.array([1.0, 1.0, 1.0, 400.0, 500.0, 600.0])
+    Zo, info, its = O.eigvecs(d, e, w, seed=1, return_iters=True, mgs=(mode == "mgs"))
+    assert info == 1 and its[1] > 2, (info, its)
+    handle.set_resident(False)
+    handle.set_reorth(mode)
     try:
-        with pytest.raises(TinvError, match="-105"):
-            run_gpu(handle, torch, d, e, w)
+        Zg, rc = run_gpu(handle, torch, d, e, w)
+        hist = _iters_of(handle)
     finally:
         handle.set_reorth("cwy")
+        handle.set_resident(True)
+    assert rc == info, (rc, info)
+    assert hist == list(np.bincount(its, minlength=8)[:8]), (hist, its)
+    Zh = Zg.cpu().numpy()
+    # MGS: the kept iterate of the flagged vector 1 is x - <x, z_0> z_0 with x ~ 1e15 e_0, i.e.
+    # rounding noise in the e_0 direction (one Gram-Schmidt projection of a vector inside the
+    # span); it and vector 2 (projected against it) are not determined -- only unit norm.
+    # The compact-WY step forms q = Y x' - e_p instead and agrees to 1e-10 everywhere.
+    cols = [0, 3, 4, 5] if mode == "mgs" else range(6)
+    for k in cols:
+        assert np.abs(Zh[:, k] - Zo[:, k]).max() <= 1e-10, k
+    assert np.abs(np.linalg.norm(Zh, axis=0) - 1).max() <= 1e-14
+
+
+@pytest.mark.parametrize("mode", ["mgs", "ordinary"])
+@pytest.mark.parametrize("cfg,n", [("cfg2", 1200), ("cfg1", None)])
+def test_reorth_modes_persistent_narrow(handle, torch, mode, cfg, n):
+    """The comparison modes' persistent-kernel code for narrow clusters (m <= 64, forced off
+    the resident kernel) against the oracle of the mode."""
+    d, e, w = W.problem(cfg, n)
+    handle.set_resident(False)
+    handle.set_reorth(mode)
+    try:
+        Zg, rc = run_gpu(handle, torch, d, e, w)
+    finally:
+        handle.set_reorth("cwy")
+        handle.set_resident(True)
+    assert rc == 0
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
+    Zo, info = O.eigvecs(d, e, w, seed=1, mgs=(mode == "mgs"))
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zg.cpu().numpy(), Zo)
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+
+
+def test_reorth_modes_unsupported_for_row_split(handle, torch):
+    from paper_1209_1910_b200.tinv import TinvError
+
+    d, e, w = W.problem("cfg4", 600)      # one wide cluster, split over 2 virtual ranks
+    handle.set_virtual_ranks(2)
+    try:
+        for mode in ("mgs", "ordinary"):
+            handle.set_reorth(mode)
+            try:
+                with pytest.raises(TinvError, match="-105"):
+                    run_gpu(handle, torch, d, e, w)
+            finally:
+                handle.set_reorth("cwy")
+    finally:
+        handle.set_virtual_ranks(1)
     Z, rc = run_gpu(handle, torch, d, e, w)   # the handle still works in cWY mode
     assert rc == 0
 
@@ -595,7 +666,8 @@ def test_mgs_unsupported_for_wide_clusters(handle, torch):
 # sequence (Y^T y by its own pass); equals the compact-WY oracle within tolerance.
 
 @pytest.mark.parametrize("cfg,n,sizes", [("cfg2", 1200, None), ("clustered", 2000, [60, 33, 17, 9, 2]),
-                                         ("type3", 420, None)])
+                                         ("type3", 420, None), ("cfg4", 600, None), ("type2", 700, None),
+                                         ("cfg3", 1050, None), ("clustered", 5000, [300, 40, 9])])
 def test_ordinary_cwy_path_parity(handle, torch, cfg, n, sizes):
     d, e, w = _clustered(n, sizes) if sizes else W.problem(cfg, n)
     handle.set_reorth("ordinary")
