@@ -176,10 +176,23 @@ int tinv_set_resident(tinv_t h, int enable);
  * ordinary sequence of §3.3.1 (with the T_j erratum fixed; SURVEY §8(f)
  * row 4): Y^T y_j by a pass of its own instead of the reduced sequence's reuse of the BC pass.
  * Same factorization, start vectors, stopping rule and restarts; the vectors agree with mode 0
- * up to rounding.  Modes 1 and 2 run in the resident kernel only: tinv_eigvecs returns
- * TINV_ERR_UNSUPPORTED when a cluster does not fit it (m > 64 or n > 4096).  Returns 0, -2
- * for another mode, TINV_ERR_HANDLE. */
+ * up to rounding.  Narrow clusters run them in the resident kernel, wide ones in the
+ * persistent kernel (MGS with one group barrier per accepted vector on groups of at most
+ * TINV_MGS_G = 16 CTAs); a cluster row-split over ranks (nranks > 1 or virtual ranks) makes
+ * tinv_eigvecs return TINV_ERR_UNSUPPORTED in modes 1 and 2.  Returns 0, -2 for another mode,
+ * TINV_ERR_HANDLE. */
 int tinv_set_reorth(tinv_t h, int mode);
+
+/* Blocked look-ahead (Eq. (4), Alg. 3 PAPER.md:314-334,
+ * the u-step PAPER.md:530-538): for wide clusters (m > 64) of single-rank groups, at the start
+ * of every block of b consecutive vectors k .. k+b-1 the accepted reflectors are applied to
+ * the block's first iterates at once, U = (I - Y_k T_k^T Y_k^T) X = X - Y_k (T_k^T (Y_k^T X)),
+ * as two skinny GEMMs and a TRMM (fp64, one pass over Y_k for each GEMM instead of two per
+ * vector); vector p of the block then applies only the reflectors k .. p-1 of its own block
+ * to its column of U.  Same results up to rounding.  b in 2..8 (larger values are clamped),
+ * 0 or 1 = off (default; the environment variable TINV_LAB overrides).  Compact-WY modes only
+ * (ignored with MGS).  Returns 0 or TINV_ERR_HANDLE. */
+int tinv_set_lookahead(tinv_t h, int b);
 int tinv_get_stats(tinv_t h, tinv_stats_t* out);
 
 /* Number of exported entry points (for the loader test). */

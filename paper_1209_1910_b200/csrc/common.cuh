@@ -141,6 +141,7 @@ __host__ __device__ __forceinline__ int64_t bix(int64_t i, int64_t j, int64_t n)
 // (m <= kNarrowM) use a uniform row stride roundup(m, 2) instead (the padding of the leading
 // triangle is < m^2/2 doubles), so any row range is one contiguous span with a fixed stride.
 constexpr int kNarrowM = 64;
+constexpr int kLabMax = 8;   // largest block of the blocked look-ahead (cwy.cu)
 __host__ __device__ __forceinline__ int64_t y_row_off(int64_t i, int64_t m) {
     if (m <= kNarrowM) return i * ((m + 1) & ~int64_t(1));
     auto tri = [](int64_t r) -> int64_t {  // sum_{r'<r} roundup(r'+1, 2)

@@ -1294,6 +1294,201 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
     return c2;
 }
 
+// ---------------------------------------------------------------- blocked look-ahead
+// SURVEY §8(f) row 2 (Eq. (4), Alg. 3, u-step PAPER.md:530-538):
+// for the block of NV <= kLabMax upcoming first iterates X = [x^(1)_k .. x^(1)_{k+NV-1}] (all
+// computed by the batched solve), apply the k accepted reflectors at once:
+//   BL1  G  = Y_k^T X            (k x NV)  columns of Y_k split over the CTAs (whole dots, no partials)
+//   BL2  G' = T_k^T G            (k x NV)  columns of T (rows of T^T) split over the CTAs
+//   BL3  U  = X - Y_k G'         (n x NV, rows >= k)  rows split over the CTAs
+// Skinny GEMMs: 2 NV flops per 8 bytes of Y (<= 2 flop/B at NV = 8), far below the fp64 FMA
+// peak per byte of HBM, so they are DFMA loops on staged operands, not fp64 tensor-core tiles.
+// Operands written inside this kernel are read through L2 (ld.cg).
+
+// Stage nseg contiguous global segments seg(s)[0, len) (16-byte aligned, produced in this kernel)
+// into shared memory dst + s * dstride: one TMA bulk copy per segment (length rounded up to an
+// even count), all completed on sm.rbar; every thread returns after they landed.
+template <class Seg>
+__device__ __forceinline__ void tma_stage(const Smem& sm, int nseg, Seg seg, int64_t len, double* dst, int64_t dstride) {
+    const int tid = threadIdx.x;
+    const uint32_t use = *sm.rcnt;
+    const int64_t lw = (len + 1) & ~int64_t(1);
+    __syncthreads();
+    if (tid < nseg && lw > 0) {
+        fence_proxy_async_global();
+        mbar_add_tx(sm.rbar, (uint32_t)(lw * 8));
+        bulk_g2s(dst + (int64_t)tid * dstride, seg(tid), (uint32_t)(lw * 8), sm.rbar);
+    }
+    __syncthreads();
+    if (tid == 0) mbar_arrive(sm.rbar);
+    mbar_wait(sm.rbar, use & 1u);
+    __syncthreads();
+    if (tid == 0) *sm.rcnt = use + 1;
+    __syncthreads();
+}
+
+// columns [a, b) of [0, k) balanced by their row counts (column c of Y_k has rows c .. n-1)
+__device__ __forceinline__ void part_cols_tri(int64_t k, int64_t n, int r, int G, int64_t& a, int64_t& b) {
+    auto cum = [n](int64_t c) -> int64_t { return c * n - c * (c - 1) / 2; };
+    const int64_t W = cum(k);
+    a = (r == 0) ? 0 : bsearch_cum(0, k, (W * r) / G, cum);
+    b = (r == G - 1) ? k : bsearch_cum(0, k, (W * (r + 1)) / G, cum);
+    a &= ~int64_t(1);   // column pairs (16-byte loads): boundaries even
+    b = (r == G - 1) ? k : (b & ~int64_t(1));
+}
+
+// BL1 on columns [c0, c1): G[v * ldg + c] = sum_{i >= c} Y[i][c] X_v[i]; also ||X_v||^2 over
+// rows [x0, x1) into xsq[v] (this CTA's partial).  Scratch: `scr` (>= 8192 + 4096 doubles).
+template <int NV>
+__device__ void lab_gemm1(const Smem& sm, const double* __restrict__ Y, int64_t m, int64_t n, int64_t c0, int64_t c1,
+                          const double* X, int64_t xst, int nv, double* G, int64_t ldg, double* scr, int64_t x0,
+                          int64_t x1, double* xsq) {
+    const int tid = threadIdx.x;
+    // ||X_v||^2 partials (rows [x0, x1))
+    {
+        double q[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) q[v] = 0.0;
+        for (int64_t i = x0 + tid; i < x1; i += NT)
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                const double xv = (v < nv) ? ld(X + v * xst + i) : 0.0;
+                q[v] = fma(xv, xv, q[v]);
+            }
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            const double t = block_sum<NT>(q[v], scr + 12288);
+            if (tid == 0) xsq[v] = t;
+        }
+    }
+    if (c1 <= c0) return;
+    const int npair = (int)((c1 - c0 + 1) / 2);
+    const int CW = min(NT, pow2ceil(npair));   // pair lanes
+    const int RL = NT / CW;                    // row lanes
+    constexpr int XR = 1024;                   // rows of X staged per chunk (XR * NV <= 8192)
+    double* xs = scr;
+    double* red = scr + 8192;
+    for (int pb = 0; pb < npair; pb += CW) {
+        const int cp = pb + tid % CW, rl = tid / CW;
+        const int64_t c = c0 + 2 * (int64_t)cp;
+        const bool act = cp < npair;
+        double acc[2 * NV];
+#pragma unroll
+        for (int u = 0; u < 2 * NV; u++) acc[u] = 0.0;
+        for (int64_t r0 = c0 + 2 * (int64_t)pb; r0 < n; r0 += XR) {
+            const int64_t r1 = (r0 + XR < n) ? r0 + XR : n;
+            // X rows [r0, r1) of the nv vectors by TMA (layout [v][row]); vectors >= nv: zero
+            tma_stage(sm, nv, [&](int v) { return X + v * xst + r0; }, r1 - r0, xs, XR);
+            for (int64_t q = tid; q < (int64_t)(NV - nv) * XR; q += NT) xs[(int64_t)nv * XR + q] = 0.0;
+            __syncthreads();
+            if (act) {
+                constexpr int U = 16;   // 16 independent 16-byte loads per thread in flight
+                for (int64_t ib = r0 + rl; ib < r1; ib += (int64_t)RL * U) {
+                    double2 y[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int64_t i = ib + (int64_t)u * RL;
+                        y[u] = (i < r1 && i >= c) ? ld2(Y + y_row_off(i, m) + c) : make_double2(0.0, 0.0);
+                        if (i == c) y[u].y = 0.0;   // row c holds column c only
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int64_t i = ib + (int64_t)u * RL;
+                        if (i < r1) {
+                            const double* xr = xs + (i - r0);
+#pragma unroll
+                            for (int v = 0; v < NV; v++) {
+                                const double xv = xr[(int64_t)v * XR];
+                                acc[2 * v] = fma(y[u].x, xv, acc[2 * v]);
+                                acc[2 * v + 1] = fma(y[u].y, xv, acc[2 * v + 1]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        // sum the row lanes in order (deterministic)
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 2 * NV; u++) red[(int64_t)u * NT + tid] = acc[u];
+        __syncthreads();
+        if (act && rl == 0) {
+            for (int u = 0; u < 2 * NV; u++) {
+                double t = 0.0;
+                for (int l = 0; l < RL; l++) t += red[(int64_t)u * NT + l * CW + (tid % CW)];
+                const int64_t cc = c + (u & 1);
+                if (cc < c1) st(G + (int64_t)(u >> 1) * ldg + cc, t);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// BL2 / BL3: out_v[r] = base_v(r) - sum_{k in row r} row_r[k] V_v[k] for rows [r0, r1) (warp per
+// row, vectors V staged in shared memory by chunks of CC columns, per-row sums in shared memory).
+//   BL2: rows l of column-packed T (T[0..l][l]), V = G, base = 0       -> G'
+//   BL3: rows i of Y_k (columns 0..k-1),          V = G', base = X_v[i] -> U
+template <int NV, class RowPtr, class RowLen, class Epi>
+__device__ void lab_rowdots(const Smem& sm, int64_t r0, int64_t r1, int64_t P, const double* V, int64_t ldv, int nv,
+                            double* scr, RowPtr rowptr, RowLen rowlen, Epi epi) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int CC = 1024;                    // staged columns per chunk (NV * CC <= 8192)
+    double* vs = scr;
+    double* acc = scr + 8192;                   // [row - r0][NV]
+    const int64_t R = r1 - r0;
+    if (R <= 0) return;
+    for (int64_t rb0 = r0; rb0 < r1; rb0 += 4096 / NV) {   // row blocks whose sums fit `acc`
+        const int64_t rb1 = (rb0 + 4096 / NV < r1) ? rb0 + 4096 / NV : r1;
+        for (int64_t q = tid; q < (rb1 - rb0) * NV; q += NT) acc[q] = 0.0;
+        for (int64_t c0 = 0; c0 < P; c0 += CC) {
+            const int64_t c1 = (c0 + CC < P) ? c0 + CC : P;
+            // the nv vectors' columns [c0, c1) by TMA; vectors >= nv: zero
+            tma_stage(sm, nv, [&](int v) { return V + v * ldv + c0; }, c1 - c0, vs, CC);
+            for (int64_t q = tid; q < (int64_t)(NV - nv) * CC; q += NT) vs[(int64_t)nv * CC + q] = 0.0;
+            __syncthreads();
+            for (int64_t r = rb0 + warp; r < rb1; r += NW) {
+                const int64_t len = rowlen(r);
+                if (len <= c0) continue;
+                const int64_t e1 = (len < c1) ? len : c1;
+                const double* row = rowptr(r);
+                double a[NV];
+#pragma unroll
+                for (int v = 0; v < NV; v++) a[v] = 0.0;
+                constexpr int U = 8;
+                for (int64_t k0 = c0 + 2 * lane; k0 < e1; k0 += 64 * U) {
+                    double2 y[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int64_t k = k0 + 64 * u;
+                        y[u] = (k < e1) ? ld2(row + k) : make_double2(0.0, 0.0);
+                        if (k + 1 >= e1) y[u].y = 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int64_t k = k0 + 64 * u - c0;
+                        if (k0 + 64 * u < e1) {
+#pragma unroll
+                            for (int v = 0; v < NV; v++) {
+                                const double2 g = *reinterpret_cast<const double2*>(vs + v * CC + k);
+                                a[v] = fma(y[u].x, g.x, a[v]);
+                                a[v] = fma(y[u].y, g.y, a[v]);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    const double t = warp_sum(a[v]);
+                    if (lane == 0) acc[(r - rb0) * NV + v] += t;
+                }
+            }
+        }
+        __syncthreads();
+        for (int64_t q = tid; q < (rb1 - rb0) * NV; q += NT) epi(rb0 + q / NV, (int)(q % NV), acc[q]);
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1450,6 +1645,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
 
         // ================= vectors j_c = 1 .. m-1
         bool la_have = false;   // look-ahead of this vector's first pass A is ready
+        // blocked look-ahead: vectors p >= kNarrowM + 1 form blocks of a.lab
+        const bool lab_cl = a.lab > 1 && ws.labU != nullptr && mode != 1 && NR == 1 && !narrow && m > kNarrowM + 1;
+        constexpr int64_t kLab0 = kNarrowM + 1;
+        auto in_lab = [&](int64_t q) { return lab_cl && q >= kLab0; };
+        int64_t lab_k = 0;   // start of the current block
         unsigned int* sw_prog = reinterpret_cast<unsigned int*>(S + (int64_t)Gt * SST);   // sweep bands
         unsigned int sw_ep = 0;   // fused sweeps so far in this cluster (the progress tag's epoch)
         if (r == 0 && tid == 0) publish(sw_prog, 0u);   // visible after the next group barrier
@@ -1475,6 +1675,39 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             part_tt(p, cg, Gt, ptt0, ptt1, a.piece_cost);
             part_tn(p, cg, Gt, ptn0, ptn1, a.piece_cost);
             part_rows_weighted(n, p + 1, cg, Gt, pd0, pd1, a.piece_cost);
+            bool use_lab = in_lab(p);   // first iteration from the block's U (no pass A, TT or BC rows)
+            if (use_lab && (p - kLab0) % a.lab == 0) {
+                // ---------------- BL1-BL3: U = X - Y_k T_k^T Y_k^T X for x^(1)_k .. x^(1)_{k+nv-1}
+                lab_k = p;
+                const int nv = (int)((m - p < a.lab) ? m - p : a.lab);
+                const double* Xb = a.X1c + j * n2v;
+                double* scr = ring_base;   // no pass ring in flight between phases
+                int64_t c0, c1, x0, x1;
+                part_cols_tri(p, n, cg, Gt, c0, c1);
+                part_uniform(0, n, cg, Gt, x0, x1);
+                lab_gemm1<kLabMax>(sm, Y, m, n, c0, c1, Xb, n2v, nv, ws.labG, mc, scr, x0, x1, ws.labP + (int64_t)cg * kLabMax);
+                gsync();
+                if (r == 0 && tid < nv) {   // ||x_v||^2 for the degeneracy test (reading 16)
+                    double t = 0.0;
+                    for (int q = 0; q < Gt; q++) t += ld(ws.labP + (int64_t)q * kLabMax + tid);
+                    st(ws.labX2 + tid, t);
+                }
+                int64_t l0, l1;
+                part_tt(p, cg, Gt, l0, l1, 0);
+                lab_rowdots<kLabMax>(sm, l0, l1, p, ws.labG, mc, nv, scr, [&](int64_t l) { return Tc + tcol_off(l); },
+                                     [&](int64_t l) -> int64_t { return l + 1; },
+                                     [&](int64_t l, int v, double t) { if (v < nv) st(ws.labGp + v * mc + l, t); });
+                gsync();
+                int64_t i0, i1;
+                part_uniform(p, n, cg, Gt, i0, i1);
+                lab_rowdots<kLabMax>(sm, i0, i1, p, ws.labGp, mc, nv, scr, [&](int64_t i) { return Y + y_row_off(i, m); },
+                                     [&](int64_t) -> int64_t { return p; },
+                                     [&](int64_t i, int v, double t) {
+                                         if (v < nv) st(ws.labU + v * n2v + i, ld(Xb + v * n2v + i) - t);
+                                     });
+                gsync();
+                PH(0);
+            }
             while (!done) {
                 double c = 1.0;   // the reflector's c (reduced / ordinary); 1 for MGS (r = q)
                 int64_t dq0 = pd0, dq1 = pd1;   // rows of q that this CTA holds after the step
@@ -1521,6 +1754,71 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     if (xv == sm.cf)
                         for (int q = tid; q < R; q += NT) st(ws.q + dq0 + q, xv[q]);
                     __syncthreads();
+                    PH(4);
+                } else {
+                if (use_lab) {
+                    // ---------------- block vector, iteration 1: x' = U_v = Q_k^T x^(1)_p; apply the
+                    // block's own reflectors k .. p-1:  g_r = Y_{k:p}^T x',  g'_r = T_kk^T g_r (the
+                    // trailing block of T_p),  uhat = rows >= p of x' - Y_{k:p} g'_r  (Eq. (4))
+                    const int v = (int)(p - lab_k);
+                    const double* Uv = ws.labU + v * n2v;
+                    double* gr = sm.vs;          // g_r   (<= kLabMax)
+                    double* grp = sm.vs + 16;    // g'_r
+                    if (v > 0) {
+                        int64_t i0, i1;
+                        part_uniform(lab_k, n, cg, Gt, i0, i1);
+                        double av[kLabMax];
+#pragma unroll
+                        for (int q = 0; q < kLabMax; q++) av[q] = 0.0;
+                        for (int64_t i = i0 + tid; i < i1; i += NT) {
+                            const double ui = ld(Uv + i);
+                            const double* yr = Y + y_row_off(i, m) + lab_k;
+#pragma unroll
+                            for (int q = 0; q < kLabMax; q++)
+                                if (q < v && lab_k + q <= i) av[q] = fma(ld(yr + q), ui, av[q]);
+                        }
+#pragma unroll
+                        for (int q = 0; q < kLabMax; q++) {
+                            if (q >= v) break;
+                            const double t = block_sum<NT>(av[q], sm.red);
+                            if (tid == 0) st(P_ + (int64_t)cg * mc + q, t);
+                        }
+                        gsync();
+                        PH(1);
+                        {   // every CTA: g_r (fixed order: lane-strided partials, warp tree), then T_kk^T g_r
+                            const int q = tid >> 5, lane = tid & 31;
+                            if (q < v) {
+                                double t = 0.0;
+                                for (int u = lane; u < Gt; u += 32) t += ld(P_ + (int64_t)u * mc + q);
+                                t = warp_sum(t);
+                                if (lane == 0) gr[q] = t;
+                            }
+                            __syncthreads();
+                            if (tid < v) {
+                                const int64_t l = lab_k + tid;
+                                const double* tc = Tc + tcol_off(l) + lab_k;
+                                double t = 0.0;
+                                for (int q2 = 0; q2 <= tid; q2++) t = fma(ld(tc + q2), gr[q2], t);
+                                grp[tid] = t;
+                            }
+                            __syncthreads();
+                        }
+                    }
+                    int64_t i0, i1;
+                    part_uniform(p, n, cg, Gt, i0, i1);
+                    double u2 = 0.0;
+                    for (int64_t i = i0 + tid; i < i1; i += NT) {
+                        double ui = ld(Uv + i);
+                        const double* yr = Y + y_row_off(i, m) + lab_k;
+                        for (int q = 0; q < v; q++) ui = fma(-ld(yr + q), grp[q], ui);
+                        mst(ws.u + i, ui);
+                        u2 = fma(ui, ui, u2);
+                    }
+                    u2 = block_sum<NT>(u2, sm.red);
+                    if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
+                    if (mode != 2)   // s' = Yhat^T uhat (one read of Yhat)
+                        wide_colacc(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.u, p, P_ + (int64_t)cg * mc, false, pol_once);
+                    gsync();
                     PH(4);
                 } else {
                 if (!use_la && !use_a2) {
@@ -1662,12 +1960,15 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 }
                 gsync();
                 PH(4);
+                }   // block vector / regular first passes
                 // ---------------- R2: scalars (every CTA, identical), s = s' - c Y[p,:]
                 const uint64_t q2s = dclk();
                 double un = sqrt(reduce_slot(sm, S, Gt, SSlots::U2));
-                const double x2 = reduce_slot(sm, S, Gt, use_la ? SSlots::X2N : SSlots::X2);
+                const double x2 = use_lab ? ld(ws.labX2 + (p - lab_k))
+                                          : reduce_slot(sm, S, Gt, use_la ? SSlots::X2N : SSlots::X2);
                 use_la = false;
                 use_a2 = false;
+                use_lab = false;
                 double u0 = ld(ws.u + p);
                 const bool zero_u = (un == 0.0);   // reading: exactly-zero uhat -> e_1
                 if (zero_u) { u0 = 1.0; un = 1.0; }
@@ -1796,7 +2097,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     }
                     // y_p^T x^(1)_{p+1}: the last column of the next vector's first pass A
                     double gpn = 0.0;
-                    const bool want_gpn = (p + 1 < m) && la_ok;
+                    const bool want_gpn = (p + 1 < m) && la_ok && !in_lab(p + 1);
                     const double* xn = a.X1c + (j + 1) * n2v;
                     if (want_gpn && !narrow) {   // (narrow: fused into the D stream below)
                         for (int64_t i = (i0 > p ? i0 : p) + tid; i < i1; i += NT)
@@ -1948,7 +2249,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     PH(8);
                     // look-ahead only when it can overlap the back sweep (other CTAs of the
                     // group, or warps 1.. of a single-CTA narrow group)
-                    const bool la = !la_done && p + 1 < m && la_ok;
+                    const bool la = !la_done && p + 1 < m && la_ok && !in_lab(p + 1);
                     // fused A2 (single-rank wide groups): pass A of the next iteration (g = Y_p^T x
                     // with the solve's x) streams Y_p behind the back sweep, band by band as the
                     // rows become final, together with the look-ahead Y_p^T x^(1)_{p+1}: one read

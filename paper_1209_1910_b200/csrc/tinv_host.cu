@@ -93,6 +93,7 @@ struct tinv_s {
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
+    int lab = 0;                      // blocked look-ahead block size (tinv_set_lookahead; 0/1 = off)
     int mgs = 0;                      // reorthogonalisation: 0 reduced cWY (§3.3.2), 1 classical MGS
                                       // (Alg. 1), 2 ordinary cWY (§3.3.1)
     int res_cs2 = 1000, res_cs4 = 1000, res_cs8 = 1000;   // m from which a cluster gets >= 2 / 4 / 8 CTAs
@@ -484,6 +485,12 @@ int tinv_set_resident(tinv_t h, int enable) {
     return 0;
 }
 
+int tinv_set_lookahead(tinv_t h, int b) {
+    if (!h) return TINV_ERR_HANDLE;
+    h->lab = b < 0 ? 0 : b;
+    return 0;
+}
+
 int tinv_set_reorth(tinv_t h, int mode) {
     if (!h) return TINV_ERR_HANDLE;
     if (mode < 0 || mode > 2) return -2;
@@ -714,6 +721,8 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         join_b2();
         return TINV_ERR_UNSUPPORTED;
     }
+    // blocked look-ahead: block size (TINV_LAB, 0/1 = off), compact-WY modes
+    const int lab = (h->mgs == 1) ? 0 : std::min(kLabMax, std::max(0, getenv("TINV_LAB") ? atoi(getenv("TINV_LAB")) : h->lab));
     // MGS pays one group barrier per accepted vector: its groups are kept small (TINV_MGS_G CTAs)
     const int gmax = (h->mgs == 1) ? std::max(1, getenv("TINV_MGS_G") ? atoi(getenv("TINV_MGS_G")) : 16) : (1 << 30);
     Schedule sc = rs_real ? make_schedule(cs, 0, nclus, n, nctas_max)
@@ -945,6 +954,14 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.P = c.take<double>((size_t)G * W.mcap);
                 W.P2 = c.take<double>((size_t)G * W.mcap);
                 W.S = c.take<double>((size_t)G * 16 + 16);
+                W.labG = W.labGp = W.labU = W.labX2 = W.labP = nullptr;
+                if (lab > 1 && mc > cwy_narrow_max() && RG == 1) {
+                    W.labG = c.take<double>((size_t)kLabMax * W.mcap);
+                    W.labGp = c.take<double>((size_t)kLabMax * W.mcap);
+                    W.labU = c.take<double>((size_t)kLabMax * ((n + 1) & ~int64_t(1)) + 2);
+                    W.labX2 = c.take<double>(kLabMax);
+                    W.labP = c.take<double>((size_t)G * kLabMax);
+                }
                 W.bar = bars + g;
                 W.nrk = 1;
                 W.rk = 0;
@@ -1039,6 +1056,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.poll_ns = getenv("TINV_POLLNS") ? atoi(getenv("TINV_POLLNS")) : 0;
         ca.dbg = getenv("TINV_DBG") ? atoi(getenv("TINV_DBG")) : 0;
         ca.reorth = h->mgs;
+        ca.lab = lab;
         unsigned long long* pcta = nullptr;
         if (getenv("TINV_PROF_CTA")) {   // debug only (not the product path): per-CTA phase busy times
             CK(cudaMalloc(&pcta, sizeof(unsigned long long) * 16 * sc.nctas));

@@ -112,6 +112,15 @@ struct GroupWS {
     double* S;          // scalar partials [Gt][16] (Gt = CTAs of the group over all ranks)
     double* P2;         // look-ahead partial sums [Gt][mcap]
     double* ysol;       // forward-sweep workspace of the chained solve (n)
+    // blocked look-ahead (CwyArgs::lab > 1, wide clusters): for the block of
+    // b upcoming first iterates X = [x^(1)_k .. x^(1)_{k+b-1}]:  G = Y_k^T X,  G' = T_k^T G
+    // (labG, [v][mcap]),  U = X - Y_k G'  (labU, [v][n2v], rows >= k), ||x_v||^2 (labX2 [v]);
+    // labP: per-CTA partials of ||x_v||^2 [Gt][8].  NULL when the group has no block look-ahead.
+    double* labG;
+    double* labGp;
+    double* labU;
+    double* labX2;
+    double* labP;
     GroupBarrier* bar;
     int64_t mcap;
     // Row split of one cluster over `nrk` ranks: every rank holds a full
@@ -166,6 +175,7 @@ struct CwyArgs {
     int poll_ns;             // back-off of the band polls in ns (TINV_POLLNS)
     int dbg;                 // debug build experiments (TINV_DBG bits)
     int reorth;              // 0 reduced compact WY (§3.3.2), 1 classical MGS (Alg. 1), 2 ordinary compact WY (§3.3.1)
+    int lab;                 // blocked look-ahead block size b (2..8; 0/1 = off), wide clusters of single-rank groups
     unsigned long long* prof_cta;   // debug: per-CTA busy time before each phase's barrier [cta*16 + phase], or NULL
 };
 

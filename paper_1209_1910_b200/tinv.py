@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(_HERE, "libtinv.so")
 
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",
-           "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks", "tinv_set_resident", "tinv_set_reorth")
+           "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks", "tinv_set_resident", "tinv_set_reorth",
+           "tinv_set_lookahead")
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
 PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "st_wait", "st_body", "st_sync", "st_blkend")
@@ -85,6 +86,8 @@ def load_library(path: str = LIB_PATH):
     L.tinv_set_resident.argtypes = [P, C.c_int]
     L.tinv_set_reorth.restype = C.c_int
     L.tinv_set_reorth.argtypes = [P, C.c_int]
+    L.tinv_set_lookahead.restype = C.c_int
+    L.tinv_set_lookahead.argtypes = [P, C.c_int]
     L.tinv_set_virtual_ranks.restype = C.c_int
     L.tinv_set_virtual_ranks.argtypes = [P, C.c_int]
     L.tinv_eigvals.restype = C.c_int
@@ -178,6 +181,12 @@ class Tinv:
         rc = self._L.tinv_set_reorth(self._h, code)
         if rc:
             raise TinvError(f"tinv_set_reorth failed: {rc}")
+
+    def set_lookahead(self, b: int):
+        """Blocked look-ahead block size (include/tinv.h tinv_set_lookahead; 0/1 = off)."""
+        rc = self._L.tinv_set_lookahead(self._h, int(b))
+        if rc:
+            raise TinvError(f"tinv_set_lookahead failed: {rc}")
 
     def set_virtual_ranks(self, nranks: int):
         rc = self._L.tinv_set_virtual_ranks(self._h, int(nranks))

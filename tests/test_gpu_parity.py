@@ -700,3 +700,61 @@ def test_reorth_modes_without_handover(handle, torch, mode):
     Zo, info = O.eigvecs(d, e, w, seed=1, mgs=(mode == "mgs"))
     wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zg.cpu().numpy(), Zo)
     assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+
+
+# ------------------------------------------------------------------ blocked look-ahead
+# tinv_set_lookahead(h, b) -- the first iterates of each block of b vectors
+# get the accepted reflectors applied at once (two skinny GEMMs + a TRMM); same results as the
+# per-vector step up to rounding: parity with the compact-WY oracle.
+
+@pytest.mark.parametrize("b", [2, 5, 8])
+@pytest.mark.parametrize("cfg,n", [("cfg4", 600), ("type2", 700), ("cfg3", 1050), ("cfg5", 1500)])
+def test_blocked_lookahead_parity(handle, torch, cfg, n, b):
+    d, e, w = W.problem(cfg, n)
+    handle.set_lookahead(b)
+    try:
+        Zg, rc = run_gpu(handle, torch, d, e, w)
+    finally:
+        handle.set_lookahead(0)
+    assert rc == 0
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
+    Zo, info = O.eigvecs(d, e, w, seed=1)
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zg.cpu().numpy(), Zo)
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+
+
+def test_blocked_lookahead_restarts(handle, torch):
+    """Block vectors that restart (reading 16), in the reduced and the ordinary sequence:
+    T = diag(1, 200, 201, ..) (n = 80) with 70 shifts on eigenvalue 1 -- one cluster of 70, so
+    vectors 65..69 take the block path; their iterates stay in span(z_0) and restart (the
+    oracle flags 54 vectors).  Same return code and iteration histogram as the oracle."""
+    d = np.concatenate([[1.0], 200.0 + np.arange(79.0)])
+    e = np.zeros(79)
+    w = np.concatenate([[1.0] * 70, d[70:]])
+    Zo, info, its = O.eigvecs(d, e, w, seed=1, return_iters=True)
+    assert info > 0 and (its[65:70] > 2).all(), (info, its[60:75])
+    for md in ("cwy", "ordinary"):
+        handle.set_lookahead(4)
+        handle.set_reorth(md)
+        try:
+            Zg, rc = run_gpu(handle, torch, d, e, w)
+            hist = _iters_of(handle)
+        finally:
+            handle.set_reorth("cwy")
+            handle.set_lookahead(0)
+        assert rc == info, (md, rc, info)
+        assert hist == list(np.bincount(its, minlength=8)[:8]), (md, hist, its)
+        assert np.abs(np.linalg.norm(Zg.cpu().numpy(), axis=0) - 1).max() <= 1e-14
+
+
+def test_blocked_lookahead_full_size_cfg4(handle, torch):
+    d, e, w = W.problem("cfg4")
+    handle.set_lookahead(8)
+    try:
+        Zg, rc = run_gpu(handle, torch, d, e, w)
+    finally:
+        handle.set_lookahead(0)
+    assert rc == 0
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
