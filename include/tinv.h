@@ -20,6 +20,7 @@
 #ifndef TINV_H
 #define TINV_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -193,6 +194,28 @@ int tinv_set_reorth(tinv_t h, int mode);
  * 0 or 1 = off (default; the environment variable TINV_LAB overrides).  Compact-WY modes only
  * (ignored with MGS).  Returns 0 or TINV_ERR_HANDLE. */
 int tinv_set_lookahead(tinv_t h, int b);
+
+/* Multi-rank diagnostics (SURVEY §8(e) row split; the peer-memory path of a row-split call
+ * without its cross-rank barrier, so several ranks may share one GPU).
+ *
+ * tinv_allgather_fn: a host all-gather supplied by the caller -- every rank passes `bytes`
+ * bytes at `send`; on return `recv` holds nranks * bytes, rank k's at k * bytes.  Collective;
+ * returns 0 on success.  tinv_set_host_exchange(h, fn, ctx) makes the library exchange its
+ * CUDA IPC handles (and run its unmap barrier) through fn instead of NCCL; fn = NULL restores
+ * NCCL.  A handle may be created with nranks > 1 and nccl_id = NULL (no communicator): then
+ * tinv_eigvecs returns TINV_ERR_NCCL and only these diagnostics work.
+ *
+ * tinv_debug_peer_map(h, bytes, tag, out): collective.  Grows the handle's cWY workspace to at
+ * least `bytes` (>= 64) exactly as a row-split call does (peers unmap the old allocation,
+ * collectively, before it is freed), writes `tag` into its first 8 bytes, maps every peer
+ * rank's workspace through CUDA IPC (cudaIpcGetMemHandle / cudaIpcOpenMemHandle, handles
+ * exchanged as above), then a kernel reads the first 8 bytes of every rank's replica through
+ * those mappings into out[0 .. nranks) (HOST array; out[k] = rank k's tag).  The mappings stay
+ * open until the next growth, a column-sharded call or tinv_destroy (collective).  Returns 0,
+ * -2 (nranks < 2 or bytes < 64), -4 (out NULL), TINV_ERR_NCCL, TINV_ERR_CUDA. */
+typedef int (*tinv_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+int tinv_set_host_exchange(tinv_t h, tinv_allgather_fn fn, void* ctx);
+int tinv_debug_peer_map(tinv_t h, size_t bytes, uint64_t tag, uint64_t* out);
 int tinv_get_stats(tinv_t h, tinv_stats_t* out);
 
 /* Number of exported entry points (for the loader test). */

@@ -1476,10 +1476,43 @@ __device__ void lab_rowdots(const Smem& sm, int64_t r0, int64_t r1, int64_t P, c
                         }
                     }
                 }
+                if (NV == 8) {
+                    // 8 warp sums at once: halve the values held per lane at each xor step (9
+                    // shuffles instead of 40); lane L ends with the total of vector (L >> 2) & 7
+                    // summed over its four-lane group, fixed order (deterministic)
 #pragma unroll
-                for (int v = 0; v < NV; v++) {
-                    const double t = warp_sum(a[v]);
-                    if (lane == 0) acc[(r - rb0) * NV + v] += t;
+                    for (int h = 0; h < 4; h++) {
+                        const bool up = lane & 16;
+                        const double send = up ? a[h] : a[h + 4];
+                        const double keep = up ? a[h + 4] : a[h];
+                        a[h] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const bool up = lane & 8;
+                        const double send = up ? a[h] : a[h + 2];
+                        const double keep = up ? a[h + 2] : a[h];
+                        a[h] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                    }
+                    {
+                        const bool up = lane & 4;
+                        const double send = up ? a[0] : a[1];
+                        const double keep = up ? a[1] : a[0];
+                        a[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                    }
+                    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+                    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+                    // lane bits 4,3,2 chose the upper halves: vector index = 4 b16 + 2 b8 + b4
+                    if ((lane & 3) == 0) {
+                        const int v = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                        acc[(r - rb0) * NV + v] += a[0];
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < NV; v++) {
+                        const double t = warp_sum(a[v]);
+                        if (lane == 0) acc[(r - rb0) * NV + v] += t;
+                    }
                 }
             }
         }
@@ -2405,6 +2438,20 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     if (dsub)
         for (int k = 0; k < 4; k++) a.prof[12 + k] = dtim[k];
 #undef PH
+}
+
+// Multi-rank diagnostic (tinv_debug_peer_map): read the first word of every rank's workspace
+// replica through the peer-memory mapping, addressed as the persistent kernel addresses peer
+// replicas (own base + delta[k] doubles).  Plain loads; nothing here waits on another rank.
+__global__ void peer_read_kernel(const double* base, const int64_t* delta, int nrk, uint64_t* out) {
+    const int k = threadIdx.x;
+    if (k < nrk) {
+        const double* p = base + __ldg(delta + k);
+        out[k] = *reinterpret_cast<const volatile unsigned long long*>(p);
+    }
+}
+void launch_peer_read(const double* base, const int64_t* delta, int nrk, uint64_t* out, cudaStream_t s) {
+    peer_read_kernel<<<1, 32 * ((nrk + 31) / 32), 0, s>>>(base, delta, nrk, out);
 }
 
 int cwy_threads() { return NT; }

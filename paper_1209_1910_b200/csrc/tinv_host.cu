@@ -93,7 +93,7 @@ struct tinv_s {
     double* bnd = nullptr;            // bisection bounds (3 doubles)
     int vranks = 1;                   // virtual ranks for the row split (testing on one device)
     int resident = 1;                 // narrow clusters in the resident (DSMEM) kernel
-    int lab = 0;                      // blocked look-ahead block size (tinv_set_lookahead; 0/1 = off)
+    int lab = 8;                      // blocked look-ahead block size (tinv_set_lookahead; 0/1 = off)
     int mgs = 0;                      // reorthogonalisation: 0 reduced cWY (§3.3.2), 1 classical MGS
                                       // (Alg. 1), 2 ordinary cWY (§3.3.1)
     int res_cs2 = 1000, res_cs4 = 1000, res_cs8 = 1000;   // m from which a cluster gets >= 2 / 4 / 8 CTAs
@@ -109,6 +109,8 @@ struct tinv_s {
     std::vector<char> peer_hdl;       // the IPC handles the mappings were opened from
     void* ipc_buf = nullptr;          // device staging for the handle allgather / barrier
     bool exported = false;            // peers hold IPC mappings of our cw (a row-split call ran)
+    tinv_allgather_fn xchg = nullptr; // host all-gather replacing NCCL for the handle exchange (tests)
+    void* xchg_ctx = nullptr;
     // pinned image of the cWY schedule header
     void* h_hdr = nullptr;
     size_t h_hdr_bytes = 0;
@@ -311,15 +313,20 @@ int map_peers(tinv_s* h, cudaStream_t st) {
         h->peer_cw.assign(h->nranks, nullptr);
         h->peer_hdl.assign(64 * (size_t)h->nranks, 0);
     }
-    if (!h->ipc_buf) CK(cudaMalloc(&h->ipc_buf, 64 * (size_t)h->nranks + 64));
+    if (!h->ipc_buf && !h->xchg) CK(cudaMalloc(&h->ipc_buf, 64 * (size_t)h->nranks + 64));
     cudaIpcMemHandle_t mine;
     CK(cudaIpcGetMemHandle(&mine, h->cw));
-    char* buf = (char*)h->ipc_buf;
-    CK(cudaMemcpyAsync(buf + 64 * h->rank, &mine, 64, cudaMemcpyHostToDevice, st));
-    if (g_nccl.allGather(buf + 64 * h->rank, buf, 64, ncclUint8, h->comm, st)) return TINV_ERR_NCCL;
     std::vector<char> all(64 * (size_t)h->nranks);
-    CK(cudaMemcpyAsync(all.data(), buf, all.size(), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (h->xchg) {   // host all-gather supplied by the caller (tinv_set_host_exchange)
+        CK(cudaStreamSynchronize(st));
+        if (h->xchg(&mine, all.data(), 64, h->xchg_ctx)) return TINV_ERR_NCCL;
+    } else {
+        char* buf = (char*)h->ipc_buf;
+        CK(cudaMemcpyAsync(buf + 64 * h->rank, &mine, 64, cudaMemcpyHostToDevice, st));
+        if (g_nccl.allGather(buf + 64 * h->rank, buf, 64, ncclUint8, h->comm, st)) return TINV_ERR_NCCL;
+        CK(cudaMemcpyAsync(all.data(), buf, all.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
     for (int k = 0; k < h->nranks; k++) {
         if (k == h->rank) continue;
         if (h->peer_cw[k] && !memcmp(h->peer_hdl.data() + 64 * k, all.data() + 64 * k, 64)) continue;
@@ -342,7 +349,12 @@ int unmap_peers_collective(tinv_s* h, cudaStream_t st) {
     for (auto& pp : h->peer_cw)
         if (pp) { cudaIpcCloseMemHandle(pp); pp = nullptr; }
     std::fill(h->peer_hdl.begin(), h->peer_hdl.end(), 0);
-    if (h->comm && h->ipc_buf) {
+    if (h->xchg) {   // barrier through the caller's host all-gather
+        CK(cudaStreamSynchronize(st));
+        std::vector<char> sink((size_t)h->nranks);
+        char one = 1;
+        if (h->xchg(&one, sink.data(), 1, h->xchg_ctx)) return TINV_ERR_NCCL;
+    } else if (h->comm && h->ipc_buf) {
         if (g_nccl.allReduce(h->ipc_buf, h->ipc_buf, 1, ncclUint8, ncclSum, h->comm, st)) return TINV_ERR_NCCL;
         CK(cudaStreamSynchronize(st));
     }
@@ -430,8 +442,8 @@ int tinv_create(tinv_t* out, const tinv_config_t* cfg) {
     CK(cudaStreamCreateWithFlags(&h->bst, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_b2, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_img, cudaEventDisableTiming));
-    if (h->nranks > 1) {
-        if (!cfg->nccl_id || !g_nccl.load()) { delete h; return TINV_ERR_NCCL; }
+    if (h->nranks > 1 && cfg->nccl_id) {   // NULL: no communicator (peer-map diagnostics only)
+        if (!g_nccl.load()) { delete h; return TINV_ERR_NCCL; }
         ncclUniqueId id;
         memcpy(&id, cfg->nccl_id, sizeof(id));
         if (g_nccl.commInitRank(&h->comm, h->nranks, id, h->rank) != 0) { delete h; return TINV_ERR_NCCL; }
@@ -482,6 +494,62 @@ int tinv_set_virtual_ranks(tinv_t h, int nranks) {
 int tinv_set_resident(tinv_t h, int enable) {
     if (!h) return TINV_ERR_HANDLE;
     h->resident = enable != 0;
+    return 0;
+}
+
+int tinv_set_host_exchange(tinv_t h, tinv_allgather_fn fn, void* ctx) {
+    if (!h) return TINV_ERR_HANDLE;
+    h->xchg = fn;
+    h->xchg_ctx = ctx;
+    return 0;
+}
+
+int tinv_debug_peer_map(tinv_t h, size_t bytes, uint64_t tag, uint64_t* out) {
+    if (!h) return TINV_ERR_HANDLE;
+    if (h->nranks < 2 || bytes < 64) return -2;
+    if (!out) return -4;
+    if (!h->xchg && !h->comm) return TINV_ERR_NCCL;
+    CK(cudaSetDevice(h->device));
+    cudaStream_t st = h->stream;
+    CK(cudaStreamSynchronize(st));
+    if (bytes > h->cw_bytes) {   // same growth path as a row-split call: peers unmap before we free
+        if (h->exported)
+            if (int rc = unmap_peers_collective(h, st)) return rc;
+        if (h->cw) cudaFree(h->cw);
+        h->cw = nullptr;
+        h->cw_bytes = 0;
+        CK(cudaMalloc(&h->cw, bytes));
+        h->cw_bytes = bytes;
+    }
+    CK(cudaMemcpy(h->cw, &tag, sizeof(tag), cudaMemcpyHostToDevice));
+    if (int rc = map_peers(h, st)) return rc;
+    h->exported = true;
+    std::vector<int64_t> dv(h->nranks, 0);
+    for (int k = 0; k < h->nranks; k++)
+        dv[k] = (k == h->rank) ? 0 : ((char*)h->peer_cw[k] - (char*)h->cw) / 8;
+    // every rank has written its tag before any rank reads (host barrier)
+    {
+        std::vector<char> sink((size_t)h->nranks);
+        char one = 1;
+        if (h->xchg) { if (h->xchg(&one, sink.data(), 1, h->xchg_ctx)) return TINV_ERR_NCCL; }
+        else {
+            if (!h->ipc_buf) CK(cudaMalloc(&h->ipc_buf, 64 * (size_t)h->nranks + 64));
+            if (g_nccl.allReduce(h->ipc_buf, h->ipc_buf, 1, ncclUint8, ncclSum, h->comm, st)) return TINV_ERR_NCCL;
+            CK(cudaStreamSynchronize(st));
+        }
+    }
+    int64_t* ddv = nullptr;
+    uint64_t* dout = nullptr;
+    CK(cudaMalloc(&ddv, sizeof(int64_t) * h->nranks));
+    CK(cudaMalloc(&dout, sizeof(uint64_t) * h->nranks));
+    CK(cudaMemcpy(ddv, dv.data(), sizeof(int64_t) * h->nranks, cudaMemcpyHostToDevice));
+    launch_peer_read(reinterpret_cast<const double*>(h->cw), ddv, h->nranks, dout, st);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, sizeof(uint64_t) * h->nranks, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(ddv);
+    cudaFree(dout);
+    if (e != cudaSuccess) return TINV_ERR_CUDA;
     return 0;
 }
 
@@ -541,6 +609,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     if (!w) return -5;
     if (!Z) return -6;
     if (ldz < n) return -7;
+    if (h->nranks > 1 && !h->comm) return TINV_ERR_NCCL;   // created without an NCCL id
     CK(cudaSetDevice(h->device));
     if (int r = ensure_base(h, n)) return r;
     const auto t_host0 = std::chrono::steady_clock::now();   // TINV_DEBUG: host-side timeline

@@ -216,6 +216,7 @@ int64_t batched_slot_cap(int64_t n);
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 void launch_pack(const PackArgs& a, cudaStream_t s);
 void launch_identity(double* Z, int64_t n, int64_t ldz, cudaStream_t s);
+void launch_peer_read(const double* base, const int64_t* delta, int nrk, uint64_t* out, cudaStream_t s);
 cudaError_t launch_cwy(const CwyArgs& a, int nctas, size_t smem, cudaStream_t s);
 int cwy_threads();
 size_t cwy_smem_bytes(int64_t vcap, int nstg);

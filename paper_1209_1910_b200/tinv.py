@@ -17,7 +17,10 @@ LIB_PATH = os.path.join(_HERE, "libtinv.so")
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",
            "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks", "tinv_set_resident", "tinv_set_reorth",
-           "tinv_set_lookahead")
+           "tinv_set_lookahead", "tinv_set_host_exchange", "tinv_debug_peer_map")
+
+# include/tinv.h tinv_allgather_fn: int (*)(const void* send, void* recv, size_t bytes, void* ctx)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 KERNEL_NAMES = ("prep", "batched_lu", "finalize", "cwy", "misc", "total")
 PHASE_NAMES = ("first", "A", "R1", "TT", "BC", "R2", "TN", "D", "test", "solve_fwd", "solve_back", "solve_wait", "st_wait", "st_body", "st_sync", "st_blkend")
@@ -88,6 +91,10 @@ def load_library(path: str = LIB_PATH):
     L.tinv_set_reorth.argtypes = [P, C.c_int]
     L.tinv_set_lookahead.restype = C.c_int
     L.tinv_set_lookahead.argtypes = [P, C.c_int]
+    L.tinv_set_host_exchange.restype = C.c_int
+    L.tinv_set_host_exchange.argtypes = [P, ALLGATHER_FN, P]
+    L.tinv_debug_peer_map.restype = C.c_int
+    L.tinv_debug_peer_map.argtypes = [P, C.c_size_t, C.c_uint64, P]
     L.tinv_set_virtual_ranks.restype = C.c_int
     L.tinv_set_virtual_ranks.argtypes = [P, C.c_int]
     L.tinv_eigvals.restype = C.c_int
@@ -116,6 +123,7 @@ class Tinv:
         self._torch = torch
         L = load_library()
         self.device = device
+        self.nranks = nranks
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
@@ -187,6 +195,32 @@ class Tinv:
         rc = self._L.tinv_set_lookahead(self._h, int(b))
         if rc:
             raise TinvError(f"tinv_set_lookahead failed: {rc}")
+
+    def set_host_exchange(self, allgather):
+        """Exchange the CUDA IPC handles through ``allgather(send: bytes, nbytes) -> bytes`` (a
+        host all-gather over the ranks, e.g. torch.distributed on gloo) instead of NCCL
+        (include/tinv.h tinv_set_host_exchange; diagnostics / tests)."""
+        def _fn(send, recv, nbytes, _ctx):
+            try:
+                out = allgather(C.string_at(send, nbytes), nbytes)
+                C.memmove(recv, out, len(out))
+                return 0
+            except Exception:
+                return 1
+        self._xchg = ALLGATHER_FN(_fn)   # keep the trampoline alive
+        rc = self._L.tinv_set_host_exchange(self._h, self._xchg, None)
+        if rc:
+            raise TinvError(f"tinv_set_host_exchange failed: {rc}")
+
+    def debug_peer_map(self, nbytes: int, tag: int):
+        """tinv_debug_peer_map: map every rank's workspace over CUDA IPC and read each rank's tag
+        through the mapping; returns the list of tags (collective)."""
+        n = self.nranks
+        out = (C.c_uint64 * n)()
+        rc = self._L.tinv_debug_peer_map(self._h, int(nbytes), int(tag), out)
+        if rc:
+            raise TinvError(f"tinv_debug_peer_map failed: {rc} ({strerror(rc)})")
+        return list(out)
 
     def set_virtual_ranks(self, nranks: int):
         rc = self._L.tinv_set_virtual_ranks(self._h, int(nranks))
