@@ -103,11 +103,19 @@ int tinv_eigvecs_host(tinv_t h, int64_t n, const double* d, const double* e, con
  * Peters-Wilkinson clusters of PAPER.md:135-139) are split into nranks contiguous,
  * cost-balanced column ranges [col_lo[r], col_hi[r]) that never cut a cluster (cost of a
  * cluster of m >= 2 vectors: m^2 n, the reorthogonalisation's HBM traffic; singletons: 1).
- * tinv_eigvecs with nranks > 1 computes exactly these columns on rank r.  Deterministic.
+ * tinv_eigvecs with nranks > 1 computes exactly these columns on rank r, except the columns
+ * of the row-split cluster (below), which every rank computes together.  Deterministic.
  * Returns 0, or -k for invalid argument k (n < 1; nclus outside [1, n]; cstart NULL or not a
  * valid cluster table; nranks < 1; col_lo / col_hi NULL).  Arrays are caller-owned host
  * memory of nclus + 1 and nranks entries. */
 int tinv_partition(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi);
+
+/* tinv_partition plus the row split (SURVEY §8(e) regime 2): *split (if not NULL) receives the
+ * index of the cluster whose rows are split over all ranks -- the costliest cluster when it is
+ * wide (m > 64) and costs at least 1/nranks of all clusters' m^2 n -- or -1 (nranks == 1 or no
+ * such cluster).  The ranges are balanced without that cluster's cost; its columns end up
+ * complete on every rank.  Same return codes as tinv_partition. */
+int tinv_plan(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi, int* split);
 
 /* Release the handle and its device workspace.  With nranks > 1 and a previous row-split
  * call (peers hold CUDA IPC mappings of this rank's workspace) it is collective: every rank

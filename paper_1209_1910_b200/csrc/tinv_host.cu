@@ -283,11 +283,12 @@ Schedule make_schedule(const int* cs, int c_lo, int c_hi, int64_t n, int nctas, 
 }
 
 // contiguous cluster ranges per rank, balanced by cost (deterministic)
-void rank_ranges(const int* cs, int nclus, int64_t n, int nranks, std::vector<int>& lo, std::vector<int>& hi) {
+void rank_ranges(const int* cs, int nclus, int64_t n, int nranks, std::vector<int>& lo, std::vector<int>& hi,
+                 int skip_c = -1) {
     std::vector<double> pre(nclus + 1, 0.0);
     for (int c = 0; c < nclus; c++) {
         double m = cs[c + 1] - cs[c];
-        pre[c + 1] = pre[c] + (m >= 2 ? m * m * (double)n : 0.0) + m;
+        pre[c + 1] = pre[c] + ((c == skip_c) ? 0.0 : (m >= 2 ? m * m * (double)n : 0.0) + m);   // skip_c: row-split
     }
     lo.assign(nranks, 0);
     hi.assign(nranks, 0);
@@ -299,6 +300,26 @@ void rank_ranges(const int* cs, int nclus, int64_t n, int nranks, std::vector<in
         if (r == nranks - 1) c = nclus;
         hi[r] = c;
     }
+}
+
+// The cluster a multi-rank call row-splits over all ranks (SURVEY §8(e) regime 2), or -1: the
+// costliest cluster (m^2 n) when it is wide (m > the resident/narrow limit) and at least one
+// rank's fair share of all the reorthogonalisation work.  Deterministic, identical on all ranks.
+int split_cluster(const int* cs, int nclus, int64_t n, int nranks, double* cost_big = nullptr,
+                  double* cost_all = nullptr) {
+    int cb = -1;
+    double big = 0.0, all = 0.0;
+    for (int c = 0; c < nclus; c++) {
+        const double m = cs[c + 1] - cs[c];
+        if (m < 2) continue;
+        const double cst = m * m * (double)n;
+        all += cst;
+        if (cst > big) { big = cst; cb = c; }
+    }
+    if (cost_big) *cost_big = big;
+    if (cost_all) *cost_all = all;
+    if (nranks < 2 || cb < 0 || cs[cb + 1] - cs[cb] <= cwy_narrow_max() || big * nranks < all) return -1;
+    return cb;
 }
 
 void ev_record(tinv_s* h, int k) {
@@ -369,7 +390,7 @@ extern "C" {
 
 int tinv_abi_version(void) { return 1; }
 
-int tinv_partition(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi) {
+int tinv_plan(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi, int* split) {
     if (n < 1) return -1;
     if (nclus < 1 || nclus > n) return -2;
     if (!cstart) return -3;
@@ -379,13 +400,19 @@ int tinv_partition(int64_t n, int64_t nclus, const int* cstart, int nranks, int*
     if (cstart[0] != 0 || cstart[nclus] != n) return -3;
     for (int64_t c = 0; c < nclus; c++)
         if (cstart[c + 1] <= cstart[c]) return -3;
+    const int cb = split_cluster(cstart, (int)nclus, n, nranks);
     std::vector<int> lo, hi;
-    rank_ranges(cstart, (int)nclus, n, nranks, lo, hi);
+    rank_ranges(cstart, (int)nclus, n, nranks, lo, hi, cb);
     for (int r = 0; r < nranks; r++) {
         col_lo[r] = cstart[lo[r]];
         col_hi[r] = cstart[hi[r]];
     }
+    if (split) *split = cb;
     return 0;
+}
+
+int tinv_partition(int64_t n, int64_t nclus, const int* cstart, int nranks, int* col_lo, int* col_hi) {
+    return tinv_plan(n, nclus, cstart, nranks, col_lo, col_hi, nullptr);
 }
 
 const char* tinv_strerror(int code) {
@@ -709,8 +736,23 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const int* cs = h->h_cstart;
 
     // ---------------- compact-WY kernel over this rank's clusters
+    // Row split: a wide cluster whose reorthogonalisation is at least one rank's
+    // fair share of all of it (cfg4/cfg5: the only cluster; Type 1 at n = 10500: 92%) is shared by
+    // all ranks -- every rank keeps a replica of its group workspace, the rows of every pass are
+    // split over all ranks' CTAs, small results are mirrored into every replica and the per-CTA
+    // partial sums are read from their owner's replica.  The other clusters are sharded over the
+    // ranks by columns as usual (their own groups in the same launch).  Virtual ranks run the
+    // same scheme as groups of one launch on one device (tinv_set_virtual_ranks, tests).
+    double cost_big = 0.0, cost_all = 0.0;
+    const int nrk_cand = h->nranks > 1 ? h->nranks : std::max(1, h->vranks);
+    const int cbig = split_cluster(cs, nclus, n, nrk_cand, &cost_big, &cost_all);
+    const bool split_big = cbig >= 0;
+    const bool rs_real = h->nranks > 1 && split_big;
+    const int NRK = rs_real ? h->nranks : ((h->nranks == 1 && h->vranks > 1 && split_big) ? h->vranks : 1);
+    const bool rs_virtual = !rs_real && NRK > 1;
+    const int csplit = (NRK > 1) ? cbig : -1;   // the row-split cluster, or -1
     std::vector<int> rlo, rhi;
-    rank_ranges(cs, nclus, n, h->nranks, rlo, rhi);
+    rank_ranges(cs, nclus, n, h->nranks, rlo, rhi, rs_real ? cbig : -1);
     const int64_t vcap = ((int64_t)po.max_cluster + 1) / 2 * 2 + 2;   // >= every group's mcap
     int nstg = 0;   // TMA ring for narrow clusters (2 <= m <= cwy_narrow_max()) of this rank
     for (int c = rlo[h->rank]; c < rhi[h->rank] && !nstg; c++) {
@@ -725,18 +767,6 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         return TINV_ERR_UNSUPPORTED;
     }
     const int nctas_max = h->nsm * std::max(1, po.n_clustered > 0 ? cwy_max_ctas_per_sm(smem) : 1);
-    // Row split: when the clustered work is one wide cluster (cfg4/cfg5), all
-    // ranks share it -- every rank keeps a replica of the group workspace, the rows of every
-    // pass are split over all ranks' CTAs, small results are mirrored into every replica and
-    // the per-CTA partial sums are read from their owner's replica.  Virtual ranks run the
-    // same scheme as groups of one launch on one device (tinv_set_virtual_ranks, tests).
-    int nbig = 0;
-    for (int c = 0; c < nclus; c++)
-        if (cs[c + 1] - cs[c] >= 2) nbig++;
-    const bool wide1 = nbig == 1 && po.max_cluster > cwy_narrow_max();
-    const bool rs_real = h->nranks > 1 && wide1;
-    const int NRK = rs_real ? h->nranks : ((h->nranks == 1 && h->vranks > 1 && wide1) ? h->vranks : 1);
-    const bool rs_virtual = !rs_real && NRK > 1;
     // a previous call row-split (peers mapped our workspace); this one shards by columns, so the
     // ranks' workspace sizes may diverge: release the mappings collectively first
     if (h->nranks > 1 && h->exported && !rs_real)
@@ -747,7 +777,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     std::vector<char> resident(nclus, 0);
     struct ResGroup { int cs, RL, M2; size_t smem; std::vector<int> cl; };
     std::vector<ResGroup> rgroups;
-    if (!rs_real && NRK == 1 && n <= 4096 && h->resident) {
+    if (n <= 4096 && h->resident) {   // (the row-split cluster is wide: never resident)
         const int css[4] = {1, 2, 4, 8};
         for (int c = rlo[h->rank]; c < rhi[h->rank]; c++) {
             const int m = cs[c + 1] - cs[c];
@@ -794,24 +824,59 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     const int lab = (h->mgs == 1) ? 0 : std::min(kLabMax, std::max(0, getenv("TINV_LAB") ? atoi(getenv("TINV_LAB")) : h->lab));
     // MGS pays one group barrier per accepted vector: its groups are kept small (TINV_MGS_G CTAs)
     const int gmax = (h->mgs == 1) ? std::max(1, getenv("TINV_MGS_G") ? atoi(getenv("TINV_MGS_G")) : 16) : (1 << 30);
-    Schedule sc = rs_real ? make_schedule(cs, 0, nclus, n, nctas_max)
-                          : make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max, &resident, gmax);
-    if (rs_virtual && sc.size.size() == 1) {   // split the group into NRK equal virtual ranks
-        const int Gv = std::max(1, sc.size[0] / NRK);   // >= 1 CTA per virtual rank (small clusters)
-        const int cl = sc.clist[0];
-        const int64_t mc = sc.mcap[0];
-        sc = Schedule{};
+    Schedule sc;
+    int nrep = 0;   // leading groups that hold the row-split cluster (replicated over RG ranks)
+    if (csplit < 0) {
+        sc = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, nctas_max, &resident, gmax);
+    } else {
+        // CTAs of the row-split group per rank: its per-rank work against the largest local
+        // work of any rank (identical on every rank: the replicas' layouts must match)
+        const double mb = cs[csplit + 1] - cs[csplit];
+        auto cost_of = [&](int c) { const double m = cs[c + 1] - cs[c]; return (m >= 2 && c != csplit) ? m * m * (double)n : 0.0; };
+        double loc_max = 0.0;
+        const int nr = h->nranks;
+        for (int q = 0; q < nr; q++) {
+            double l = 0.0;
+            for (int c = rlo[q]; c < rhi[q]; c++) l += cost_of(c);
+            loc_max = std::max(loc_max, l);
+        }
+        const int cap = (int)std::max(1.0, std::min((double)nctas_max, std::ceil(mb * (double)n * 8.0 / (256.0 * 1024.0))));
+        const double per_rank = cost_big / NRK;
+        const double loc = rs_virtual ? cost_all - cost_big : loc_max;   // virtual ranks: one GPU runs all
+        int Gbig = (loc > 0.0) ? (int)std::floor(nctas_max * (rs_virtual ? cost_big / cost_all : per_rank / (per_rank + loc)))
+                               : nctas_max;
+        Gbig = std::min(Gbig, cap);
+        const int Gv = rs_virtual ? std::max(1, Gbig / NRK) : std::max(1, Gbig);
+        nrep = rs_virtual ? NRK : 1;
+        int left = nctas_max - nrep * Gv;
+        std::vector<char> skip = resident;
+        skip[csplit] = 1;
+        Schedule loc_s;
+        bool any_local = false;
+        for (int c = rlo[h->rank]; c < rhi[h->rank]; c++)
+            if (cs[c + 1] - cs[c] >= 2 && !skip[c]) any_local = true;
+        if (any_local) {
+            if (left < 1) { join_b2(); return TINV_ERR_UNSUPPORTED; }
+            loc_s = make_schedule(cs, rlo[h->rank], rhi[h->rank], n, left, &skip, gmax);
+        }
         sc.coff.push_back(0);
-        for (int k = 0; k < NRK; k++) {
+        for (int k = 0; k < nrep; k++) {
             sc.cta0.push_back(k * Gv);
             sc.size.push_back(Gv);
-            sc.clist.push_back(cl);
+            sc.clist.push_back(csplit);
             sc.coff.push_back(k + 1);
-            sc.mcap.push_back(mc);
+            sc.mcap.push_back((int64_t)mb);
         }
-        sc.nctas = NRK * Gv;
+        for (size_t g = 0; g < loc_s.size.size(); g++) {
+            sc.cta0.push_back(nrep * Gv + loc_s.cta0[g]);
+            sc.size.push_back(loc_s.size[g]);
+            for (int q = loc_s.coff[g]; q < loc_s.coff[g + 1]; q++) sc.clist.push_back(loc_s.clist[q]);
+            sc.coff.push_back((int)sc.clist.size());
+            sc.mcap.push_back(loc_s.mcap[g]);
+        }
+        sc.nctas = nrep * Gv + loc_s.nctas;
     }
-    const int RG = (rs_real || rs_virtual) ? NRK : 1;   // ranks per group
+    const int RG = (csplit >= 0) ? NRK : 1;   // ranks per replicated group
     ev_record(h, 5);
     if (!rgroups.empty()) {
         // unit lists (LPT by the cluster's work ~ its vectors) for every group, one H2D copy
@@ -991,22 +1056,12 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         size_t hdr_lo = 0, hdr_hi = 0;
         auto layout = [&](char* p, std::vector<GroupWS>& ws, int** arrs, long long** syncs, GroupWS** dws) {
             Carve c{p};
-            prof = c.take<unsigned long long>((size_t)ng * 16);
-            arrs[0] = c.take<int>(ng);
-            hdr_lo = (size_t)((char*)arrs[0] - p);
-            arrs[1] = c.take<int>(ng);
-            arrs[2] = c.take<int>(ng + 1);
-            arrs[3] = c.take<int>(sc.clist.size());
-            *syncs = c.take<long long>(ng);
-            *dws = c.take<GroupWS>(ng);
-            GroupBarrier* bars = c.take<GroupBarrier>(ng);
-            int64_t* dl = c.take<int64_t>((size_t)ng * RG);
-            hdr_hi = c.off;
             ws.resize(ng);
-            for (int g = 0; g < ng; g++) {
+            auto carve_group = [&](int g) {
+                const int rg = (g < nrep) ? RG : 1;   // ranks sharing this group
                 int64_t mc = sc.mcap[g];
                 int64_t m2 = (mc + 1) & ~int64_t(1);
-                int G = sc.size[g] * RG;   // partial / scalar slots for the CTAs of all ranks
+                int G = sc.size[g] * rg;   // partial / scalar slots for the CTAs of all ranks
                 GroupWS& W = ws[g];
                 W.mcap = m2 + 2;
                 W.Y = c.take<double>(y_row_off(n, mc) + 2);
@@ -1024,25 +1079,43 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.P2 = c.take<double>((size_t)G * W.mcap);
                 W.S = c.take<double>((size_t)G * 16 + 16);
                 W.labG = W.labGp = W.labU = W.labX2 = W.labP = nullptr;
-                if (lab > 1 && mc > cwy_narrow_max() && RG == 1) {
+                if (lab > 1 && mc > cwy_narrow_max() && rg == 1) {
                     W.labG = c.take<double>((size_t)kLabMax * W.mcap);
                     W.labGp = c.take<double>((size_t)kLabMax * W.mcap);
                     W.labU = c.take<double>((size_t)kLabMax * ((n + 1) & ~int64_t(1)) + 2);
                     W.labX2 = c.take<double>(kLabMax);
                     W.labP = c.take<double>((size_t)G * kLabMax);
                 }
-                W.bar = bars + g;
+                W.bar = nullptr;
                 W.nrk = 1;
                 W.rk = 0;
                 W.vrt = 0;
                 W.delta = nullptr;
-                if (RG > 1) {   // replicated layout: the barrier lives inside the replica
+                if (rg > 1) {   // replicated layout: the barrier lives inside the replica
                     W.bar = c.take<GroupBarrier>(2);
-                    W.nrk = RG;
+                    W.nrk = rg;
                     W.rk = rs_real ? h->rank : g;
                     W.vrt = rs_virtual ? 1 : 0;
-                    W.delta = dl + (size_t)g * RG;
                 }
+            };
+            // the row-split group(s) first: at the same offset from the base on every rank (a
+            // peer replica is addressed as own pointer + delta), whatever the local schedule
+            for (int g = 0; g < nrep; g++) carve_group(g);
+            prof = c.take<unsigned long long>((size_t)ng * 16);
+            arrs[0] = c.take<int>(ng);
+            hdr_lo = (size_t)((char*)arrs[0] - p);
+            arrs[1] = c.take<int>(ng);
+            arrs[2] = c.take<int>(ng + 1);
+            arrs[3] = c.take<int>(sc.clist.size());
+            *syncs = c.take<long long>(ng);
+            *dws = c.take<GroupWS>(ng);
+            GroupBarrier* bars = c.take<GroupBarrier>(ng);
+            int64_t* dl = c.take<int64_t>((size_t)ng * RG);
+            hdr_hi = c.off;
+            for (int g = nrep; g < ng; g++) carve_group(g);
+            for (int g = 0; g < ng; g++) {
+                if (!ws[g].bar) ws[g].bar = bars + g;
+                if (g < nrep && RG > 1) ws[g].delta = dl + (size_t)g * RG;
             }
             return c.off;
         };
@@ -1087,8 +1160,8 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             put(dws, ws.data(), sizeof(GroupWS) * ng);
             if (RG > 1) {
                 std::vector<int64_t> dv((size_t)ng * RG, 0);
-                if (rs_virtual) {
-                    for (int g = 0; g < ng; g++)
+                if (rs_virtual) {   // the NRK virtual ranks' groups are 0 .. nrep-1
+                    for (int g = 0; g < nrep; g++)
                         for (int k = 0; k < RG; k++) dv[(size_t)g * RG + k] = ws[k].Y - ws[g].Y;
                 } else {
                     if (int rc = map_peers(h, st)) return rc;
@@ -1100,7 +1173,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             }
             CK(cudaMemcpyAsync(base + hdr_lo, img, hb, cudaMemcpyHostToDevice, st));
             if (RG > 1) {
-                for (int g = 0; g < ng; g++) CK(cudaMemsetAsync(ws[g].bar, 0, 2 * sizeof(GroupBarrier), st));
+                for (int g = 0; g < nrep; g++) CK(cudaMemsetAsync(ws[g].bar, 0, 2 * sizeof(GroupBarrier), st));
                 if (rs_real) {   // every rank's counters are zero before any kernel adds to them
                     if (g_nccl.allReduce(h->ipc_buf, h->ipc_buf, 1, ncclUint8, ncclSum, h->comm, st))
                         return TINV_ERR_NCCL;
@@ -1195,11 +1268,11 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     S.solve_bytes = 144.0 * (double)n * (double)n;  // factor 32n + 2 x 56n per vector
 
     // ---------------- multi-rank: broadcast each rank's cluster columns
-    if (h->nranks > 1 && !rs_real) {
+    // (the row-split cluster's columns are complete on every rank already)
+    if (h->nranks > 1) {
         if (g_nccl.groupStart()) return TINV_ERR_NCCL;
-        for (int r = 0; r < h->nranks; r++) {
-            int64_t c0 = cs[rlo[r]], c1 = cs[rhi[r]];
-            if (c1 <= c0) continue;
+        auto bcast = [&](int64_t c0, int64_t c1, int r) -> int {
+            if (c1 <= c0) return 0;
             if (ldz == n) {
                 if (g_nccl.broadcast(Z + c0 * ldz, Z + c0 * ldz, (size_t)((c1 - c0) * ldz), ncclFloat64, r, h->comm, st))
                     return TINV_ERR_NCCL;
@@ -1208,6 +1281,18 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                     if (g_nccl.broadcast(Z + j * ldz, Z + j * ldz, (size_t)n, ncclFloat64, r, h->comm, st))
                         return TINV_ERR_NCCL;
             }
+            return 0;
+        };
+        for (int r = 0; r < h->nranks; r++) {
+            const int64_t c0 = cs[rlo[r]], c1 = cs[rhi[r]];
+            int rc = 0;
+            if (rs_real && cbig >= rlo[r] && cbig < rhi[r]) {
+                rc = bcast(c0, cs[cbig], r);
+                if (!rc) rc = bcast(cs[cbig + 1], c1, r);
+            } else {
+                rc = bcast(c0, c1, r);
+            }
+            if (rc) return rc;
         }
         if (g_nccl.groupEnd()) return TINV_ERR_NCCL;
     }
@@ -1218,7 +1303,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
     h->iters_n = n;   // iters_hist and reorth_bytes: computed by tinv_get_stats after its read-back
-    h->rb_clo = rs_real ? 0 : rlo[h->rank];
+    h->rb_clo = rs_real ? 0 : rlo[h->rank];   // (row split: all clusters, approximately)
     h->rb_chi = rs_real ? nclus : rhi[h->rank];
     S.launches = launches;
     if (h->profiling) {

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libtinv.so")
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",
            "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks", "tinv_set_resident", "tinv_set_reorth",
-           "tinv_set_lookahead", "tinv_set_host_exchange", "tinv_debug_peer_map")
+           "tinv_set_lookahead", "tinv_set_host_exchange", "tinv_debug_peer_map", "tinv_plan")
 
 # include/tinv.h tinv_allgather_fn: int (*)(const void* send, void* recv, size_t bytes, void* ctx)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -103,6 +103,8 @@ def load_library(path: str = LIB_PATH):
     L.tinv_eig.argtypes = [P, I64, P, P, P, P, I64, C.c_uint64]
     L.tinv_partition.restype = C.c_int
     L.tinv_partition.argtypes = [I64, I64, P, C.c_int, P, P]
+    L.tinv_plan.restype = C.c_int
+    L.tinv_plan.argtypes = [I64, I64, P, C.c_int, P, P, P]
     L.tinv_abi_version.restype = C.c_int
     _lib = L
     return L
@@ -298,3 +300,20 @@ def partition(cstart, nranks: int):
     if rc != 0:
         raise TinvError(rc, L.tinv_strerror(rc).decode())
     return list(zip(lo.tolist(), hi.tolist()))
+
+
+def plan(cstart, nranks: int):
+    """(ranges, split): tinv_plan -- the column ranges of tinv_partition and the index of the
+    cluster whose rows every rank shares (-1: none)."""
+    import numpy as np
+
+    cs = np.ascontiguousarray(cstart, dtype=np.int32)
+    nclus = cs.shape[0] - 1
+    lo = np.zeros(nranks, dtype=np.int32)
+    hi = np.zeros(nranks, dtype=np.int32)
+    sp = C.c_int(-2)
+    L = load_library()
+    rc = L.tinv_plan(int(cs[-1]), nclus, cs.ctypes.data, int(nranks), lo.ctypes.data, hi.ctypes.data, C.byref(sp))
+    if rc != 0:
+        raise TinvError(rc, L.tinv_strerror(rc).decode())
+    return list(zip(lo.tolist(), hi.tolist())), sp.value

@@ -758,3 +758,19 @@ def test_blocked_lookahead_full_size_cfg4(handle, torch):
     assert rc == 0
     res, orth = invariants_gpu(torch, d, e, w, Zg)
     assert res <= 10.0 and orth <= 10.0
+
+
+@pytest.mark.parametrize("vr", [2, 3])
+def test_row_split_virtual_ranks_mixed(handle, torch, vr):
+    """A dominant wide cluster (700 of 3000 vectors) plus a wide one of 100 and many small ones: the big cluster is
+    row-split over `vr` virtual ranks while the others run as ordinary groups (and narrow ones
+    in the resident kernel) in the same launch -- SURVEY §8(e) regime 2 next to regime 1.
+    Parity with the oracle."""
+    d, e, w = _clustered(3000, [700, 100, 9])
+    handle.set_virtual_ranks(vr)
+    try:
+        full_parity(handle, torch, d, e, w)
+        st = handle.stats()
+    finally:
+        handle.set_virtual_ranks(1)
+    assert st["ngroups"] >= vr + 1, st["ngroups"]     # vr split groups + the other clusters' groups

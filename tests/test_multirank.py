@@ -33,30 +33,56 @@ def _free_port():
     return p
 
 
+def _problem(cfg, n):
+    if cfg == "mixed":   # one dominant wide cluster (row split) plus small ones (sharded)
+        rng = np.random.default_rng(5)
+        groups = [120] + [3] * ((n - 120) // 3)
+        rng.shuffle(groups)
+        d = np.concatenate([g + 1e-7 * rng.uniform(-1, 1, k) for g, k in enumerate(groups)])
+        e = 1e-9 * rng.uniform(-1, 1, len(d) - 1)
+        return d, e, W.eigenvalues(d, e)
+    return W.problem(cfg, n)
+
+
 def _worker(rank, world, port, cfg, n, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        d, e, w = W.problem(cfg, n)
+        d, e, w = _problem(cfg, n)
         n = len(d)
         cs = O.clusters(w, O.tnorm(d, e))
-        ranges = tinv.partition(cs, world)
+        ranges, split = tinv.plan(cs, world)
         lo, hi = ranges[rank]
-        # this rank's columns (stand-in for the GPU compute of its clusters)
+        # this rank's columns (stand-in for the GPU compute of its clusters); the row-split
+        # cluster is computed by all ranks together (on the GPU: its rows split over them)
         Zloc = np.zeros((n, n))
-        if hi > lo:
-            Zr, info = O.eigvecs(d, e, w, seed=1, j_lo=lo, j_hi=hi)
+        own = [(lo, hi)]
+        if split >= 0:
+            a, b = int(cs[split]), int(cs[split + 1])
+            own = [(lo, min(hi, a)), (max(lo, b), hi)] if lo <= a < hi else own
+            Zs, info = O.eigvecs(d, e, w, seed=1, j_lo=a, j_hi=b)
             assert info == 0
-            Zloc[:, lo:hi] = Zr
-        # exchange: every rank broadcasts its block (what the library does with NCCL)
+            Zloc[:, a:b] = Zs[:, a:b] if Zs.shape[1] == n else Zs
+        for a, b in own:
+            if b > a:
+                Zr, info = O.eigvecs(d, e, w, seed=1, j_lo=a, j_hi=b)
+                assert info == 0
+                Zloc[:, a:b] = Zr[:, a:b] if Zr.shape[1] == n else Zr
+        # exchange: every rank broadcasts its block (what the library does with NCCL), the
+        # split cluster's columns excepted (complete everywhere)
         Z = torch.tensor(Zloc)
         for r, (a, b) in enumerate(ranges):
-            blk = Z[:, a:b].contiguous()
-            dist.broadcast(blk, src=r)
-            Z[:, a:b] = blk
+            blocks = [(a, b)]
+            if split >= 0 and a <= int(cs[split]) < b:
+                blocks = [(a, int(cs[split])), (int(cs[split + 1]), b)]
+            for x, y in blocks:
+                blk = Z[:, x:y].contiguous()
+                dist.broadcast(blk, src=r)
+                Z[:, x:y] = blk
         np.save(os.path.join(out_dir, f"Z{rank}.npy"), Z.numpy())
         np.save(os.path.join(out_dir, f"ranges{rank}.npy"), np.array(ranges))
+        np.save(os.path.join(out_dir, f"split{rank}.npy"), np.array([split]))
     finally:
         dist.destroy_process_group()
 
@@ -66,13 +92,15 @@ def _run(tmp_path, cfg, n, world=2):
     mp.spawn(_worker, args=(world, port, cfg, n, str(tmp_path)), nprocs=world, join=True)
     Zs = [np.load(tmp_path / f"Z{r}.npy") for r in range(world)]
     rs = [np.load(tmp_path / f"ranges{r}.npy") for r in range(world)]
+    sp = [int(np.load(tmp_path / f"split{r}.npy")[0]) for r in range(world)]
+    assert len(set(sp)) == 1                          # every rank derived the same row split
     return Zs, rs
 
 
-@pytest.mark.parametrize("cfg,n", [("cfg2", 400), ("cfg3", 630), ("cfg1", 200)])
+@pytest.mark.parametrize("cfg,n", [("cfg2", 400), ("cfg3", 630), ("cfg1", 200), ("mixed", 600)])
 def test_sharded_assembly_equals_single_process(tmp_path, cfg, n):
     Zs, rs = _run(tmp_path, cfg, n)
-    d, e, w = W.problem(cfg, n)
+    d, e, w = _problem(cfg, n)
     Zref, info = O.eigvecs(d, e, w, seed=1)
     assert info == 0
     for r in range(len(Zs)):
@@ -100,9 +128,33 @@ def test_partition_balances_reorth_cost():
     cs = np.arange(0, n + 1, 10)
     ranges = tinv.partition(cs, 4)
     assert ranges == [(0, 40), (40, 80), (80, 120), (120, 160)]
-    # one giant cluster cannot be split by columns: it lands on one rank
+    # one giant cluster cannot be split by columns: it lands on one rank -- and is row-split
     ranges = tinv.partition(np.array([0, 100]), 3)
     assert sorted(b - a for a, b in ranges) == [0, 0, 100]
+    assert tinv.plan(np.array([0, 100]), 3)[1] == 0
+    assert tinv.plan(np.array([0, 100]), 1)[1] == -1          # one rank: nothing to split
+    assert tinv.plan(np.array([0, 60]), 2)[1] == -1           # narrow (m <= 64): never split
+
+
+def test_plan_row_split_rule():
+    """the costliest cluster is row-split when it is wide and worth >= 1/N of all
+    the m^2 n work; the other clusters are balanced over the ranks without it."""
+    # clusters 300, 100, 100, 100 (n = 600): 300^2 = 9e4 of 1.2e5 total
+    cs = np.array([0, 300, 400, 500, 600])
+    for nr in (2, 4, 8):
+        ranges, split = tinv.plan(cs, nr)
+        assert split == 0
+        owned = [c for c in range(1, 4) if any(a <= cs[c] < b for a, b in ranges)]
+        assert owned == [1, 2, 3]
+    # four equal clusters: none is worth more than its share at N = 2 ... but is at N = 8
+    cs = np.array([0, 100, 200, 300, 400])
+    assert tinv.plan(cs, 2)[1] == -1
+    assert tinv.plan(cs, 8)[1] == 0
+    # with the split cluster excluded, the remaining three balance one per rank on 3 ranks
+    ranges, split = tinv.plan(np.array([0, 300, 400, 500, 600]), 3)
+    assert split == 0
+    sizes = sorted(b - a for a, b in ranges)
+    assert sizes[-1] <= 400                                # the big one does not weigh down a rank
 
 
 def test_partition_rejects_invalid_tables():
