@@ -53,6 +53,7 @@ def lib():
             "orc_cwy_orth": (None, [I64, I64, P, P]),
             "orc_cwy_ordinary_orth": (None, [I64, I64, P, P]),
             "orc_cwy_build": (None, [I64, I64, P, P]),
+            "orc_cwy_apply_block": (None, [I64, I64, P, I64, P, C.c_int, P]),
             "orc_sturm_count": (I64, [I64, P, P, C.c_double, C.c_double]),
             "orc_bisect": (None, [I64, P, P, P]),
             "orc_eigvecs": (I64, [I64, P, P, P, P, I64, C.c_uint64, P]),
@@ -186,6 +187,19 @@ def cwy_build(V):
         T[k, k] = P[k, k]
         Y[k:, k] = P[k + 1:, k]
     return Y, T
+
+
+def cwy_apply_block(V, X, trans=True):
+    """Blocked look-ahead oracle: with Y, T from V's columns (§3.3.2),
+    U = X - Y T^T Y^T X (trans) or X - Y T Y^T X."""
+    V = np.asfortranarray(V, dtype=np.float64)
+    X = np.asfortranarray(X, dtype=np.float64)
+    n, k = V.shape
+    b = X.shape[1]
+    U = np.zeros((n, b), order="F")
+    lib().orc_cwy_apply_block(n, k, V.ctypes.data_as(C.c_void_p), b, X.ctypes.data_as(C.c_void_p), int(bool(trans)),
+                              U.ctypes.data_as(C.c_void_p))
+    return U
 
 
 def sturm_count(d, e, x, tn=None):

@@ -314,27 +314,46 @@ void orc_cwy_first(orc_cwy_t* a, const double* z)
     free(q);
 }
 
-void orc_cwy_apply(const orc_cwy_t* a, const double* x, double* out)
+/* Blocked application of the accepted reflectors to b vectors (Eq.(4)
+ * PAPER.md:304-313, Alg. 3): builds Y_k/T_k from the first k columns of V by
+ * the §3.3.2 step, then for each column x of X (n x b, column-major) writes
+ *   trans = 1:  U = (I - Y T Y^T)^T x = x - Y (T^T (Y^T x))   (the u-step PAPER.md:530-538)
+ *   trans = 0:  U = (I - Y T Y^T) x   = x - Y (T (Y^T x))
+ * in the plain order of the definition (three GEMV loops per column).  Test oracle of the
+ * blocked look-ahead; nothing on the eigenvector path calls it. */
+void orc_cwy_apply_block(int64_t n, int64_t k, const double* V, int64_t b, const double* X, int trans, double* U)
 {
-    int64_t n = a->n, m = a->count;
-    double* g = (double*)calloc((size_t)(m + 1), sizeof(double));
-    double* h = (double*)calloc((size_t)(m + 1), sizeof(double));
-    for (int64_t k = 0; k < m; k++) {
-        double s = 0.0;
-        for (int64_t i = 0; i < n; i++) s += Yget(a, i, k) * x[i];
-        g[k] = s;
+    orc_cwy_t a;
+    orc_cwy_init(&a, n, k > 0 ? k : 1);
+    double* q = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int64_t j = 0; j < k; j++) {
+        double c, nu;
+        orc_cwy_step(&a, j, V + j * n, q, &c, &nu);
     }
-    for (int64_t l = 0; l < m; l++) {
-        double s = 0.0;
-        for (int64_t k = l; k < m; k++) s += PT(a, l, k) * g[k];
-        h[l] = s;
+    double* g = (double*)calloc((size_t)(k + 1), sizeof(double));
+    double* h = (double*)calloc((size_t)(k + 1), sizeof(double));
+    for (int64_t v = 0; v < b; v++) {
+        const double* x = X + v * n;
+        double* out = U + v * n;
+        for (int64_t c = 0; c < k; c++) {                     /* g = Y^T x */
+            double s = 0.0;
+            for (int64_t i = 0; i < n; i++) s += Yget(&a, i, c) * x[i];
+            g[c] = s;
+        }
+        for (int64_t l = 0; l < k; l++) {                     /* h = T^T g  or  T g */
+            double s = 0.0;
+            if (trans) for (int64_t c = 0; c <= l; c++) s += PT(&a, c, l) * g[c];
+            else       for (int64_t c = l; c < k; c++) s += PT(&a, l, c) * g[c];
+            h[l] = s;
+        }
+        for (int64_t i = 0; i < n; i++) {                     /* U = x - Y h */
+            double s = 0.0;
+            for (int64_t c = 0; c < k; c++) s += Yget(&a, i, c) * h[c];
+            out[i] = x[i] - s;
+        }
     }
-    for (int64_t i = 0; i < n; i++) {
-        double s = 0.0;
-        for (int64_t k = 0; k < m; k++) s += Yget(a, i, k) * h[k];
-        out[i] = x[i] - s;
-    }
-    free(g); free(h);
+    free(g); free(h); free(q);
+    orc_cwy_free(&a);
 }
 
 /* ---------------------------------------------------------------- cross-checks */

@@ -78,8 +78,10 @@ void orc_cwy_step(orc_cwy_t* a, int64_t p, const double* v, double* q, double* c
 /* Alg.4 lines 10-11: build Y_1/T_1 from the accepted z. */
 void orc_cwy_first(orc_cwy_t* a, const double* z);
 
-/* Apply (I - Y T Y^T) to x (dense, all rows) -- test helper for Eq.(4). */
-void orc_cwy_apply(const orc_cwy_t* a, const double* x, double* out);
+/* Blocked look-ahead oracle: Y_k/T_k from V's first k columns (§3.3.2
+ * steps), then U[:, v] = x_v - Y (T^T (Y^T x_v)) (trans = 1) or x_v - Y (T (Y^T x_v)) (trans = 0)
+ * for the b columns of X; all arrays column-major, ld n. */
+void orc_cwy_apply_block(int64_t n, int64_t k, const double* V, int64_t b, const double* X, int trans, double* U);
 
 /* Alg. 2: Householder orthogonalisation of V (n x m, column-major,
  * ld n) into Q (ordinary sign, q_j = H_1...H_j e_j).  Test cross-check only. */

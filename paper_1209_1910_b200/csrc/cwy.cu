@@ -1074,6 +1074,25 @@ __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, boo
     }
 }
 
+// L2 prefetch of the first stages of this CTA's next wide pass (issued before the group
+// barrier that precedes the pass, so its first TMA copies hit L2): the pieces of the first
+// block with rows, for up to `nr` rows; lanes of warp 0, one prefetch per piece.
+template <class Src>
+__device__ __forceinline__ void pf_first(const Src& src, int r0, int r1, int nr) {
+    if (threadIdx.x >= 32 || r1 <= r0) return;
+    const int NB = src.nblk();
+    for (int kb = 0; kb < NB; kb++) {
+        int a, b;
+        src.rows(kb, r0, r1, a, b);
+        if (a >= b) continue;
+        for (int r = a + (int)threadIdx.x; r < b && r < a + nr; r += 32) {
+            const int lo = max(src.cs(r) & ~1, kb * PW), hi = min((src.ce(r) + 1) & ~1, kb * PW + PW);
+            if (hi > lo) l2_prefetch(src.base(r) + lo, hi - lo);
+        }
+        return;
+    }
+}
+
 // Row dots of a wide pass: dot(r) = sum_{cs(r) <= k < ce(r)} row_r[k] v[k] (and with a second
 // vector w when TWO); epi(r, dot, dot2) after all blocks, one thread per row.
 template <bool TWO, class Src, class Epi>
@@ -1918,6 +1937,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         }
                     }
                 }
+                if (a.pf && p > kNarrowM) pf_first(SrcTc{Tc, (int)p}, (int)ptt0, (int)ptt1, a.pf);
                 gsync();
                 PH(2);
                 // ---------------- TT: g' = T_p^T g
@@ -1934,6 +1954,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                 [&](int64_t k) -> int64_t { return k + 1; },
                                 [&](int64_t k, double v) { mst(ws.gp + k, v); });
                     }
+                }
+                if (a.pf && p > kNarrowM) {
+                    int64_t i0, i1;
+                    part_uniform(p, n, cg, Gt, i0, i1);
+                    pf_first(SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, a.pf);
                 }
                 gsync();
                 PH(3);
@@ -2049,6 +2074,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     }
                 }
                 if (dsub && !(a.dbg & 2)) dtim[3] += dclk() - q2m;
+                if (a.pf && p > kNarrowM) pf_first(SrcTr{Tr, (int)m2, (int)p}, (int)ptn0, (int)ptn1, a.pf);
                 gsync();
                 PH(5);
                 // ---------------- TN: [Ts, h] = T_p [s, yrow]; column p of T and Y; x'
@@ -2112,6 +2138,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     for (int64_t i = i0 + tid; i < i1; i += NT)
                         st(Y + y_row_off(i, m) + p, (i == p) ? y0 : (zero_u ? 0.0 : ld(ws.u + i)));
                 }
+                if (a.pf && p + 1 > kNarrowM) pf_first(SrcY{Y, (int)m, (int)p + 1}, (int)pd0, (int)pd1, a.pf);
                 gsync();
                 PH(6);
                 }   // reduced / ordinary compact-WY step

@@ -1199,6 +1199,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.dbg = getenv("TINV_DBG") ? atoi(getenv("TINV_DBG")) : 0;
         ca.reorth = h->mgs;
         ca.lab = lab;
+        ca.pf = getenv("TINV_PF") ? atoi(getenv("TINV_PF")) : 0;
         unsigned long long* pcta = nullptr;
         if (getenv("TINV_PROF_CTA")) {   // debug only (not the product path): per-CTA phase busy times
             CK(cudaMalloc(&pcta, sizeof(unsigned long long) * 16 * sc.nctas));

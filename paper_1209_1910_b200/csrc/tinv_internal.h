@@ -176,6 +176,7 @@ struct CwyArgs {
     int dbg;                 // debug build experiments (TINV_DBG bits)
     int reorth;              // 0 reduced compact WY (§3.3.2), 1 classical MGS (Alg. 1), 2 ordinary compact WY (§3.3.1)
     int lab;                 // blocked look-ahead block size b (2..8; 0/1 = off), wide clusters of single-rank groups
+    int pf;                  // rows whose first pieces of the next wide pass are prefetched into L2 before a barrier (TINV_PF; 0 = off)
     unsigned long long* prof_cta;   // debug: per-CTA busy time before each phase's barrier [cta*16 + phase], or NULL
 };
 

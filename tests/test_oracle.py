@@ -203,6 +203,23 @@ def test_eq4_compact_wy_identity():
         assert np.abs(lhs - _dense_householder_product(Y, T)).max() <= 1e-13
 
 
+def test_cwy_apply_block_is_householder_q():
+    """Blocked look-ahead oracle: U = (I - Y T Y^T)^T X with Y, T from k
+    columns of V is Q^T X for the complete Q of LAPACK's Householder QR of V (dgeqrf/dorgqr:
+    H_1 .. H_k with the same sign convention beta = -sign(alpha) ||.||), and the untransposed
+    application is Q X.  Independent of the oracle's own Y/T algebra."""
+    rng = np.random.default_rng(14)
+    for n, k, b in [(6, 1, 1), (12, 5, 3), (40, 17, 8), (120, 60, 8)]:
+        V = rng.normal(size=(n, k))
+        X = rng.normal(size=(n, b))
+        Q, _ = np.linalg.qr(V, mode="complete")
+        assert np.abs(O.cwy_apply_block(V, X, trans=True) - Q.T @ X).max() <= 1e-12 * max(1.0, np.abs(X).max())
+        assert np.abs(O.cwy_apply_block(V, X, trans=False) - Q @ X).max() <= 1e-12 * max(1.0, np.abs(X).max())
+    # k = 0: nothing applied
+    X = rng.normal(size=(9, 2))
+    assert np.array_equal(O.cwy_apply_block(np.zeros((9, 0)), X), X)
+
+
 def test_cwy_equals_householder_qr():
     # Householder-QR special case: cWY-orthogonalising V yields QR(V)'s Q up to column signs.
     rng = np.random.default_rng(12)
