@@ -552,3 +552,32 @@ def test_rescaling_reading21_scale_free():
         assert wv <= 1e-10 and ws >= 1 - 1e-10
         outs[k] = Z
     assert np.array_equal(outs[300], outs[-500]) and np.array_equal(outs[300], outs[-1000])
+
+
+def test_cfg5_golden_columns_are_eigenvectors():
+    """tests/golden/cfg5_oracle_cols.npz (written by tests/golden/make_cfg5_golden.py from a
+    full oracle run on cfg5, n = 16000, one cluster): the stored columns are unit eigenvectors
+    of T for the stored w (residual <= 10 n eps ||T||_1, the P0 bound), mutually orthogonal,
+    the stored w is the workload's (hash and values), and every vector took 2 iterations."""
+    import hashlib
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg5_oracle_cols.npz")
+    if not os.path.exists(path):
+        pytest.skip("cfg5 golden columns not generated")
+    g = np.load(path)
+    d, e, w = W.problem("cfg5")
+    n = len(d)
+    wg = np.asarray(g["w"])
+    assert g["w_sha"].item().decode() == hashlib.sha256(np.ascontiguousarray(wg).tobytes()).hexdigest()
+    tn = O.tnorm(d, e)
+    assert np.abs(wg - w).max() <= 1e3 * EPS * tn
+    assert int(g["info"]) == 0 and (np.asarray(g["iters"]) == 2).all()
+    cols = np.asarray(g["cols"])
+    Z = np.asarray(g["Z"])
+    TZ = d[:, None] * Z
+    TZ[:-1] += e[:, None] * Z[1:]
+    TZ[1:] += e[:, None] * Z[:-1]
+    res = np.linalg.norm(TZ - Z * wg[cols][None, :], axis=0).max() / (n * EPS * tn)
+    assert res <= 10.0, res
+    G = Z.T @ Z
+    assert np.abs(G - np.eye(len(cols))).max() / (n * EPS) <= 10.0
