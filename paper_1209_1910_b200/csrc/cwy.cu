@@ -534,7 +534,9 @@ __device__ __forceinline__ unsigned int acquire(const unsigned int* prog) {
 }
 
 __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const Smem& sm, uint32_t& mbph,
-                           unsigned int* prog = nullptr, unsigned int tag = 0) {
+                           unsigned int* prog = nullptr, unsigned int tag = 0, uint64_t* dt = nullptr) {
+    // dt (debug build, TINV_DBG bit 3): SM clocks in [0] ring waits, [1] the chains, [2] the rest, [3] total
+    const uint64_t d0 = dt ? (uint64_t)clock64() : 0;
     const int64_t n = a.n;
     const double* __restrict__ F = a.F + j * n * 4;
     const double* __restrict__ ts = ws.ysol;
@@ -561,9 +563,11 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
     for (int64_t k = 0; k < C; k++) {
         const int slot = (int)(k % kRing);
         double* xb = xbuf + (k & 1) * CH;
+        const uint64_t e0 = dt ? (uint64_t)clock64() : 0;
         bulk_wait_read<1>();   // the store of chunk k-2 has read this buffer
         mbar_wait(sm.mbar + slot, (mbph >> slot) & 1u);
         mbph ^= 1u << slot;
+        const uint64_t e1 = dt ? (uint64_t)clock64() : 0;
         const double* Fs = ring + (int64_t)slot * 5 * CH;
         const double* Ts = Fs + 4 * CH;
         const int64_t c = C - 1 - k;
@@ -599,6 +603,12 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
                 *reinterpret_cast<double2*>(xb + u0 + u) = make_double2(xv[u], xv[u + 1]);
         }
         if (cnt & 1) xb[cnt] = 0.0;   // x[n] (padding of the last, odd chunk)
+        if (dt) {
+            const uint64_t e2 = (uint64_t)clock64();
+            dt[0] += e1 - e0;
+            dt[1] += e2 - e1;
+            dt[2] -= e2;   // + the chunk's end below
+        }
         fence_proxy_async_smem();     // generic smem writes -> the bulk store
         bulk_s2g(x + lo, xb, (uint32_t)((cnt + 1) & ~1) * 8u);
         bulk_commit();
@@ -611,10 +621,12 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
             fence_proxy_async_global();
             publish(prog, tag + (unsigned int)(k / a.band_ch));
         }
+        if (dt) dt[2] += (uint64_t)clock64();
     }
     bulk_wait_all();
     fence_proxy_async_global();   // the bulk-stored x before the group barrier's release
     if (prog) publish(prog, tag + (unsigned int)sweep_bands(n, a.band_ch));
+    if (dt) dt[3] += (uint64_t)clock64() - d0;
 }
 
 // Composition of the forward maps of CTAs 0..cnt-1 (S slots FA, FB), applied in CTA order, by
@@ -1459,8 +1471,11 @@ __device__ void lab_rowdots(const Smem& sm, int64_t r0, int64_t r1, int64_t P, c
     for (int64_t rb0 = r0; rb0 < r1; rb0 += 4096 / NV) {   // row blocks whose sums fit `acc`
         const int64_t rb1 = (rb0 + 4096 / NV < r1) ? rb0 + 4096 / NV : r1;
         for (int64_t q = tid; q < (rb1 - rb0) * NV; q += NT) acc[q] = 0.0;
-        for (int64_t c0 = 0; c0 < P; c0 += CC) {
-            const int64_t c1 = (c0 + CC < P) ? c0 + CC : P;
+        int64_t lmax = 0;   // the longest row of the block: no chunk beyond it is staged
+        for (int64_t r = rb0; r < rb1; r++) lmax = max(lmax, rowlen(r));
+        const int64_t Pc = (lmax < P) ? lmax : P;
+        for (int64_t c0 = 0; c0 < Pc; c0 += CC) {
+            const int64_t c1 = (c0 + CC < Pc) ? c0 + CC : Pc;
             // the nv vectors' columns [c0, c1) by TMA; vectors >= nv: zero
             tma_stage(sm, nv, [&](int v) { return V + v * ldv + c0; }, c1 - c0, vs, CC);
             for (int64_t q = tid; q < (int64_t)(NV - nv) * CC; q += NT) vs[(int64_t)nv * CC + q] = 0.0;
@@ -1909,7 +1924,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         part_uniform(0, p - 1, cg, Gt, k0, k1);
                         reduce_partials(sm, ws.P2, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
                         const uint64_t q1 = dclk();
-                        const bool dla = dsub && !(a.dbg & 3);
+                        const bool dla = dsub && !(a.dbg & 11);
                         if (dla) dtim[0] += q1 - q0;
                         const double gl = reduce_slot(sm, S, Gt, SSlots::GPN);
                         if (r == 0 && tid == 0) st(ws.g + p - 1, gl);   // every rank, its own replica
@@ -1929,7 +1944,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                 dtim[3] += dclk() - q2;
                             }
                             dA = 0;
-                        } else if (dsub) dtim[0] += q1 - q0;
+                        } else if (dsub && !(a.dbg & 8)) dtim[0] += q1 - q0;
                         if (kWideDebug && (a.dbg & 1)) {   // experiment: the same reduction again
                             reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks,
                                             dsub ? dtim + 2 : nullptr);
@@ -2049,7 +2064,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 const double y0 = u0 - c;
                 const double* yrow = Y + y_row_off(p, m);
                 const uint64_t q2m = dclk();
-                if (dsub && !(a.dbg & 3)) dtim[2] += q2m - q2s;
+                if (dsub && !(a.dbg & 11)) dtim[2] += q2m - q2s;
                 if (mode == 2) {
                     // ordinary sequence (§3.3.1): s = Y_p^T y_p by a pass of its
                     // own over rows p..n-1 (y_p = uhat with its first entry y_0), then reduced
@@ -2073,7 +2088,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                         [&](int64_t k, double v) { mst(ws.s + k, v - c * ld(yrow + k)); }, rks);
                     }
                 }
-                if (dsub && !(a.dbg & 2)) dtim[3] += dclk() - q2m;
+                if (dsub && !(a.dbg & 10)) dtim[3] += dclk() - q2m;
                 if (a.pf && p > kNarrowM) pf_first(SrcTr{Tr, (int)m2, (int)p}, (int)ptn0, (int)ptn1, a.pf);
                 gsync();
                 PH(5);
@@ -2390,7 +2405,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         __syncthreads();
                         rph = *reinterpret_cast<volatile uint32_t*>(sm.red + NW + 7);
                     } else if (r == 0 && tid == 0) {
-                        back_sweep(a, ws, j, sm, mbph, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8);
+                        back_sweep(a, ws, j, sm, mbph, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8,
+                                   (kWideDebug && (a.dbg & 8) && dsub) ? dtim : nullptr);
                     }
                     mark(10);
                     if (a2 && r > 0) {
