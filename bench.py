@@ -4,11 +4,12 @@ iteration with compact-WY reorthogonalisation (DSTEIN-cWY, Alg. 4), fp6
 
 Metric (BASELINE.json): eigenvectors/s (all n, fp64) at n = 2000-16000; reorth HBM GB/s vs
 peak.  One step = one tinv_eigvecs call on one synthetic input resident in HBM.  Default
-workload: configs[3] (cfg4, n = 8000, one giant cluster): the HBM-bound regime the metric's
-"reorth HBM GB/s vs peak" half refers to.  Other configs: --config cfg1..cfg5 (cfg2 = the
+workload: configs[4] (cfg5, n = 16000, the top of the metric's n range; one cluster of 16000
+vectors): the HBM-bound regime the metric's "reorth HBM GB/s vs peak" half refers to, ~18 s
+per step.  Other configs: --config cfg1..cfg5 (cfg4 = n = 8000, one cluster; cfg2 = the
 n = 2000 many-small-clusters, latency-bound case).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl tinv|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl tinv|reference]
 
 --gpus N > 1 without a torch.distributed environment re-executes itself under
 torch.distributed.run (one process per GPU, NCCL, 127.0.0.1).  Multi-rank: a single giant
@@ -230,7 +231,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None, help="timed steps (default 5 for cfg4/cfg5, else 30)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg4", choices=list(WORKLOAD_DESC))
+    ap.add_argument("--config", default="cfg5", choices=list(WORKLOAD_DESC))
     ap.add_argument("--impl", default="tinv", choices=["tinv", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")

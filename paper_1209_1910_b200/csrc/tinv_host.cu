@@ -1194,7 +1194,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.piece_cost = getenv("TINV_PIECE_COST") ? atoi(getenv("TINV_PIECE_COST")) : 4000;
         ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
         ca.a2 = getenv("TINV_A2") ? atoi(getenv("TINV_A2")) : 1;
-        ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 16;
+        ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 8;
         ca.poll_ns = getenv("TINV_POLLNS") ? atoi(getenv("TINV_POLLNS")) : 0;
         ca.dbg = getenv("TINV_DBG") ? atoi(getenv("TINV_DBG")) : 0;
         ca.reorth = h->mgs;
