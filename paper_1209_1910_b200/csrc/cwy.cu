@@ -44,6 +44,7 @@ constexpr int kRing = 4;                             // back-sweep ring depth
 constexpr int64_t kSolveDoubles = kRing * 5 * CH;    // back-sweep ring slots (4 CH factor doubles + CH t)
 constexpr int kVsD = 128;                            // staged vector of the short (P <= 65) passes
 constexpr int kNBar = 32;                            // mbarrier slots (incl. 2 use counters), 16-B multiple
+constexpr int kXFull = 27, kXEmpty = 29;             // two-thread back sweep: x staging handover (2 + 2)
 
 // Global accesses: data produced inside this kernel by other CTAs goes through L2 (.cg,
 // never a stale L1 line); explicit global-space intrinsics also let the compiler hoist
@@ -629,6 +630,160 @@ __device__ void back_sweep(const CwyArgs& a, const GroupWS& ws, int64_t j, const
     if (dt) dt[3] += (uint64_t)clock64() - d0;
 }
 
+// One 256-row chunk of the back-sweep chain (rows cnt-1 .. 0 of the ring slot, x into xb), as a
+// separate non-inlined function: the kernel's register pressure (255, spills) does not reach
+// this loop (TINV_SWEEP2=2).
+__device__ __noinline__ void sweep_chunk(const double* __restrict__ Fs, const double* __restrict__ Ts, double* __restrict__ xb,
+                                         int cnt, double* x12) {
+    double x1 = x12[0], x2 = x12[1];
+    const int top = cnt & ~15;
+    for (int u = cnt - 1; u >= top; u--) {
+        const double2 bc = *reinterpret_cast<const double2*>(Fs + u * 4 + 2);
+        const double xi = fma(-bc.x, x1, fma(-bc.y, x2, Ts[u]));
+        xb[u] = xi;
+        x2 = x1;
+        x1 = xi;
+    }
+    for (int u0 = top - 16; u0 >= 0; u0 -= 16) {
+        double bb[16], cc[16], tt[16], xv[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            const double2 bc = *reinterpret_cast<const double2*>(Fs + (u0 + u) * 4 + 2);
+            bb[u] = bc.x; cc[u] = bc.y; tt[u] = Ts[u0 + u];
+        }
+#pragma unroll
+        for (int u = 15; u >= 0; u--) {
+            xv[u] = fma(-bb[u], x1, fma(-cc[u], x2, tt[u]));
+            x2 = x1;
+            x1 = xv[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u += 2)
+            *reinterpret_cast<double2*>(xb + u0 + u) = make_double2(xv[u], xv[u + 1]);
+    }
+    x12[0] = x1;
+    x12[1] = x2;
+}
+
+// The same sweep split over two threads of CTA 0 (the wide window, where warps 1.. of CTA 0 are
+// otherwise idle): the chain thread (`helper` false) only waits for its ring slot, runs the
+// 16-row batches into the x staging buffer and hands the chunk over (fence.proxy.async +
+// mbarrier xfull); the helper thread (warp 1) refills the ring, issues the chunk's bulk store,
+// frees the staging buffer (mbarrier xempty) once the store has read it, and publishes the
+// bands.  The per-chunk TMA / bulk-store / release work (~16% of the single-thread sweep) leaves
+// the dependent chain.  Same arithmetic, same order as back_sweep.  `xseq` counts the chunks
+// of every such sweep (both threads keep identical copies): buffer = seq & 1, its use = seq >> 1.
+__device__ void back_sweep_ws(const CwyArgs& a, const GroupWS& ws, int64_t j, const Smem& sm, uint32_t& mbph,
+                              uint32_t& xseq, bool helper, unsigned int* prog, unsigned int tag) {
+    const int64_t n = a.n;
+    const double* __restrict__ F = a.F + j * n * 4;
+    const double* __restrict__ ts = ws.ysol;
+    double* __restrict__ x = ws.x;
+    double* ring = sm.bring;
+    const int64_t C = (n + CH - 1) / CH;
+    uint64_t* xfull = sm.mbar + kXFull;
+    uint64_t* xempty = sm.mbar + kXEmpty;
+    double* xbuf = sm.racc;   // 2 CH doubles
+    auto rows = [&](int64_t k, int64_t& lo, int64_t& hi) {
+        const int64_t c = C - 1 - k;
+        lo = c * CH;
+        hi = (lo + CH < n) ? lo + CH : n;
+    };
+    if (helper) {
+        auto issue = [&](int64_t k) {
+            const int slot = (int)(k % kRing);
+            int64_t lo, hi;
+            rows(k, lo, hi);
+            const uint32_t fb = (uint32_t)((hi - lo) * 32), tb = (uint32_t)(((hi - lo + 1) & ~int64_t(1)) * 8);
+            double* dst = ring + (int64_t)slot * 5 * CH;
+            mbar_expect_tx(sm.mbar + slot, fb + tb);
+            bulk_g2s(dst, F + lo * 4, fb, sm.mbar + slot);
+            bulk_g2s(dst + 4 * CH, ts + lo, tb, sm.mbar + slot);
+        };
+        fence_proxy_async_global();
+        for (int64_t k = 0; k < C && k < kRing; k++) issue(k);
+        for (int64_t k = 0; k < C; k++) {
+            const uint32_t sq = xseq + (uint32_t)k, b = sq & 1u;
+            mbar_wait(xfull + b, (sq >> 1) & 1u);   // chunk k in xbuf[b]; its ring slot is consumed
+            if (k + kRing < C) issue(k + kRing);
+            int64_t lo, hi;
+            rows(k, lo, hi);
+            bulk_s2g(x + lo, xbuf + b * CH, (uint32_t)((hi - lo + 1) & ~int64_t(1)) * 8u);
+            bulk_commit();
+            if (k > 0) {   // the store of chunk k-1 has read its buffer
+                bulk_wait_read<1>();
+                mbar_arrive(xempty + (b ^ 1u));
+            }
+            // band b = chunks [b band_ch, (b+1) band_ch) complete once at most the newest group
+            // (this chunk's store) is pending
+            if (prog && k % a.band_ch == 0 && k > 0) {
+                asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+                fence_proxy_async_global();
+                publish(prog, tag + (unsigned int)(k / a.band_ch));
+            }
+        }
+        bulk_wait_read<0>();
+        mbar_arrive(xempty + ((xseq + (uint32_t)C - 1u) & 1u));
+        bulk_wait_all();
+        fence_proxy_async_global();   // the bulk-stored x before the group barrier's release
+        if (prog) publish(prog, tag + (unsigned int)sweep_bands(n, a.band_ch));
+    } else {
+        double x1 = 0.0, x2 = 0.0;
+        for (int64_t k = 0; k < C; k++) {
+            const uint32_t sq = xseq + (uint32_t)k, b = sq & 1u;
+            const int slot = (int)(k % kRing);
+            double* xb = xbuf + b * CH;
+            if (sq >= 2u) mbar_wait(xempty + b, ((sq >> 1) - 1u) & 1u);   // the store of seq - 2 read it
+            mbar_wait(sm.mbar + slot, (mbph >> slot) & 1u);
+            mbph ^= 1u << slot;
+            const double* Fs = ring + (int64_t)slot * 5 * CH;
+            const double* Ts = Fs + 4 * CH;
+            int64_t lo, hi;
+            rows(k, lo, hi);
+            const int cnt = (int)(hi - lo);
+            if (a.sweep2 == 2) {
+                double x12[2] = {x1, x2};
+                sweep_chunk(Fs, Ts, xb, cnt, x12);
+                x1 = x12[0];
+                x2 = x12[1];
+                if (cnt & 1) xb[cnt] = 0.0;
+                fence_proxy_async_smem();
+                mbar_arrive(xfull + b);
+                continue;
+            }
+            const int top = cnt & ~15;
+            for (int u = cnt - 1; u >= top; u--) {
+                const double2 bc = *reinterpret_cast<const double2*>(Fs + u * 4 + 2);
+                const double xi = fma(-bc.x, x1, fma(-bc.y, x2, Ts[u]));
+                xb[u] = xi;
+                x2 = x1;
+                x1 = xi;
+            }
+            for (int u0 = top - 16; u0 >= 0; u0 -= 16) {
+                double bb[16], cc[16], tt[16], xv[16];
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const double2 bc = *reinterpret_cast<const double2*>(Fs + (u0 + u) * 4 + 2);
+                    bb[u] = bc.x; cc[u] = bc.y; tt[u] = Ts[u0 + u];
+                }
+#pragma unroll
+                for (int u = 15; u >= 0; u--) {
+                    xv[u] = fma(-bb[u], x1, fma(-cc[u], x2, tt[u]));
+                    x2 = x1;
+                    x1 = xv[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 16; u += 2)
+                    *reinterpret_cast<double2*>(xb + u0 + u) = make_double2(xv[u], xv[u + 1]);
+            }
+            if (cnt & 1) xb[cnt] = 0.0;   // x[n] (padding of the last, odd chunk)
+            fence_proxy_async_smem();     // generic smem writes -> the helper's bulk store
+            mbar_arrive(xfull + b);
+        }
+    }
+    xseq += (uint32_t)C;
+}
+
 // Composition of the forward maps of CTAs 0..cnt-1 (S slots FA, FB), applied in CTA order, by
 // warp 0 (lane-serial pieces + a warp scan); broadcast through `buf`.
 __device__ __forceinline__ Aff1 compose_ctas(const double* S, int cnt, Aff1* buf) {
@@ -893,6 +1048,7 @@ constexpr int NCW = NW - 1;              // consumer warps
 constexpr int NCT = NCW * 32;            // consumer threads
 constexpr int PW = 2 * NCT;              // column block / piece width (doubles) = 448
 static_assert(PW == kPieceW, "piece width of the partitions");
+static_assert(PW == kWidePieceW, "piece width known to the host (workspace sizes)");
 constexpr int PPS = NCW;                 // pieces per stage = consumer warps
 constexpr int RCH = 1024;                // rows per chunk (row accumulators; coefficients in Smem::cf)
 constexpr int kWStgD = PPS * PW;         // doubles per wide ring slot
@@ -977,7 +1133,7 @@ __device__ __forceinline__ int wide_rps(int pst) { return min(2 * NCW, kWStgD / 
 // ones copied) and blk_end(kb) after its last stage; these may use consumer_sync() but not
 // __syncthreads.  chunk_begin / chunk_end run on all threads around each chunk (may
 // __syncthreads).
-template <class Src, class Body, class BlkBegin, class BlkEnd, class ChunkBegin, class ChunkEnd>
+template <int CR = RCH, class Src, class Body, class BlkBegin, class BlkEnd, class ChunkBegin, class ChunkEnd>
 __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, bool reverse_blocks, uint64_t pol,
                             ChunkBegin chunk_begin, BlkBegin blk_begin, Body body, BlkEnd blk_end,
                             ChunkEnd chunk_end) {
@@ -986,8 +1142,8 @@ __device__ void wide_stream(const WRing& rg, const Src& src, int r0, int r1, boo
     // piece stride / rows per stage: a single narrow block packs up to 32 rows per stage
     const int PST = wide_pst(src);
     const int RPS = wide_rps(PST);
-    for (int c0 = r0; c0 < r1; c0 += RCH) {
-        const int c1 = min(r1, c0 + RCH);
+    for (int c0 = r0; c0 < r1; c0 += CR) {
+        const int c1 = min(r1, c0 + CR);
         chunk_begin(c0, c1);
         auto blk_of = [&](int t) { return reverse_blocks ? NB - 1 - t : t; };
         // stage cursor: block step t, next row; returns false at the end
@@ -1247,6 +1403,10 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
     if (r1 <= r0) return 0.0;
     double* cf2 = sm.racc;   // second coefficient chunk (the row accumulators are unused here)
     static_assert(2 * RCH >= CFCH, "second coefficient chunk in the row accumulators");
+    // accumulating passes (several chunks / calls): the block's previous sums are loaded when the
+    // block starts and added at its end, so the L2 round trip overlaps the block's stages
+    // instead of stalling every block end (the fused pass A2 runs ~8 calls per vector)
+    double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
     wide_stream(
         rg, src, r0, r1, reverse_blocks, pol,
         [&](int c0, int c1) {
@@ -1264,7 +1424,17 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
             __syncthreads();
             a0 = a1 = b0 = b1 = 0.0;
         },
-        [&](int, int, int) {},
+        [&](int kb, int, int) {
+            if (multi) {
+                const int k = kb * PW + 2 * tc;
+                o0 = (k < P) ? ld(out + k) : 0.0;
+                o1 = (k + 1 < P) ? ld(out + k + 1) : 0.0;
+                if (TWO) {
+                    o2 = (k < P) ? ld(out2 + k) : 0.0;
+                    o3 = (k + 1 < P) ? ld(out2 + k + 1) : 0.0;
+                }
+            }
+        },
         [&](int kb, int ra, int rb, const double* slot) {
             const int k = kb * PW + 2 * tc;
             const int PST = wide_pst(src);
@@ -1311,12 +1481,12 @@ __device__ double wide_colacc(const Smem& sm, const WRing& rg, const Src& src, i
         [&](int kb) {
             const int k = kb * PW + 2 * tc;
             if (k < P) {
-                st(out + k, multi ? ld(out + k) + a0 : a0);
-                if (TWO) st(out2 + k, multi ? ld(out2 + k) + b0 : b0);
+                st(out + k, multi ? o0 + a0 : a0);
+                if (TWO) st(out2 + k, multi ? o2 + b0 : b0);
             }
             if (k + 1 < P) {
-                st(out + k + 1, multi ? ld(out + k + 1) + a1 : a1);
-                if (TWO) st(out2 + k + 1, multi ? ld(out2 + k + 1) + b1 : b1);
+                st(out + k + 1, multi ? o1 + a1 : a1);
+                if (TWO) st(out2 + k + 1, multi ? o3 + b1 : b1);
             }
             a0 = a1 = b0 = b1 = 0.0;
         },
@@ -1455,6 +1625,143 @@ __device__ void lab_gemm1(const Smem& sm, const double* __restrict__ Y, int64_t 
     }
 }
 
+// BL1 streamed through the wide ring (the column split above reads ~430-byte row segments and
+// reaches ~1.2 TB/s on cfg5).  Work units are (column block kb, row i) for i in [kb PW, n),
+// kb < ceil(k / PW), in block-major order, split evenly over the Gt CTAs; a CTA's range is one
+// or a few segments (a column block, a row range), each streamed with whole 448-column row
+// pieces.  Consumer thread t' owns the block's columns 2t', 2t'+1 and accumulates them against
+// the nv vectors' rows (staged per 512-row chunk) for the whole segment; the segment's sums go
+// to partial slot kb + q (slots are unique: in block-major order every new (block, CTA)
+// incidence starts at a block or a CTA boundary), and lab_bl1_reduce adds the slots of each
+// block in CTA order (deterministic).
+struct SrcYB {     // column block kb of Y_P alone: columns [kb PW, min(P, kb PW + PW))
+    const double* Y;
+    int m, P, kb;
+    __device__ const double* base(int r) const { return Y + y_row_off(r, m) + (int64_t)kb * PW; }
+    __device__ int cs(int) const { return 0; }
+    __device__ int ce(int r) const { return min(r + 1, P) - kb * PW; }
+    __device__ void rows(int, int r0, int r1, int& a, int& b) const {
+        a = max(r0, kb * PW);
+        b = r1;
+    }
+    __device__ int nblk() const { return 1; }
+    __device__ int width() const { return min(PW, P - kb * PW); }
+};
+constexpr int kBl1CR = 510;   // rows per coefficient chunk
+constexpr int kBl1XS = 512;   // staged rows per vector: the chunk from its even-aligned start (TMA: 16-B aligned)
+static_assert(kLabMax * kBl1XS <= CFCH + 2 * RCH, "BL1 coefficient chunk in cf + racc");
+__device__ __forceinline__ int64_t bl1_cum(int64_t kb, int64_t n) { return kb * n - (int64_t)PW * (kb * (kb - 1) / 2); }
+__device__ __forceinline__ int64_t bl1_bound(int64_t U, int q, int Gt) { return (U * q) / Gt; }
+// CTA whose unit range holds unit u
+__device__ __forceinline__ int bl1_owner(int64_t U, int64_t u, int Gt) {
+    int q = (int)min((int64_t)Gt - 1, (u * Gt) / (U > 0 ? U : 1));
+    while (q + 1 < Gt && bl1_bound(U, q + 1, Gt) <= u) q++;
+    while (q > 0 && bl1_bound(U, q, Gt) > u) q--;
+    return q;
+}
+
+template <int NV>
+__device__ void lab_bl1_stream(const Smem& sm, const WRing& rg, const double* __restrict__ Y, int64_t m, int64_t n,
+                               int64_t k, const double* X, int64_t xst, int nv, double* PB, int q, int Gt,
+                               int64_t x0, int64_t x1, double* xsq, uint64_t pol) {
+    const int tid = threadIdx.x, tc = tid - 32;
+    {   // ||X_v||^2 partials (rows [x0, x1))
+        double qq[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) qq[v] = 0.0;
+        for (int64_t i = x0 + tid; i < x1; i += NT)
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                const double xv = (v < nv) ? ld(X + v * xst + i) : 0.0;
+                qq[v] = fma(xv, xv, qq[v]);
+            }
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            const double t = block_sum<NT>(qq[v], sm.red);
+            if (tid == 0) xsq[v] = t;
+        }
+    }
+    const int64_t NB = (k + PW - 1) / PW;
+    const int64_t U = bl1_cum(NB, n);
+    int64_t u = bl1_bound(U, q, Gt);
+    const int64_t ue = bl1_bound(U, q + 1, Gt);
+    double* xs = sm.cf;   // [v][kBl1XS] (cf and racc are contiguous)
+    while (u < ue) {
+        // segment: block kb, rows [ra, rb)
+        int64_t kb = 0;
+        while (kb + 1 < NB && bl1_cum(kb + 1, n) <= u) kb++;
+        const int64_t blk_end = bl1_cum(kb + 1, n);
+        const int64_t ra = kb * PW + (u - bl1_cum(kb, n));
+        const int64_t rb = ra + ((ue < blk_end ? ue : blk_end) - u);
+        const int gc = (int)kb * PW + 2 * tc;   // this consumer's first column
+        double acc[NV][2];
+#pragma unroll
+        for (int v = 0; v < NV; v++) acc[v][0] = acc[v][1] = 0.0;
+        int cb = 0;
+        const SrcYB src{Y, (int)m, (int)k, (int)kb};
+        const int PST = wide_pst(src);
+        wide_stream<kBl1CR>(
+            rg, src, (int)ra, (int)rb, false, pol,
+            [&](int c0, int c1) {
+                cb = c0 & ~1;
+                tma_stage(sm, nv, [&](int v) { return X + v * xst + cb; }, c1 - cb, xs, kBl1XS);
+                for (int t = tid; t < (NV - nv) * kBl1XS; t += NT) xs[nv * kBl1XS + t] = 0.0;
+                __syncthreads();
+            },
+            [&](int, int, int) {},
+            [&](int, int sa, int sb, const double* slot) {
+                if (2 * tc >= PST) return;
+                // every row of the stage covers the whole (full-width) block: no masks
+                const bool full = (sa >= (int)kb * PW + PW - 1) && ((int)kb * PW + PW <= (int)k);
+                for (int qr = 0; qr < sb - sa; qr++) {
+                    const int i = sa + qr;
+                    const double2 y = *reinterpret_cast<const double2*>(slot + qr * PST + 2 * tc);
+                    double y0 = y.x, y1 = y.y;
+                    if (!full) {
+                        y0 = (gc <= i && gc < (int)k) ? y0 : 0.0;
+                        y1 = (gc + 1 <= i && gc + 1 < (int)k) ? y1 : 0.0;
+                    }
+                    const double* xr = xs + (i - cb);
+#pragma unroll
+                    for (int v = 0; v < NV; v++) {
+                        const double xv = xr[v * kBl1XS];
+                        acc[v][0] = fma(y0, xv, acc[v][0]);
+                        acc[v][1] = fma(y1, xv, acc[v][1]);
+                    }
+                }
+            },
+            [&](int) {}, [&](int, int) {});
+        if (tc >= 0) {
+            double* slotp = PB + (kb + q) * (int64_t)(NV * PW);
+#pragma unroll
+            for (int v = 0; v < NV; v++)
+                *reinterpret_cast<double2*>(slotp + v * PW + 2 * tc) = make_double2(acc[v][0], acc[v][1]);
+        }
+        u += rb - ra;
+    }
+}
+
+// G[v][c] (ldg) for this CTA's columns: the slots of c's block summed in CTA order
+template <int NV>
+__device__ void lab_bl1_reduce(const double* PB, int64_t k, int64_t n, int q, int Gt, int nv, double* G, int64_t ldg) {
+    const int64_t NB = (k + PW - 1) / PW;
+    const int64_t U = bl1_cum(NB, n);
+    int64_t c0, c1;
+    part_uniform(0, k, q, Gt, c0, c1);
+    for (int64_t t = threadIdx.x; t < (c1 - c0) * nv; t += NT) {
+        const int v = (int)(t / (c1 - c0));
+        const int64_t c = c0 + t % (c1 - c0);
+        const int64_t kb = c / PW, lc = c - kb * PW;
+        const int qa = bl1_owner(U, bl1_cum(kb, n), Gt), qb = bl1_owner(U, bl1_cum(kb + 1, n) - 1, Gt);
+        double sum = 0.0;
+        for (int r = qa; r <= qb; r++) {
+            if (bl1_bound(U, r + 1, Gt) <= bl1_bound(U, r, Gt)) continue;   // empty range
+            sum += ld(PB + (kb + r) * (int64_t)(NV * PW) + v * PW + lc);
+        }
+        st(G + v * ldg + c, sum);
+    }
+}
+
 // BL2 / BL3: out_v[r] = base_v(r) - sum_{k in row r} row_r[k] V_v[k] for rows [r0, r1) (warp per
 // row, vectors V staged in shared memory by chunks of CC columns, per-row sums in shared memory).
 //   BL2: rows l of column-packed T (T[0..l][l]), V = G, base = 0       -> G'
@@ -1556,6 +1863,86 @@ __device__ void lab_rowdots(const Smem& sm, int64_t r0, int64_t r1, int64_t P, c
     }
 }
 
+// ---------------------------------------------------------------- fused pass A2, column-owner form
+// Pass A of iteration 2 (g = Y_p^T x) streamed behind the back sweep band by band.  Each of the
+// Gl = G - 1 streaming CTAs owns one column block kb of Y_p (CTAs per block in proportion to
+// the block's elements, at least one) and, in every band, an even share of the band's rows that
+// reach the block; its 448 column sums stay in registers across all bands (no global
+// read-modify-write per band and block) and are written once.  R1 then adds the few partials of
+// each block in CTA order.  Needs NB <= Gl blocks.
+__device__ __forceinline__ int64_t a2c_work(int64_t kb, int64_t n, int64_t P) {
+    return (n - kb * PW) * (int64_t)min((int64_t)PW, P - kb * PW);
+}
+// first streaming CTA (0-based among the Gl) of block kb
+__device__ __forceinline__ int a2c_start(int64_t kb, int64_t n, int64_t P, int Gl) {
+    const int64_t NB = (P + PW - 1) / PW;
+    int64_t W = 0, cw = 0;
+    for (int64_t b = 0; b < NB; b++) {
+        const int64_t w = a2c_work(b, n, P);
+        W += w;
+        if (b < kb) cw += w;
+    }
+    return (int)(kb + ((int64_t)(Gl - NB) * cw) / W);
+}
+__device__ __forceinline__ void a2c_assign(int64_t n, int64_t P, int Gl, int rl, int& kb, int& j, int& cnt) {
+    const int64_t NB = (P + PW - 1) / PW;
+    kb = 0;
+    while (kb + 1 < NB && a2c_start(kb + 1, n, P, Gl) <= rl) kb++;
+    const int s0 = a2c_start(kb, n, P, Gl);
+    const int s1 = (kb + 1 < NB) ? a2c_start(kb + 1, n, P, Gl) : Gl;
+    j = rl - s0;
+    cnt = s1 - s0;
+}
+// rows [i0, i1) of block kb of Y_P against coefficients x: a0, a1 (+=) for the consumer's columns
+// 2t', 2t'+1 of the block; x2 (+=) the coefficients' squares when want_x2
+__device__ void a2c_stream(const Smem& sm, const WRing& rg, const double* __restrict__ Y, int64_t m, int64_t P,
+                           int kb, int i0, int i1, const double* x, double& a0, double& a1, double& x2, bool want_x2,
+                           uint64_t pol) {
+    const int tid = threadIdx.x, tc = tid - 32;
+    const SrcYB src{Y, (int)m, (int)P, kb};
+    const int PST = wide_pst(src);
+    const int gc = kb * PW + 2 * tc;
+    int cb = 0;
+    wide_stream(
+        rg, src, i0, i1, false, pol,
+        [&](int c0, int c1) {
+            cb = c0;
+            for (int r = c0 + tid; r < c1; r += NT) {
+                const double c = ld(x + r);
+                sm.cf[r - c0] = c;
+                if (want_x2) x2 = fma(c, c, x2);
+            }
+            __syncthreads();
+        },
+        [&](int, int, int) {},
+        [&](int, int sa, int sb, const double* slot) {
+            if (2 * tc >= PST) return;
+            const bool full = (sa >= kb * PW + PW - 1) && (kb * PW + PW <= (int)P);
+            const double* sp = slot + 2 * tc;
+            const double* cp = sm.cf + (sa - cb);
+            if (full) {
+#pragma unroll 7
+                for (int q = 0; q < sb - sa; q++) {
+                    const double2 y = *reinterpret_cast<const double2*>(sp + q * PST);
+                    const double c = cp[q];
+                    a0 = fma(y.x, c, a0);
+                    a1 = fma(y.y, c, a1);
+                }
+            } else {
+                for (int q = 0; q < sb - sa; q++) {
+                    const int i = sa + q;
+                    const double2 y = *reinterpret_cast<const double2*>(sp + q * PST);
+                    const double c = cp[q];
+                    const double y0 = (gc <= i && gc < (int)P) ? y.x : 0.0;
+                    const double y1 = (gc + 1 <= i && gc + 1 < (int)P) ? y.y : 0.0;
+                    a0 = fma(y0, c, a0);
+                    a1 = fma(y1, c, a1);
+                }
+            }
+        },
+        [&](int) {}, [&](int, int) {});
+}
+
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1592,11 +1979,16 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         mbar_init(sm.vbar + 1, 1);
         sm.vuse[0] = sm.vuse[1] = 0;
         mbar_init(sm.mbar + 26, 1);
+        for (int k = 0; k < 2; k++) {
+            mbar_init(sm.mbar + kXFull + k, 1);
+            mbar_init(sm.mbar + kXEmpty + k, 1);
+        }
         *reinterpret_cast<uint32_t*>(sm.mbar + 25) = 0;
         fence_mbar_init();
     }
     __syncthreads();
     uint32_t mbph = 0;   // back-sweep ring phase bits (thread 0)
+    uint32_t xseq = 0;   // chunks of the two-thread back sweeps so far (threads 0 and 32 of CTA 0)
     uint32_t rph = 0;    // pass ring phase bits (every thread)
     // pass timers (whole launch, not windowed): the first consumer thread of the first
     // group's first CTA (+ prof_sel)
@@ -1729,6 +2121,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             bool done = false, flagged = false;
             bool use_la = la_have;           // first iteration: A already done in look-ahead
             bool use_a2 = false;             // pass A of this iteration fused behind the back sweep
+            bool use_a2c = false;            // ... in the column-owner form (partials per column block)
             bool la_done = false;            // look-ahead for vector p+1 issued
             la_have = false;
             // L2 policy of the streams: once Y_p no longer fits a share of L2, the passes that read
@@ -1752,8 +2145,16 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 int64_t c0, c1, x0, x1;
                 part_cols_tri(p, n, cg, Gt, c0, c1);
                 part_uniform(0, n, cg, Gt, x0, x1);
-                lab_gemm1<kLabMax>(sm, Y, m, n, c0, c1, Xb, n2v, nv, ws.labG, mc, scr, x0, x1, ws.labP + (int64_t)cg * kLabMax);
+                if (ws.labPB != nullptr) {
+                    lab_bl1_stream<kLabMax>(sm, wr, Y, m, n, p, Xb, n2v, nv, ws.labPB, cg, Gt, x0, x1,
+                                            ws.labP + (int64_t)cg * kLabMax, pol_once);
+                    gsync();
+                    lab_bl1_reduce<kLabMax>(ws.labPB, p, n, cg, Gt, nv, ws.labG, mc);
+                } else {
+                    lab_gemm1<kLabMax>(sm, Y, m, n, c0, c1, Xb, n2v, nv, ws.labG, mc, scr, x0, x1, ws.labP + (int64_t)cg * kLabMax);
+                }
                 gsync();
+                if (kWideDebug && (a.dbg & 16)) mark(12);   // debug: BL1 / BL2 in slots 12 / 13
                 if (r == 0 && tid < nv) {   // ||x_v||^2 for the degeneracy test (reading 16)
                     double t = 0.0;
                     for (int q = 0; q < Gt; q++) t += ld(ws.labP + (int64_t)q * kLabMax + tid);
@@ -1765,6 +2166,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                      [&](int64_t l) -> int64_t { return l + 1; },
                                      [&](int64_t l, int v, double t) { if (v < nv) st(ws.labGp + v * mc + l, t); });
                 gsync();
+                if (kWideDebug && (a.dbg & 16)) mark(13);
                 int64_t i0, i1;
                 part_uniform(p, n, cg, Gt, i0, i1);
                 lab_rowdots<kLabMax>(sm, i0, i1, p, ws.labGp, mc, nv, scr, [&](int64_t i) { return Y + y_row_off(i, m); },
@@ -1929,6 +2331,18 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         const double gl = reduce_slot(sm, S, Gt, SSlots::GPN);
                         if (r == 0 && tid == 0) st(ws.g + p - 1, gl);   // every rank, its own replica
                         if (dla) dtim[1] += dclk() - q1;
+                    } else if (use_a2c) {
+                        // column-owner A2: the partials of column k's block, in CTA order
+                        part_uniform(0, p, cg, Gt, k0, k1);
+                        const int Gl = G - 1;
+                        for (int64_t k = k0 + tid; k < k1; k += NT) {
+                            const int64_t kb = k / PW;
+                            const int s0 = a2c_start(kb, n, p, Gl);
+                            const int s1 = (kb + 1 < (p + PW - 1) / PW) ? a2c_start(kb + 1, n, p, Gl) : Gl;
+                            double t = 0.0;
+                            for (int q = s0; q < s1; q++) t += ld(P_ + (int64_t)(1 + q) * mc + k);
+                            st(ws.g + k, t);
+                        }
                     } else {
                         part_uniform(0, p, cg, Gt, k0, k1);
                         reduce_partials(sm, P_, mc, Gt, k0, k1, [&](int64_t k, double v) { mst(ws.g + k, v); }, rks);
@@ -2041,6 +2455,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                                           : reduce_slot(sm, S, Gt, use_la ? SSlots::X2N : SSlots::X2);
                 use_la = false;
                 use_a2 = false;
+                use_a2c = false;
                 use_lab = false;
                 double u0 = ld(ws.u + p);
                 const bool zero_u = (un == 0.0);   // reading: exactly-zero uhat -> e_1
@@ -2404,12 +2819,50 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         }
                         __syncthreads();
                         rph = *reinterpret_cast<volatile uint32_t*>(sm.red + NW + 7);
+                    } else if (r == 0 && a.sweep2) {
+                        if (tid == 0 || tid == 32)
+                            back_sweep_ws(a, ws, j, sm, mbph, xseq, tid == 32, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8);
                     } else if (r == 0 && tid == 0) {
                         back_sweep(a, ws, j, sm, mbph, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8,
                                    (kWideDebug && (a.dbg & 8) && dsub) ? dtim : nullptr);
                     }
                     mark(10);
-                    if (a2 && r > 0) {
+                    const bool a2c = a2 && !la && a.a2c && (p + PW - 1) / PW <= G - 1;
+                    if (a2c && r > 0) {
+                        // column-owner form: this CTA's block, its share of each band's rows
+                        const unsigned int tag = (sw_ep + 1) << 8;
+                        const int nbands = sweep_bands(n, a.band_ch);
+                        int kb, jb, cnt;
+                        a2c_assign(n, p, G - 1, r - 1, kb, jb, cnt);
+                        double a0 = 0.0, a1 = 0.0, x2 = 0.0;
+                        for (int b = 0; b < nbands; b++) {
+                            const int64_t C = (n + 255) / 256;
+                            const int64_t chi = C - (int64_t)b * a.band_ch, clo = chi - a.band_ch > 0 ? chi - a.band_ch : 0;
+                            const int64_t b0 = clo * 256, b1 = chi * 256 < n ? chi * 256 : n;
+                            const int64_t lo = b0 > (int64_t)kb * PW ? b0 : (int64_t)kb * PW;
+                            if (tid == 0) {
+                                uint32_t spins = 0;
+                                while (acquire(sw_prog) < tag + (unsigned int)b + 1u) {
+                                    if (a.poll_ns) __nanosleep(a.poll_ns);
+                                    if (++spins > (1u << 30)) __trap();
+                                }
+                            }
+                            __syncthreads();
+                            if (b1 <= lo) continue;
+                            int64_t i0, i1;
+                            part_uniform(lo, b1, jb, cnt, i0, i1);
+                            if (i1 > i0) a2c_stream(sm, wr, Y, m, p, kb, (int)i0, (int)i1, ws.x, a0, a1, x2, kb == 0, pol_once);
+                        }
+                        {
+                            const int tc = tid - 32, c = kb * PW + 2 * tc;
+                            if (tc >= 0 && 2 * tc < PW) {
+                                if (c < p) st(P_ + (int64_t)cg * mc + c, a0);
+                                if (c + 1 < p) st(P_ + (int64_t)cg * mc + c + 1, a1);
+                            }
+                        }
+                        x2 = block_sum<NT>(x2, sm.red);
+                        if (tid == 0) st(S + cg * SST + SSlots::X2, x2);
+                    } else if (a2 && r > 0) {
                         // bands bottom-up; this CTA's rows of each band by the pass weights
                         const unsigned int tag = (sw_ep + 1) << 8;
                         const int nbands = sweep_bands(n, a.band_ch);
@@ -2463,7 +2916,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         if (tid == 0) mst(S + cg * SST + SSlots::X2N, x2n);
                     }
                     if (la) la_done = true;
-                    if (a2) { sw_ep++; use_a2 = true; }
+                    if (a2) { sw_ep++; use_a2 = true; use_a2c = a2c; }
                     gsync();
                     PH(11);
                     xcur = ws.x;
@@ -2475,10 +2928,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
     }
     if (r == 0 && tid == 0) a.syncs[g] = nsync;
     if (timing)
-        for (int k = 0; k < 12; k++) a.prof[g * 16 + k] = tacc[k];
+        for (int k = 0; k < ((kWideDebug && (a.dbg & 16)) ? 14 : 12); k++) a.prof[g * 16 + k] = tacc[k];
     if (timing0 && !kWideDebug)
         for (int k = 0; k < 4; k++) a.prof[12 + k] = ntim[k];
-    if (dsub)
+    if (dsub && !(a.dbg & 16))
         for (int k = 0; k < 4; k++) a.prof[12 + k] = dtim[k];
 #undef PH
 }

@@ -822,6 +822,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     }
     // blocked look-ahead: block size (TINV_LAB, 0/1 = off), compact-WY modes
     const int lab = (h->mgs == 1) ? 0 : std::min(kLabMax, std::max(0, getenv("TINV_LAB") ? atoi(getenv("TINV_LAB")) : h->lab));
+    const bool bl1_stream = getenv("TINV_BL1") ? atoi(getenv("TINV_BL1")) != 0 : true;   // streamed BL1 (else column split)
     // MGS pays one group barrier per accepted vector: its groups are kept small (TINV_MGS_G CTAs)
     const int gmax = (h->mgs == 1) ? std::max(1, getenv("TINV_MGS_G") ? atoi(getenv("TINV_MGS_G")) : 16) : (1 << 30);
     Schedule sc;
@@ -1078,13 +1079,14 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.P = c.take<double>((size_t)G * W.mcap);
                 W.P2 = c.take<double>((size_t)G * W.mcap);
                 W.S = c.take<double>((size_t)G * 16 + 16);
-                W.labG = W.labGp = W.labU = W.labX2 = W.labP = nullptr;
+                W.labG = W.labGp = W.labU = W.labX2 = W.labP = W.labPB = nullptr;
                 if (lab > 1 && mc > cwy_narrow_max() && rg == 1) {
                     W.labG = c.take<double>((size_t)kLabMax * W.mcap);
                     W.labGp = c.take<double>((size_t)kLabMax * W.mcap);
                     W.labU = c.take<double>((size_t)kLabMax * ((n + 1) & ~int64_t(1)) + 2);
                     W.labX2 = c.take<double>(kLabMax);
                     W.labP = c.take<double>((size_t)G * kLabMax);
+                    if (bl1_stream) W.labPB = c.take<double>((size_t)((mc + kWidePieceW - 1) / kWidePieceW + G) * kLabMax * kWidePieceW);
                 }
                 W.bar = nullptr;
                 W.nrk = 1;
@@ -1195,6 +1197,8 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
         ca.a2 = getenv("TINV_A2") ? atoi(getenv("TINV_A2")) : 1;
         ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 8;
+        ca.sweep2 = getenv("TINV_SWEEP2") ? atoi(getenv("TINV_SWEEP2")) : 1;
+        ca.a2c = getenv("TINV_A2C") ? atoi(getenv("TINV_A2C")) : 1;
         ca.poll_ns = getenv("TINV_POLLNS") ? atoi(getenv("TINV_POLLNS")) : 0;
         ca.dbg = getenv("TINV_DBG") ? atoi(getenv("TINV_DBG")) : 0;
         ca.reorth = h->mgs;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 namespace tinv {
+constexpr int kWidePieceW = 448;   // column block / row piece width of the wide passes (cwy.cu PW)
 
 struct GroupBarrier;
 
@@ -121,6 +122,7 @@ struct GroupWS {
     double* labU;
     double* labX2;
     double* labP;
+    double* labPB;      // streamed BL1: per (column block, CTA) partial sums [(NB + Gt)][8][448], or NULL
     GroupBarrier* bar;
     int64_t mcap;
     // Row split of one cluster over `nrk` ranks: every rank holds a full
@@ -172,6 +174,8 @@ struct CwyArgs {
     int prof_sel;            // debug: CTA whose thread 32 runs the pass timers (default: the first group's first)
     int a2;                  // fuse iteration 2's pass A behind the back sweep (TINV_A2, default 1)
     int band_ch;             // sweep chunks (256 rows) per published band (TINV_BANDCH)
+    int a2c;                 // fused pass A2 in the column-owner form (TINV_A2C, default 1)
+    int sweep2;              // window back sweep on two threads of CTA 0: chain + TMA/store helper (TINV_SWEEP2, default 1)
     int poll_ns;             // back-off of the band polls in ns (TINV_POLLNS)
     int dbg;                 // debug build experiments (TINV_DBG bits)
     int reorth;              // 0 reduced compact WY (§3.3.2), 1 classical MGS (Alg. 1), 2 ordinary compact WY (§3.3.1)
