@@ -155,7 +155,7 @@ __device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int
 
 // dynamic shared memory carve-up
 struct Smem {
-    double* vs;      // staged vector of the short passes (kVsD doubles)
+    double* vs;      // staged vector of the short passes (kVsD doubles; the A2C block table)
     double* cf;      // CFCH coefficients
     double* racc;    // 2 RCH row accumulators of wide row dots
     double* vblk;    // 2 x 2 PW: column blocks of the wide row-dot vectors (double buffer)
@@ -1873,25 +1873,22 @@ __device__ void lab_rowdots(const Smem& sm, int64_t r0, int64_t r1, int64_t P, c
 __device__ __forceinline__ int64_t a2c_work(int64_t kb, int64_t n, int64_t P) {
     return (n - kb * PW) * (int64_t)min((int64_t)PW, P - kb * PW);
 }
-// first streaming CTA (0-based among the Gl) of block kb
-__device__ __forceinline__ int a2c_start(int64_t kb, int64_t n, int64_t P, int Gl) {
+// first streaming CTA (0-based among the Gl) of every block: st[kb], kb = 0..NB (st[NB] = Gl),
+// written by thread 0 into shared memory (the caller synchronises)
+__device__ __forceinline__ void a2c_table(int64_t n, int64_t P, int Gl, int* st) {
     const int64_t NB = (P + PW - 1) / PW;
-    int64_t W = 0, cw = 0;
-    for (int64_t b = 0; b < NB; b++) {
-        const int64_t w = a2c_work(b, n, P);
-        W += w;
-        if (b < kb) cw += w;
-    }
-    return (int)(kb + ((int64_t)(Gl - NB) * cw) / W);
+    // elements of blocks [0, b) for b <= NB - 1 (full-width blocks): PW (b n - PW b (b-1) / 2)
+    auto cw = [&](int64_t b) -> int64_t { return (int64_t)PW * (b * n - (int64_t)PW * (b * (b - 1) / 2)); };
+    const int64_t W = cw(NB - 1) + a2c_work(NB - 1, n, P);
+    for (int64_t b = threadIdx.x; b <= NB; b += NT)
+        st[b] = (b == NB) ? Gl : (int)(b + ((int64_t)(Gl - NB) * cw(b)) / W);
 }
-__device__ __forceinline__ void a2c_assign(int64_t n, int64_t P, int Gl, int rl, int& kb, int& j, int& cnt) {
+__device__ __forceinline__ void a2c_assign(int64_t P, const int* st, int rl, int& kb, int& j, int& cnt) {
     const int64_t NB = (P + PW - 1) / PW;
     kb = 0;
-    while (kb + 1 < NB && a2c_start(kb + 1, n, P, Gl) <= rl) kb++;
-    const int s0 = a2c_start(kb, n, P, Gl);
-    const int s1 = (kb + 1 < NB) ? a2c_start(kb + 1, n, P, Gl) : Gl;
-    j = rl - s0;
-    cnt = s1 - s0;
+    while (kb + 1 < NB && st[kb + 1] <= rl) kb++;
+    j = rl - st[kb];
+    cnt = st[kb + 1] - st[kb];
 }
 // rows [i0, i1) of block kb of Y_P against coefficients x: a0, a1 (+=) for the consumer's columns
 // 2t', 2t'+1 of the block; x2 (+=) the coefficients' squares when want_x2
@@ -2109,6 +2106,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         constexpr int64_t kLab0 = kNarrowM + 1;
         auto in_lab = [&](int64_t q) { return lab_cl && q >= kLab0; };
         int64_t lab_k = 0;   // start of the current block
+        bool lab_fused = false;   // in-block dots of this block come from the earlier vectors' BC passes
         unsigned int* sw_prog = reinterpret_cast<unsigned int*>(S + (int64_t)Gt * SST);   // sweep bands
         unsigned int sw_ep = 0;   // fused sweeps so far in this cluster (the progress tag's epoch)
         if (r == 0 && tid == 0) publish(sw_prog, 0u);   // visible after the next group barrier
@@ -2122,6 +2120,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             bool use_la = la_have;           // first iteration: A already done in look-ahead
             bool use_a2 = false;             // pass A of this iteration fused behind the back sweep
             bool use_a2c = false;            // ... in the column-owner form (partials per column block)
+            bool tyr_have = false;           // T_p yrow of this vector in ws.tyr (this CTA's TN rows)
             bool la_done = false;            // look-ahead for vector p+1 issued
             la_have = false;
             // L2 policy of the streams: once Y_p no longer fits a share of L2, the passes that read
@@ -2139,6 +2138,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             if (use_lab && (p - kLab0) % a.lab == 0) {
                 // ---------------- BL1-BL3: U = X - Y_k T_k^T Y_k^T X for x^(1)_k .. x^(1)_{k+nv-1}
                 lab_k = p;
+                lab_fused = a.labq != 0;
                 const int nv = (int)((m - p < a.lab) ? m - p : a.lab);
                 const double* Xb = a.X1c + j * n2v;
                 double* scr = ring_base;   // no pass ring in flight between phases
@@ -2233,7 +2233,27 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     const double* Uv = ws.labU + v * n2v;
                     double* gr = sm.vs;          // g_r   (<= kLabMax)
                     double* grp = sm.vs + 16;    // g'_r
-                    if (v > 0) {
+                    if (v > 0 && lab_fused) {
+                        // g_r[q] = y0_{k+q} U_v[k+q] + sum_{i > k+q} uhat_{k+q}[i] U_v[i]: the sums were
+                        // accumulated per CTA by the BC pass of vector k+q (labQ[cta][v][q]); no pass here
+                        const int q = tid >> 5, lane = tid & 31;
+                        if (q < v) {
+                            double t = 0.0;
+                            for (int u = lane; u < Gt; u += 32) t += ld(ws.labQ + ((int64_t)u * kLabMax + v) * kLabMax + q);
+                            t = warp_sum(t);
+                            if (lane == 0) gr[q] = fma(ld(ws.labY0 + q), ld(Uv + lab_k + q), t);
+                        }
+                        __syncthreads();
+                        if (tid < v) {
+                            const int64_t l = lab_k + tid;
+                            const double* tc = Tc + tcol_off(l) + lab_k;
+                            double t = 0.0;
+                            for (int q2 = 0; q2 <= tid; q2++) t = fma(ld(tc + q2), gr[q2], t);
+                            grp[tid] = t;
+                        }
+                        __syncthreads();
+                        PH(1);
+                    } else if (v > 0) {
                         int64_t i0, i1;
                         part_uniform(lab_k, n, cg, Gt, i0, i1);
                         double av[kLabMax];
@@ -2334,13 +2354,21 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                     } else if (use_a2c) {
                         // column-owner A2: the partials of column k's block, in CTA order
                         part_uniform(0, p, cg, Gt, k0, k1);
-                        const int Gl = G - 1;
+                        int* st_tab = reinterpret_cast<int*>(sm.vs);
+                        a2c_table(n, p, G - 1, st_tab);
+                        __syncthreads();
                         for (int64_t k = k0 + tid; k < k1; k += NT) {
                             const int64_t kb = k / PW;
-                            const int s0 = a2c_start(kb, n, p, Gl);
-                            const int s1 = (kb + 1 < (p + PW - 1) / PW) ? a2c_start(kb + 1, n, p, Gl) : Gl;
+                            const int s0 = st_tab[kb], s1 = st_tab[kb + 1];
                             double t = 0.0;
-                            for (int q = s0; q < s1; q++) t += ld(P_ + (int64_t)(1 + q) * mc + k);
+                            for (int q0 = s0; q0 < s1; q0 += 8) {   // 8 independent loads per round trip
+                                double v[8];
+#pragma unroll
+                                for (int u = 0; u < 8; u++) v[u] = (q0 + u < s1) ? ld(P_ + (int64_t)(1 + q0 + u) * mc + k) : 0.0;
+#pragma unroll
+                                for (int u = 0; u < 8; u++)
+                                    if (q0 + u < s1) t += v[u];
+                            }
                             st(ws.g + k, t);
                         }
                     } else {
@@ -2418,12 +2446,41 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         u2 = block_sum<NT>(u2, sm.red);
                         if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
                     } else if (p > kNarrowM) {
+                        // vector p of a look-ahead block: dots of uhat (column p of Y below row p) with
+                        // the block's later first iterates U_v, v > p - k (their in-block g_r)
+                        const int jq = (int)(p - lab_k);
+                        const int nvb = (int)((m - lab_k < a.lab) ? m - lab_k : a.lab);
+                        const bool fq = in_lab(p) && lab_fused && jq + 1 < nvb;
+                        double lq[kLabMax];
+#pragma unroll
+                        for (int q = 0; q < kLabMax; q++) lq[q] = 0.0;
                         wide_rowdots<false>(sm, wr, SrcY{Y, (int)m, (int)p}, (int)i0, (int)i1, ws.gp, nullptr, p, pol_keep,
                                             [&](int64_t i, double v, double) {
                                                 const double ui = ld(xcur + i) - v;
                                                 mst(ws.u + i, ui);
                                                 u2 = fma(ui, ui, u2);
+                                                if (fq && i > p) {
+#pragma unroll
+                                                    for (int q = 0; q < kLabMax; q++)
+                                                        if (q > jq && q < nvb) lq[q] = fma(ui, ld(ws.labU + q * n2v + i), lq[q]);
+                                                }
                                             });
+                        if (fq) {   // CTA sums (fixed order: warp tree, then warps in order)
+#pragma unroll
+                            for (int q = 0; q < kLabMax; q++) lq[q] = warp_sum(lq[q]);
+                            __syncthreads();
+                            double* wq = reinterpret_cast<double*>(sm.acc);   // [warp][q]
+                            if ((tid & 31) == 0)
+#pragma unroll
+                                for (int q = 0; q < kLabMax; q++) wq[(tid >> 5) * kLabMax + q] = lq[q];
+                            __syncthreads();
+                            if (tid > jq && tid < nvb) {
+                                double t = 0.0;
+                                for (int w = 0; w < NW; w++) t += wq[w * kLabMax + tid];
+                                st(ws.labQ + ((int64_t)cg * kLabMax + tid) * kLabMax + jq, t);
+                            }
+                            __syncthreads();
+                        }
                         u2 = block_sum<NT>(u2, sm.red);
                         if (tid == 0) mst(S + cg * SST + SSlots::U2, u2);
                         // second read of Yhat, blocks in reverse order (the last ones are in L2);
@@ -2477,6 +2534,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 c = -((u0 >= 0.0) ? 1.0 : -1.0) * un;
                 const double tt = 1.0 / (c * c - u0 * c);
                 const double y0 = u0 - c;
+                if (in_lab(p)) {   // y_0 of this block vector (the last iteration's stays), fused dots void on zero uhat
+                    if (r == 0 && tid == 0) st(ws.labY0 + (p - lab_k), y0);
+                    if (zero_u) lab_fused = false;
+                }
                 const double* yrow = Y + y_row_off(p, m);
                 const uint64_t q2m = dclk();
                 if (dsub && !(a.dbg & 11)) dtim[2] += q2m - q2s;
@@ -2511,14 +2572,26 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 {
                     int64_t l0, l1;
                     l0 = ptn0; l1 = ptn1;
-                    if (p > kNarrowM) {
+                    if (p > kNarrowM && tyr_have && a.tyr) {
+                        // T_p yrow is the same in every iteration of vector p (T_p and row p of Y are
+                        // final): kept from the first TN, so later TNs stream T against s alone
+                        wide_rowdots<false>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, nullptr, p, pol_once,
+                                            [&](int64_t l, double a1, double) {
+                                                const double that = -tt * a1;
+                                                mst(ws.xp + l, ld(ws.tyr + l) + y0 * that);
+                                                mst(Tc + tcol_off(p) + l, that);
+                                                mst(Tr + l * m2 + p, that);
+                                            });
+                    } else if (p > kNarrowM) {
                         wide_rowdots<true>(sm, wr, SrcTr{Tr, (int)m2, (int)p}, (int)l0, (int)l1, ws.s, yrow, p, pol_once,
                                            [&](int64_t l, double a1, double a2) {
                                                const double that = -tt * a1;
+                                               st(ws.tyr + l, a2);   // this CTA's rows of T_p yrow (same rows every iteration)
                                                mst(ws.xp + l, a2 + y0 * that);
                                                mst(Tc + tcol_off(p) + l, that);
                                                mst(Tr + l * m2 + p, that);
                                            });
+                        tyr_have = true;
                     } else if (l1 > l0) {
                         stage_vec(sm, ws.s, p);
                         const int lane = tid & 31, warp = tid >> 5;
@@ -2833,7 +2906,11 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         const unsigned int tag = (sw_ep + 1) << 8;
                         const int nbands = sweep_bands(n, a.band_ch);
                         int kb, jb, cnt;
-                        a2c_assign(n, p, G - 1, r - 1, kb, jb, cnt);
+                        int* st_tab = reinterpret_cast<int*>(sm.vs);
+                        a2c_table(n, p, G - 1, st_tab);
+                        __syncthreads();
+                        a2c_assign(p, st_tab, r - 1, kb, jb, cnt);
+                        __syncthreads();
                         double a0 = 0.0, a1 = 0.0, x2 = 0.0;
                         for (int b = 0; b < nbands; b++) {
                             const int64_t C = (n + 255) / 256;

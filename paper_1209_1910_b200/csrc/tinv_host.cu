@@ -1078,14 +1078,17 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
                 W.xp = c.take<double>(W.mcap);
                 W.P = c.take<double>((size_t)G * W.mcap);
                 W.P2 = c.take<double>((size_t)G * W.mcap);
+                W.tyr = c.take<double>(W.mcap);
                 W.S = c.take<double>((size_t)G * 16 + 16);
-                W.labG = W.labGp = W.labU = W.labX2 = W.labP = W.labPB = nullptr;
+                W.labG = W.labGp = W.labU = W.labX2 = W.labP = W.labPB = W.labQ = W.labY0 = nullptr;
                 if (lab > 1 && mc > cwy_narrow_max() && rg == 1) {
                     W.labG = c.take<double>((size_t)kLabMax * W.mcap);
                     W.labGp = c.take<double>((size_t)kLabMax * W.mcap);
                     W.labU = c.take<double>((size_t)kLabMax * ((n + 1) & ~int64_t(1)) + 2);
                     W.labX2 = c.take<double>(kLabMax);
                     W.labP = c.take<double>((size_t)G * kLabMax);
+                    W.labQ = c.take<double>((size_t)G * kLabMax * kLabMax);
+                    W.labY0 = c.take<double>(kLabMax);
                     if (bl1_stream) W.labPB = c.take<double>((size_t)((mc + kWidePieceW - 1) / kWidePieceW + G) * kLabMax * kWidePieceW);
                 }
                 W.bar = nullptr;
@@ -1197,8 +1200,10 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
         ca.a2 = getenv("TINV_A2") ? atoi(getenv("TINV_A2")) : 1;
         ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 8;
-        ca.sweep2 = getenv("TINV_SWEEP2") ? atoi(getenv("TINV_SWEEP2")) : 1;
+        ca.sweep2 = getenv("TINV_SWEEP2") ? atoi(getenv("TINV_SWEEP2")) : 2;
         ca.a2c = getenv("TINV_A2C") ? atoi(getenv("TINV_A2C")) : 1;
+        ca.tyr = getenv("TINV_TYR") ? atoi(getenv("TINV_TYR")) : 1;
+        ca.labq = getenv("TINV_LABQ") ? atoi(getenv("TINV_LABQ")) : 1;
         ca.poll_ns = getenv("TINV_POLLNS") ? atoi(getenv("TINV_POLLNS")) : 0;
         ca.dbg = getenv("TINV_DBG") ? atoi(getenv("TINV_DBG")) : 0;
         ca.reorth = h->mgs;

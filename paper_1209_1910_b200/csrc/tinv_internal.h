@@ -112,6 +112,7 @@ struct GroupWS {
     double* P;          // partial sums [Gt][mcap] (a rank writes only its own CTAs' slots)
     double* S;          // scalar partials [Gt][16] (Gt = CTAs of the group over all ranks)
     double* P2;         // look-ahead partial sums [Gt][mcap]
+    double* tyr;        // T_p yrow of the current vector (mcap), kept across its iterations
     double* ysol;       // forward-sweep workspace of the chained solve (n)
     // blocked look-ahead (CwyArgs::lab > 1, wide clusters): for the block of
     // b upcoming first iterates X = [x^(1)_k .. x^(1)_{k+b-1}]:  G = Y_k^T X,  G' = T_k^T G
@@ -122,6 +123,8 @@ struct GroupWS {
     double* labU;
     double* labX2;
     double* labP;
+    double* labQ;       // fused in-block dots [Gt][v][q] (per CTA, from the BC pass of block vector k+q)
+    double* labY0;      // y_0 of the block's vectors [8]
     double* labPB;      // streamed BL1: per (column block, CTA) partial sums [(NB + Gt)][8][448], or NULL
     GroupBarrier* bar;
     int64_t mcap;
@@ -174,6 +177,8 @@ struct CwyArgs {
     int prof_sel;            // debug: CTA whose thread 32 runs the pass timers (default: the first group's first)
     int a2;                  // fuse iteration 2's pass A behind the back sweep (TINV_A2, default 1)
     int band_ch;             // sweep chunks (256 rows) per published band (TINV_BANDCH)
+    int labq;                // in-block look-ahead dots fused into the earlier vectors' BC passes (TINV_LABQ, default 1)
+    int tyr;                 // keep T_p yrow across the iterations of vector p (TINV_TYR, default 1)
     int a2c;                 // fused pass A2 in the column-owner form (TINV_A2C, default 1)
     int sweep2;              // window back sweep on two threads of CTA 0: chain + TMA/store helper (TINV_SWEEP2, default 1)
     int poll_ns;             // back-off of the band polls in ns (TINV_POLLNS)

@@ -13,6 +13,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtinv.so")
+if os.environ.get("TINV_LIB_VARIANT"):   # performance A/B of two in-tree builds (libtinv_<variant>.so)
+    LIB_PATH = os.path.join(_HERE, "libtinv_" + os.environ["TINV_LIB_VARIANT"] + ".so")
 
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",

@@ -4,6 +4,8 @@
 //  C  the library form: 16-row batches loaded from shared memory, then the chain
 //  D  as C with 32-row batches
 //  E  as C, the next batch's loads issued between the chain's FMAs (manual 2-batch unroll)
+//  F  as C with t scaled by 1e-310 (every x subnormal)
+//  G  as C with t scaled by 1e-300 and |b|, |c| ~ 1e-3 (x decays through the subnormal range)
 #include <cstdio>
 #include <vector>
 #include <random>
@@ -99,6 +101,20 @@ __global__ void probe(const double* bcg, const double* tg, int n, long long* cyc
         cyc[4] = clock64() - t0;
         acc += x1;
     }
+    {   // F, G: subnormal operands
+        for (int i = 0; i < n; i++) tf[i] = tg[i] * 1e-310;
+        double x1 = 0.0, x2 = 0.0;
+        long long t0 = clock64();
+        for (int u0 = (n & ~15) - 16; u0 >= 0; u0 -= 16) batch16(BC, tf, xo, u0, x1, x2);
+        cyc[5] = clock64() - t0;
+        acc += x1;
+        for (int i = 0; i < n; i++) { tf[i] = (i == n - 1) ? 1e-300 : 0.0; BC[i] = make_double2(BC[i].x * 2e-3, BC[i].y * 2e-3); }
+        x1 = 0.0; x2 = 0.0;
+        t0 = clock64();
+        for (int u0 = (n & ~15) - 16; u0 >= 0; u0 -= 16) batch16(BC, tf, xo, u0, x1, x2);
+        cyc[6] = clock64() - t0;
+        acc += x1;
+    }
     *sink = acc;
 }
 int main() {
@@ -116,6 +132,7 @@ int main() {
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int rep = 0; rep < 2; rep++) probe<<<1, 256, smem>>>(dbc, dt, n, dc, sink);
     long long h[8]; cudaMemcpy(h, dc, 64, cudaMemcpyDeviceToHost);
-    const char* nm[5] = {"A 1 DFMA/row, regs", "B recurrence, regs", "C 16-batch smem", "D 32-batch smem", "E 2-set interleaved"};
-    for (int v = 0; v < 5; v++) printf("%-22s %.2f cycles/row (%s)\n", nm[v], (double)h[v] / n, cudaGetErrorString(cudaGetLastError()));
+    const char* nm[7] = {"A 1 DFMA/row, regs", "B recurrence, regs", "C 16-batch smem", "D 32-batch smem", "E 2-set interleaved",
+                         "F C, subnormal x", "G C, x decaying"};
+    for (int v = 0; v < 7; v++) printf("%-22s %.2f cycles/row (%s)\n", nm[v], (double)h[v] / n, cudaGetErrorString(cudaGetLastError()));
 }
