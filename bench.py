@@ -46,6 +46,7 @@ WORKLOAD_DESC = {
 
 
 BIG = ("cfg4", "cfg5")          # one giant cluster: row split at N > 1, seconds per step
+FP64_DFMA_TFLOPS = 36.5     # measured fp64 DFMA rate of this B200 (tools/micro/fp64_peak.cu)
 
 
 def config_dict(args, n, ws):
@@ -326,8 +327,10 @@ def main():
     for k in range(min(1 if args.config in BIG else 3, args.steps)):
         flush.fill_(float(k))
         h.eigvecs(dd, de, dw, Z=Zt, seed=args.seed)
-        for kk, v in h.stats()["kernel_ms"].items():
+        stp = h.stats()
+        for kk, v in stp["kernel_ms"].items():
             kms.setdefault(kk, []).append(v)
+        kms.setdefault("dz", []).append(stp["dz_ms"])
     h.set_profiling(False)
     barrier()
     tot_ms = float(sum(step_ms))
@@ -367,6 +370,21 @@ def main():
         # measured DRAM bytes of the same kernel (committed ncu capture) over the same kernel time
         roof["traffic_gbs"] = traffic / (avg[dom] * 1e-3) / 1e9
         roof["traffic_frac"] = roof["traffic_gbs"] / peaks["hbm_gbs"]
+    if dom == "cwy" and not resident and st.get("dz_parked", 0) > 0:
+        # the deferred final pass D: its GEMM runs after the persistent kernel
+        # inside the same cWY interval, so the cWY bytes are over both; the GEMM itself is an fp64
+        # DFMA contraction reported against the measured DFMA peak
+        roof["kernel"] = "cwy_kernel + dz_gemm_kernel/dz_finish_kernel (deferred final pass D)"
+        dzms = avg.get("dz", 0.0)
+        roof["dz"] = {"kernel": "dz_gemm_kernel + dz_finish_kernel", "parked": st["dz_parked"], "ms": dzms,
+                      "share_of_step": dzms / ms_per_step if ms_per_step > 0 else None}
+        if st["nclusters"] == 1 and st["dz_parked"] == n - 64 and dzms > 0:
+            p = np.arange(64, n, dtype=np.float64)
+            flops = float(np.sum(2.0 * ((p + 1) * (p + 2) / 2 + (n - p - 1) * (p + 1))))
+            roof["dz"].update({"bound": "alu", "flops": flops, "achieved": flops / (dzms * 1e-3) / 1e12,
+                               "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
+                               "frac": flops / (dzms * 1e-3) / 1e12 / FP64_DFMA_TFLOPS,
+                               "peak_source": "measured DFMA rate, tools/micro/fp64_peak.cu (DESIGN.md section 8)"})
     if resident:
         roof["note"] = ("resident cWY kernel: Y stays in shared memory, so DRAM traffic is far below the "
                         "algorithmic bytes; the step is bound by the dependent chains and phase latencies "
@@ -391,7 +409,8 @@ def main():
         "info": {"return_codes": sorted(set(rcs)), "nclusters": st["nclusters"], "max_cluster": st["max_cluster"],
                  "n_clustered": st["n_clustered"], "iters_hist": st["iters_hist"], "kernel_ms": avg,
                  "cwy_phase_ms": st["cwy_phase_ms"], "group_syncs": st["group_syncs"], "ngroups": st["ngroups"],
-                 "cwy_ctas": st["cwy_ctas"], "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
+                 "cwy_ctas": st["cwy_ctas"], "dz_parked": st["dz_parked"], "dz_redo": st["dz_redo"],
+                 "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(d, e, w, mgs=args.reorth == "mgs")

@@ -159,9 +159,22 @@ typedef struct {
                                    sweep, x copy); with no persistent launch slots 0..3 hold
                                    the batched LU's warp-0 sweeps (factor, back, forward,
                                    back) */
+    int64_t dz_parked;          /* vectors whose last pass D was deferred to dz_gemm */
+    int64_t dz_redo;            /* > 0: parked vectors failed their deferred test and the call
+                                   was re-run without deferral; -1: re-run forced (TINV_DZ=2) */
+    double  dz_ms;              /* deferred pass D kernels (dz_gemm + dz_finish, inside the cwy
+                                   time of kernel_ms), profiling only                 */
 } tinv_stats_t;
 
 int tinv_set_profiling(tinv_t h, int enable);
+
+/* Deferred final pass D (default on, single-rank calls): in the last iteration of a
+ * wide cluster's vector the step's pass D (q = Y_{p+1} x' - e_p) is not
+ * streamed per vector; x' is kept and one GEMM after the cWY kernel forms every such q, the
+ * stopping test (Alg. 4) and z_j.  A vector whose deferred test fails makes
+ * the call re-run without deferral, so results follow Alg. 4 either way.  enable = 0 turns it
+ * off.  Returns 0 or TINV_ERR_HANDLE. */
+int tinv_set_deferred(tinv_t h, int enable);
 
 /* Testing aid for the multi-GPU row split on a single device: when the
  * clustered work of a tinv_eigvecs call is one cluster of more than 64 vectors, split it over

@@ -2071,6 +2071,10 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
         const int64_t m2 = (m + 1) & ~int64_t(1);
         const bool narrow = (m <= kNarrowM) && a.nstg > 0;
         const bool la_ok = ((G > 1) || narrow) && mode != 1;   // look-ahead can overlap the back sweep
+        // deferred final pass D: wide clusters that are their group's last (Y stays intact after
+        // the kernel), single-rank groups
+        const bool dz_cl = a.dzc != nullptr && mode != 1 && NR == 1 && !narrow && m > kNarrowM + 1 &&
+                           ci == a.g_coff[g + 1] - 1;
         double* __restrict__ Tc = ws.Tc;
         double* __restrict__ Tr = ws.Tr;
 
@@ -2645,6 +2649,30 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                 gsync();
                 PH(6);
                 }   // reduced / ordinary compact-WY step
+                // ---------------- deferred D (DESIGN §6 "deferred final pass D"): when a pass in
+                // this iteration completes the stopping rule and nothing later reads this q (no
+                // look-ahead dot for vector p+1, the cluster is its group's last), D and TEST are
+                // skipped: x' is parked in the vector's dead x^(1) slot and c in dzc[j]; after the
+                // kernel, dz_gemm forms q = Y_{p+1} x' - e_p for all parked vectors at once (one
+                // GEMM instead of one read of Y_{p+1} per vector), runs the test and writes z_j.
+                // A parked vector whose deferred test fails makes the host re-run the call
+                // without deferral, so the result never depends on the guess.
+                if (dz_cl && mode != 1 && p + 1 > kNarrowM && passes + 1 >= kPasses && kin < kMaxIts &&
+                    !((p + 1 < m) && la_ok && !in_lab(p + 1))) {
+                    int64_t k0, k1;
+                    part_uniform(0, p + 1, r, G, k0, k1);
+                    double* xd = a.dzx + j * n2v;
+                    for (int64_t k = k0 + tid; k < k1; k += NT) st(xd + k, ld(ws.xp + k));
+                    if (r == 0 && tid == 0) {
+                        a.iters[j] = its;
+                        if (flagged) atomicAdd(&a.out->nflag, 1);
+                        a.dzc[j] = c;
+                    }
+                    done = true;
+                    la_have = la_done;
+                    PH(8);
+                    continue;
+                }
                 // ---------------- D: q = Y_{p+1} x' - e_p, norms and argmax
                 Aff1 fex{1.0, 0.0};   // forward-sweep state kept from D to the solve
                 int64_t fs0 = 0, fta = 0, ftb = 0;

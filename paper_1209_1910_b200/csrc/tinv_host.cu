@@ -77,6 +77,7 @@ struct tinv_s {
     double *ds = nullptr, *es = nullptr;   // d, e as the kernels read them (prep: copies, reading 21)
     double *wt = nullptr, *X = nullptr, *fl = nullptr, *fr = nullptr, *fb = nullptr, *fc = nullptr;
     double *unn = nullptr, *zscale = nullptr, *F = nullptr, *X1c = nullptr;
+    double *dzc = nullptr, *dzp = nullptr;   // deferred pass D: c per vector, row-tile partials
     int8_t *fp = nullptr, *FP = nullptr;
     int *cstart = nullptr, *cid = nullptr, *jc = nullptr, *iters = nullptr, *slot = nullptr, *perm = nullptr;
     PrepOut* out = nullptr;
@@ -98,6 +99,7 @@ struct tinv_s {
                                       // (Alg. 1), 2 ordinary cWY (§3.3.1)
     int res_cs2 = 1000, res_cs4 = 1000, res_cs8 = 1000;   // m from which a cluster gets >= 2 / 4 / 8 CTAs
     int handover = 1;                 // narrow leaders finish in the resident kernel (n <= 2048)
+    int dz = 1;                       // deferred final pass D (tinv_set_deferred; single-rank only)
     double leader_w = 1.0;            // LPT weight of a handed-over leader (vector equivalents)
     double lpt_m = 1.0;               // LPT weight per vector: 1 + lpt_m m / 32
     // row split over real ranks: peers' cWY workspaces mapped through CUDA IPC
@@ -189,6 +191,8 @@ int ensure_base(tinv_s* h, int64_t n) {
         h->F = c.take<double>((size_t)n * (size_t)n * 4);
         h->FP = c.take<int8_t>((size_t)n * (size_t)n);
         h->X1c = c.take<double>((size_t)n * (size_t)((n + 1) & ~int64_t(1)) + 1024);
+        h->dzc = c.take<double>(n);
+        h->dzp = c.take<double>((size_t)((n + 127) / 128) * 3 * (size_t)n + 64);
         return c.off;
     };
     size_t bytes = layout(nullptr);
@@ -593,6 +597,12 @@ int tinv_set_reorth(tinv_t h, int mode) {
     return 0;
 }
 
+int tinv_set_deferred(tinv_t h, int enable) {
+    if (!h) return TINV_ERR_HANDLE;
+    h->dz = enable ? 1 : 0;
+    return 0;
+}
+
 int tinv_set_profiling(tinv_t h, int enable) {
     if (!h) return TINV_ERR_HANDLE;
     h->profiling = enable != 0;
@@ -627,8 +637,8 @@ int tinv_get_stats(tinv_t h, tinv_stats_t* out) {
     return 0;
 }
 
-int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
-                 double* Z, int64_t ldz, uint64_t seed) {
+static int eigvecs_run(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
+                       double* Z, int64_t ldz, uint64_t seed, int dz) {
     if (!h) return TINV_ERR_HANDLE;
     if (n < 1) return -2;
     if (!d) return -3;
@@ -646,6 +656,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     h->iters_n = 0;
     S.n = n;
     int launches = 0;
+    bool dz_timed = false;   // events 9 / 15 around the deferred pass D launches (profiling)
 
     // ---------------- prep, then (without waiting for the host) the batched LU, the
     // finalize of finished vectors and the factor/iterate packing of clustered vectors; the
@@ -1209,6 +1220,11 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
         ca.reorth = h->mgs;
         ca.lab = lab;
         ca.pf = getenv("TINV_PF") ? atoi(getenv("TINV_PF")) : 0;
+        if (dz) {   // deferred final pass D: c per vector, 0 = not parked
+            CK(cudaMemsetAsync(h->dzc, 0, sizeof(double) * n, st));
+            ca.dzc = h->dzc;
+            ca.dzx = h->X1c;
+        }
         unsigned long long* pcta = nullptr;
         if (getenv("TINV_PROF_CTA")) {   // debug only (not the product path): per-CTA phase busy times
             CK(cudaMalloc(&pcta, sizeof(unsigned long long) * 16 * sc.nctas));
@@ -1233,6 +1249,21 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
             }
         }
         launches++;
+        if (dz) {   // the parked columns of each group's last cluster (the kernel's dz_cl rule)
+            const int64_t n2v = (n + 1) & ~int64_t(1);
+            ev_record(h, 9);
+            dz_timed = true;
+            for (int g = 0; g < ng; g++) {
+                if (sc.coff[g + 1] <= sc.coff[g] || ws[g].nrk != 1) continue;
+                const int cl = sc.clist[sc.coff[g + 1] - 1];
+                const int64_t j1 = cs[cl], m = cs[cl + 1] - cs[cl];
+                if (m <= kNarrowM + 1) continue;
+                DzArgs za{n, m, kNarrowM, ws[g].Y, h->X1c + j1 * n2v, n2v, h->dzc + j1, Z + j1 * ldz, ldz, h->dzp, h->out};
+                CK(launch_dz(za, st));
+                launches += 2;
+            }
+            ev_record(h, 15);
+        }
         S.ngroups = ng;
         S.cwy_ctas = sc.nctas;
         // algorithmic bytes: computed after the iteration counts are known (below)
@@ -1318,6 +1349,7 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     S.launches = launches;
     if (h->profiling) {
         float ms = 0.f;
+        if (dz_timed) { cudaEventElapsedTime(&ms, h->ev[9], h->ev[15]); S.dz_ms = ms; }
         cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]); S.kernel_ms[0] = ms;
         cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); S.kernel_ms[1] = ms;
         cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); S.kernel_ms[2] = ms;
@@ -1329,7 +1361,25 @@ int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const do
     }
     const int nflag = h->h_out->nflag;
     S.nflagged = nflag;
+    S.dz_parked = h->h_out->dzpark;
     return nflag;
+}
+
+int tinv_eigvecs(tinv_t h, int64_t n, const double* d, const double* e, const double* w,
+                 double* Z, int64_t ldz, uint64_t seed) {
+    // deferred final pass D (dz.cu) on single-rank calls; TINV_DZ=0 off, TINV_DZ=2 (test hook)
+    // treats every parked vector as failed so the re-run path below is exercised
+    const int dzenv = getenv("TINV_DZ") ? atoi(getenv("TINV_DZ")) : 1;
+    const int dz = (h && h->dz && h->nranks == 1 && h->mgs != 1) ? dzenv : 0;
+    int rc = eigvecs_run(h, n, d, e, w, Z, ldz, seed, dz);
+    if (rc >= 0 && dz && (h->h_out->dzfail > 0 || dz == 2)) {
+        // a parked vector's deferred stopping test failed (or the test hook): its iteration was
+        // not the last, and later vectors used its trial reflector -- redo the call as written
+        const int fails = h->h_out->dzfail;
+        rc = eigvecs_run(h, n, d, e, w, Z, ldz, seed, 0);
+        h->stats.dz_redo = fails > 0 ? fails : -1;
+    }
+    return rc;
 }
 
 int tinv_eigvals(tinv_t h, int64_t n, const double* d, const double* e, double* w) {

@@ -18,7 +18,8 @@ struct PrepOut {
     int nflag;          // vectors that missed the stopping rule
     int nc_pad;         // slots of the vectors the batched LU iterates, rounded up to 32
     int scale_exp;      // k of the 2^k scaling (reading 21), 0 inside the window
-    int pad;
+    int dzfail;         // parked vectors (deferred pass D) whose stopping test failed -> re-run
+    int dzpark;         // parked vectors (deferred pass D) formed by dz_finish
 };
 
 struct PrepArgs {
@@ -187,7 +188,29 @@ struct CwyArgs {
     int lab;                 // blocked look-ahead block size b (2..8; 0/1 = off), wide clusters of single-rank groups
     int pf;                  // rows whose first pieces of the next wide pass are prefetched into L2 before a barrier (TINV_PF; 0 = off)
     unsigned long long* prof_cta;   // debug: per-CTA busy time before each phase's barrier [cta*16 + phase], or NULL
+    // deferred final pass D: NULL = off.  dzc[j] = c of vector j when its last
+    // pass D was deferred (0 otherwise; zeroed by the host per call); its x' is stored in
+    // dzx + j * roundup(n, 2) (= X1c, the vector's dead first iterate)
+    double* dzc;
+    double* dzx;
 };
+
+// Deferred final pass D (dz.cu): for the parked vectors p0 <= p < m of one cluster,
+// q_p = Y_{p+1} x'_p - e_p (one GEMM), the stopping test, the sign rule and z_j.
+struct DzArgs {
+    int64_t n;
+    int64_t m;          // cluster size
+    int64_t p0;         // first column that may be parked (kNarrowM)
+    const double* Y;    // the group's packed Y (y_row_off(i, m) rows)
+    const double* X;    // x' of column p at X + p * n2v (p + 1 entries)
+    int64_t n2v;
+    const double* c;    // dzc + j1: c of column p, 0 = not parked
+    double* Z;          // Z + j1 * ldz: column p at Z + p * ldz
+    int64_t ldz;
+    double* part;       // partials [row tile][3][m - p0]
+    PrepOut* out;       // dzfail (deferred test failed), counted per column
+};
+cudaError_t launch_dz(const DzArgs& a, cudaStream_t s);
 
 // Resident compact-WY kernel for narrow clusters (cwy_resident.cu): one thread-block cluster
 // of CS CTAs per eigen-cluster, Y kept in distributed shared memory.

@@ -19,7 +19,8 @@ if os.environ.get("TINV_LIB_VARIANT"):   # performance A/B of two in-tree builds
 EXPORTS = ("tinv_create", "tinv_eigvecs", "tinv_eigvecs_host", "tinv_destroy", "tinv_strerror",
            "tinv_set_profiling", "tinv_get_stats", "tinv_abi_version", "tinv_partition",
            "tinv_eigvals", "tinv_eig", "tinv_set_virtual_ranks", "tinv_set_resident", "tinv_set_reorth",
-           "tinv_set_lookahead", "tinv_set_host_exchange", "tinv_debug_peer_map", "tinv_plan")
+           "tinv_set_lookahead", "tinv_set_host_exchange", "tinv_debug_peer_map", "tinv_plan",
+           "tinv_set_deferred")
 
 # include/tinv.h tinv_allgather_fn: int (*)(const void* send, void* recv, size_t bytes, void* ctx)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -39,7 +40,8 @@ class TinvStats(C.Structure):
                 ("launches", C.c_int64), ("group_syncs", C.c_int64), ("ngroups", C.c_int64),
                 ("cwy_ctas", C.c_int64), ("resident_groups", C.c_int64), ("reorth_bytes", C.c_double), ("solve_bytes", C.c_double),
                 ("kernel_ms", C.c_double * 6), ("kernel_launches", C.c_int64 * 6),
-                ("cwy_phase_ms", C.c_double * 16)]
+                ("cwy_phase_ms", C.c_double * 16), ("dz_parked", C.c_int64), ("dz_redo", C.c_int64),
+                ("dz_ms", C.c_double)]
 
     def as_dict(self):
         return {
@@ -52,6 +54,7 @@ class TinvStats(C.Structure):
             "kernel_ms": dict(zip(KERNEL_NAMES, list(self.kernel_ms))),
             "kernel_launches": dict(zip(KERNEL_NAMES, list(self.kernel_launches))),
             "cwy_phase_ms": dict(zip(PHASE_NAMES, list(self.cwy_phase_ms))),
+            "dz_parked": self.dz_parked, "dz_redo": self.dz_redo, "dz_ms": self.dz_ms,
         }
 
 
@@ -93,6 +96,8 @@ def load_library(path: str = LIB_PATH):
     L.tinv_set_reorth.argtypes = [P, C.c_int]
     L.tinv_set_lookahead.restype = C.c_int
     L.tinv_set_lookahead.argtypes = [P, C.c_int]
+    L.tinv_set_deferred.restype = C.c_int
+    L.tinv_set_deferred.argtypes = [P, C.c_int]
     L.tinv_set_host_exchange.restype = C.c_int
     L.tinv_set_host_exchange.argtypes = [P, ALLGATHER_FN, P]
     L.tinv_debug_peer_map.restype = C.c_int
@@ -199,6 +204,12 @@ class Tinv:
         rc = self._L.tinv_set_lookahead(self._h, int(b))
         if rc:
             raise TinvError(f"tinv_set_lookahead failed: {rc}")
+
+    def set_deferred(self, enable: bool):
+        """Deferred final pass D (include/tinv.h tinv_set_deferred; default on)."""
+        rc = self._L.tinv_set_deferred(self._h, int(bool(enable)))
+        if rc:
+            raise TinvError(f"tinv_set_deferred failed: {rc}")
 
     def set_host_exchange(self, allgather):
         """Exchange the CUDA IPC handles through ``allgather(send: bytes, nbytes) -> bytes`` (a

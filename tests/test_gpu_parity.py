@@ -774,3 +774,98 @@ def test_row_split_virtual_ranks_mixed(handle, torch, vr):
     finally:
         handle.set_virtual_ranks(1)
     assert st["ngroups"] >= vr + 1, st["ngroups"]     # vr split groups + the other clusters' groups
+
+
+# ------------------------------------------------------------------ deferred final pass D
+# the last iteration's pass D (q = Y_{p+1} x' - e_p) of a wide
+# cluster's vector is formed after the cWY kernel by one GEMM (dz.cu) from the parked x'; Y and
+# T are bitwise those of the per-vector path, so only the parked columns' summation order
+# differs.  A failed deferred stopping test re-runs the call without deferral.
+
+def _run_dz(handle, torch, d, e, w, dz, env=None):
+    handle.set_deferred(dz)
+    old = os.environ.get("TINV_DZ")
+    if env is not None:
+        os.environ["TINV_DZ"] = env
+    try:
+        Z, rc = run_gpu(handle, torch, d, e, w)
+        st = handle.stats()
+    finally:
+        handle.set_deferred(True)
+        if env is not None:
+            if old is None:
+                del os.environ["TINV_DZ"]
+            else:
+                os.environ["TINV_DZ"] = old
+    return Z, rc, st
+
+
+@pytest.mark.parametrize("b", [0, 8])
+@pytest.mark.parametrize("cfg,n", [("cfg4", 600), ("cfg3", 1050), ("cfg5", 1500), ("type2", 700), ("cfg4", 1999)])
+def test_deferred_pass_d_parity(handle, torch, cfg, n, b):
+    d, e, w = W.problem(cfg, n)
+    handle.set_lookahead(b)
+    try:
+        Zd, rc, st = _run_dz(handle, torch, d, e, w, True)
+        Zn, rc2, st2 = _run_dz(handle, torch, d, e, w, False)
+    finally:
+        handle.set_lookahead(0)
+    assert rc == 0 and rc2 == 0
+    assert st["dz_parked"] > 0 and st["dz_redo"] == 0, st
+    assert st2["dz_parked"] == 0
+    assert st["iters_hist"] == st2["iters_hist"]
+    Zd_h, Zn_h = Zd.cpu().numpy(), Zn.cpu().numpy()
+    diff = np.minimum(np.abs(Zd_h - Zn_h).max(axis=0), np.abs(Zd_h + Zn_h).max(axis=0)).max()
+    assert diff <= 1e-12, diff
+    res, orth = invariants_gpu(torch, d, e, w, Zd)
+    assert res <= 10.0 and orth <= 10.0
+    Zo, info = O.eigvecs(d, e, w, seed=1)
+    wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Zd_h, Zo)
+    assert wv <= TOL_VEC and ws >= 1 - TOL_SUB
+
+
+def test_deferred_pass_d_forced_rerun(handle, torch):
+    """TINV_DZ=2 treats every parked vector as failed: the call re-runs without deferral and
+    returns exactly the per-vector path's Z."""
+    d, e, w = W.problem("cfg4", 800)
+    handle.set_lookahead(8)
+    try:
+        Zf, rc, st = _run_dz(handle, torch, d, e, w, True, env="2")
+        Zn, rc2, _ = _run_dz(handle, torch, d, e, w, False)
+    finally:
+        handle.set_lookahead(0)
+    assert rc == 0 and rc2 == 0
+    assert st["dz_redo"] == -1 and st["dz_parked"] == 0, st
+    assert torch.equal(Zf, Zn)
+
+
+def test_deferred_pass_d_restarts_and_flags(handle, torch):
+    """The restart / MAXITS fixture of test_blocked_lookahead_restarts with the deferral on:
+    same return code and iteration histogram as the oracle, whether or not a deferred test
+    failed (then the call re-ran without deferral)."""
+    d = np.concatenate([[1.0], 200.0 + np.arange(79.0)])
+    e = np.zeros(79)
+    w = np.concatenate([[1.0] * 70, d[70:]])
+    Zo, info, its = O.eigvecs(d, e, w, seed=1, return_iters=True)
+    for b in (0, 4):
+        handle.set_lookahead(b)
+        try:
+            Zg, rc, st = _run_dz(handle, torch, d, e, w, True)
+            hist = _iters_of(handle)
+        finally:
+            handle.set_lookahead(0)
+        assert rc == info, (b, rc, info, st["dz_redo"])
+        assert hist == list(np.bincount(its, minlength=8)[:8]), (b, hist)
+        assert np.abs(np.linalg.norm(Zg.cpu().numpy(), axis=0) - 1).max() <= 1e-14
+
+
+def test_deferred_pass_d_full_size_cfg4(handle, torch):
+    d, e, w = W.problem("cfg4")
+    handle.set_lookahead(8)
+    try:
+        Zg, rc, st = _run_dz(handle, torch, d, e, w, True)
+    finally:
+        handle.set_lookahead(0)
+    assert rc == 0 and st["dz_parked"] > 7000 and st["dz_redo"] == 0, st
+    res, orth = invariants_gpu(torch, d, e, w, Zg)
+    assert res <= 10.0 and orth <= 10.0
