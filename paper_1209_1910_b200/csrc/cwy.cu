@@ -99,9 +99,18 @@ __device__ __forceinline__ int64_t sum_floor_pw(int64_t l) {
     const int64_t q = (int64_t)((uint32_t)l / (uint32_t)kPieceW), rem = l - q * kPieceW;   // l < 2^31
     return (int64_t)kPieceW * q * (q - 1) / 2 + rem * q;
 }
+// Boundary q of G shares of the weight W when the group's first CTA takes (1000 - h0) / 1000 of a
+// share (CwyArgs::cta0_pm).  Measured: in pass D CTA 0 -- the short rows of the leading triangle
+// -- is 10-19% slower than the median CTA under the element + piece cost model; cutting its share
+// by 12% takes 9% off D on cfg5 and 6% on cfg4 (more brings nothing: the next CTAs bound the
+// pass), and does nothing for TT / TN, whose slowest CTAs are elsewhere.
+__device__ __forceinline__ int64_t share_bound(int64_t W, int q, int G, int h0) {
+    if (h0 == 0 || q == 0) return (W * q) / G;
+    return (W * ((int64_t)q * 1000 - h0)) / ((int64_t)G * 1000 - h0);
+}
 // rows of A / D: row i has min(i+1, P) elements in min(floor(i / kPieceW) + 1, nblk) pieces
 __device__ __forceinline__ void part_rows_weighted(int64_t n, int64_t P, int r, int G, int64_t& a, int64_t& b,
-                                                   int64_t C) {
+                                                   int64_t C, int h0 = 0) {
     if (P <= kNarrowM) C = 0;
     const int64_t NB = (P + kPieceW - 1) / kPieceW;
     const int64_t base = P * (P + 1) / 2 + C * ((NB > 1 ? sum_floor_pw(P) : 0) + P);
@@ -110,8 +119,8 @@ __device__ __forceinline__ void part_rows_weighted(int64_t n, int64_t P, int r, 
         return base + (i - P) * (P + C * NB);
     };
     int64_t W = cum(n);
-    a = (r == 0) ? 0 : bsearch_cum(0, n, (W * r) / G, cum);
-    b = (r == G - 1) ? n : bsearch_cum(0, n, (W * (r + 1)) / G, cum);
+    a = (r == 0) ? 0 : bsearch_cum(0, n, share_bound(W, r, G, h0), cum);
+    b = (r == G - 1) ? n : bsearch_cum(0, n, share_bound(W, r + 1, G, h0), cum);
 }
 // rows [b0, b1) of Y_P split over G CTAs by the same weights (rows of one band of the sweep)
 __device__ __forceinline__ void part_band_weighted(int64_t b0, int64_t b1, int64_t P, int r, int G, int64_t& a,
@@ -133,24 +142,24 @@ __device__ __forceinline__ void part_uniform(int64_t lo, int64_t hi, int r, int 
     b = lo + (len * (r + 1)) / G;
 }
 // k in [0,p): packed column k of T has k+1 elements in floor(k / kPieceW) + 1 pieces
-__device__ __forceinline__ void part_tt(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C) {
+__device__ __forceinline__ void part_tt(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C, int h0 = 0) {
     if (p <= kNarrowM) C = 0;
     const bool multi = p > kPieceW;
     auto cum = [C, multi](int64_t k) -> int64_t { return k * (k + 1) / 2 + C * ((multi ? sum_floor_pw(k) : 0) + k); };
     int64_t W = cum(p);
-    a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
-    b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
+    a = (r == 0) ? 0 : bsearch_cum(0, p, share_bound(W, r, G, h0), cum);
+    b = (r == G - 1) ? p : bsearch_cum(0, p, share_bound(W, r + 1, G, h0), cum);
 }
 // l in [0,p): row l of T has p-l elements in nblk - floor(l / kPieceW) pieces
-__device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C) {
+__device__ __forceinline__ void part_tn(int64_t p, int r, int G, int64_t& a, int64_t& b, int64_t C, int h0 = 0) {
     if (p <= kNarrowM) C = 0;
     const int64_t NB = (p + kPieceW - 1) / kPieceW;
     auto cum = [p, C, NB](int64_t l) -> int64_t {
         return l * p - l * (l - 1) / 2 + C * (l * NB - (NB > 1 ? sum_floor_pw(l) : 0));
     };
     int64_t W = cum(p);
-    a = (r == 0) ? 0 : bsearch_cum(0, p, (W * r) / G, cum);
-    b = (r == G - 1) ? p : bsearch_cum(0, p, (W * (r + 1)) / G, cum);
+    a = (r == 0) ? 0 : bsearch_cum(0, p, share_bound(W, r, G, h0), cum);
+    b = (r == G - 1) ? p : bsearch_cum(0, p, share_bound(W, r + 1, G, h0), cum);
 }
 
 // dynamic shared memory carve-up
@@ -674,7 +683,10 @@ __device__ __noinline__ void sweep_chunk(const double* __restrict__ Fs, const do
 // the dependent chain.  Same arithmetic, same order as back_sweep.  `xseq` counts the chunks
 // of every such sweep (both threads keep identical copies): buffer = seq & 1, its use = seq >> 1.
 __device__ void back_sweep_ws(const CwyArgs& a, const GroupWS& ws, int64_t j, const Smem& sm, uint32_t& mbph,
-                              uint32_t& xseq, bool helper, unsigned int* prog, unsigned int tag) {
+                              uint32_t& xseq, bool helper, unsigned int* prog, unsigned int tag, uint64_t* dt = nullptr) {
+    // dt (debug build, TINV_DBG bit 3; chain thread): SM clocks in [0] buffer / ring waits, [1] the
+    // chains, [2] the hand-over, [3] total
+    const uint64_t d0 = dt ? (uint64_t)clock64() : 0;
     const int64_t n = a.n;
     const double* __restrict__ F = a.F + j * n * 4;
     const double* __restrict__ ts = ws.ysol;
@@ -705,15 +717,16 @@ __device__ void back_sweep_ws(const CwyArgs& a, const GroupWS& ws, int64_t j, co
         for (int64_t k = 0; k < C; k++) {
             const uint32_t sq = xseq + (uint32_t)k, b = sq & 1u;
             mbar_wait(xfull + b, (sq >> 1) & 1u);   // chunk k in xbuf[b]; its ring slot is consumed
-            if (k + kRing < C) issue(k + kRing);
             int64_t lo, hi;
             rows(k, lo, hi);
             bulk_s2g(x + lo, xbuf + b * CH, (uint32_t)((hi - lo + 1) & ~int64_t(1)) * 8u);
             bulk_commit();
-            if (k > 0) {   // the store of chunk k-1 has read its buffer
-                bulk_wait_read<1>();
-                mbar_arrive(xempty + (b ^ 1u));
-            }
+            if (k + kRing < C) issue(k + kRing);
+            // the buffer is free as soon as this store has read it -- during the chain of chunk
+            // k+1, so chunk k+2 never waits for it (released one step later, after the wake-up
+            // of the next hand-over, the chain thread stood ~0.5 us per chunk: 18% of the sweep)
+            bulk_wait_read<0>();
+            mbar_arrive(xempty + b);
             // band b = chunks [b band_ch, (b+1) band_ch) complete once at most the newest group
             // (this chunk's store) is pending
             if (prog && k % a.band_ch == 0 && k > 0) {
@@ -722,8 +735,6 @@ __device__ void back_sweep_ws(const CwyArgs& a, const GroupWS& ws, int64_t j, co
                 publish(prog, tag + (unsigned int)(k / a.band_ch));
             }
         }
-        bulk_wait_read<0>();
-        mbar_arrive(xempty + ((xseq + (uint32_t)C - 1u) & 1u));
         bulk_wait_all();
         fence_proxy_async_global();   // the bulk-stored x before the group barrier's release
         if (prog) publish(prog, tag + (unsigned int)sweep_bands(n, a.band_ch));
@@ -733,6 +744,7 @@ __device__ void back_sweep_ws(const CwyArgs& a, const GroupWS& ws, int64_t j, co
             const uint32_t sq = xseq + (uint32_t)k, b = sq & 1u;
             const int slot = (int)(k % kRing);
             double* xb = xbuf + b * CH;
+            const uint64_t e0 = dt ? (uint64_t)clock64() : 0;
             if (sq >= 2u) mbar_wait(xempty + b, ((sq >> 1) - 1u) & 1u);   // the store of seq - 2 read it
             mbar_wait(sm.mbar + slot, (mbph >> slot) & 1u);
             mbph ^= 1u << slot;
@@ -742,13 +754,20 @@ __device__ void back_sweep_ws(const CwyArgs& a, const GroupWS& ws, int64_t j, co
             rows(k, lo, hi);
             const int cnt = (int)(hi - lo);
             if (a.sweep2 == 2) {
+                const uint64_t e1 = dt ? (uint64_t)clock64() : 0;
                 double x12[2] = {x1, x2};
                 sweep_chunk(Fs, Ts, xb, cnt, x12);
                 x1 = x12[0];
                 x2 = x12[1];
+                const uint64_t e2 = dt ? (uint64_t)clock64() : 0;
                 if (cnt & 1) xb[cnt] = 0.0;
                 fence_proxy_async_smem();
                 mbar_arrive(xfull + b);
+                if (dt) {
+                    dt[0] += e1 - e0;
+                    dt[1] += e2 - e1;
+                    dt[2] += (uint64_t)clock64() - e2;
+                }
                 continue;
             }
             const int top = cnt & ~15;
@@ -782,6 +801,7 @@ __device__ void back_sweep_ws(const CwyArgs& a, const GroupWS& ws, int64_t j, co
         }
     }
     xseq += (uint32_t)C;
+    if (dt) dt[3] += (uint64_t)clock64() - d0;
 }
 
 // Composition of the forward maps of CTAs 0..cnt-1 (S slots FA, FB), applied in CTA order, by
@@ -1795,7 +1815,7 @@ __device__ void lab_rowdots(const Smem& sm, int64_t r0, int64_t r1, int64_t P, c
                 double a[NV];
 #pragma unroll
                 for (int v = 0; v < NV; v++) a[v] = 0.0;
-                constexpr int U = 8;
+                constexpr int U = 8;   // (16 in flight per lane measured slower: first-iteration GEMMs 297 -> 355 ms on cfg4)
                 for (int64_t k0 = c0 + 2 * lane; k0 < e1; k0 += 64 * U) {
                     double2 y[U];
 #pragma unroll
@@ -2137,7 +2157,7 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
             part_rows_weighted(n, p, cg, Gt, pa0, pa1, a.piece_cost);
             part_tt(p, cg, Gt, ptt0, ptt1, a.piece_cost);
             part_tn(p, cg, Gt, ptn0, ptn1, a.piece_cost);
-            part_rows_weighted(n, p + 1, cg, Gt, pd0, pd1, a.piece_cost);
+            part_rows_weighted(n, p + 1, cg, Gt, pd0, pd1, a.piece_cost, a.cta0_pm);
             bool use_lab = in_lab(p);   // first iteration from the block's U (no pass A, TT or BC rows)
             if (use_lab && (p - kLab0) % a.lab == 0) {
                 // ---------------- BL1-BL3: U = X - Y_k T_k^T Y_k^T X for x^(1)_k .. x^(1)_{k+nv-1}
@@ -2922,7 +2942,8 @@ __global__ void __launch_bounds__(NT, 1) cwy_kernel(CwyArgs a) {
                         rph = *reinterpret_cast<volatile uint32_t*>(sm.red + NW + 7);
                     } else if (r == 0 && a.sweep2) {
                         if (tid == 0 || tid == 32)
-                            back_sweep_ws(a, ws, j, sm, mbph, xseq, tid == 32, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8);
+                            back_sweep_ws(a, ws, j, sm, mbph, xseq, tid == 32, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8,
+                                          (kWideDebug && (a.dbg & 8) && dsub && tid == 0) ? dtim : nullptr);
                     } else if (r == 0 && tid == 0) {
                         back_sweep(a, ws, j, sm, mbph, a2 ? sw_prog : nullptr, (sw_ep + 1) << 8,
                                    (kWideDebug && (a.dbg & 8) && dsub) ? dtim : nullptr);

@@ -1208,6 +1208,7 @@ static int eigvecs_run(tinv_t h, int64_t n, const double* d, const double* e, co
         ca.vcap = vcap;
         ca.nstg = nstg;
         ca.piece_cost = getenv("TINV_PIECE_COST") ? atoi(getenv("TINV_PIECE_COST")) : 4000;
+        ca.cta0_pm = getenv("TINV_CTA0") ? std::max(0, std::min(900, atoi(getenv("TINV_CTA0")))) : 120;
         ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
         ca.a2 = getenv("TINV_A2") ? atoi(getenv("TINV_A2")) : 1;
         ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 8;
@@ -1246,6 +1247,11 @@ static int eigvecs_run(tinv_t h, int64_t n, const double* d, const double* e, co
                 int amax = (int)(std::max_element(v.begin(), v.end()) - v.begin());
                 fprintf(stderr, "[tinv] cta busy phase %2d (ms): min %.3f med %.3f max %.3f (cta %d) cta0 %.3f\n", k,
                         srt.front(), srt[srt.size() / 2], srt.back(), amax, v[0]);
+                if (atoi(getenv("TINV_PROF_CTA")) >= 2) {   // every CTA's value
+                    fprintf(stderr, "[tinv] cta busy phase %2d all:", k);
+                    for (double x : v) fprintf(stderr, " %.3f", x);
+                    fprintf(stderr, "\n");
+                }
             }
         }
         launches++;

@@ -175,6 +175,7 @@ struct CwyArgs {
     int nstg;                // TMA ring stages for narrow clusters (0 = ring not allocated)
     int prof_p0, prof_p1;    // phase timers count only vectors with prof_p0 <= j_c < prof_p1
     int piece_cost;          // partition cost of one wide row piece, in elements (cwy.cu part_*)
+    int cta0_pm;             // per-mille cut of CTA 0's share of pass D's rows (wide clusters; cwy.cu share_bound)
     int prof_sel;            // debug: CTA whose thread 32 runs the pass timers (default: the first group's first)
     int a2;                  // fuse iteration 2's pass A behind the back sweep (TINV_A2, default 1)
     int band_ch;             // sweep chunks (256 rows) per published band (TINV_BANDCH)

@@ -869,3 +869,32 @@ def test_deferred_pass_d_full_size_cfg4(handle, torch):
     assert rc == 0 and st["dz_parked"] > 7000 and st["dz_redo"] == 0, st
     res, orth = invariants_gpu(torch, d, e, w, Zg)
     assert res <= 10.0 and orth <= 10.0
+
+
+@pytest.mark.parametrize("cfg,n", [("cfg4", 900), ("cfg5", 1500), ("type1", 1050)])
+def test_pass_d_cta0_share(handle, torch, cfg, n):
+    """TINV_CTA0 (per-mille cut of CTA 0's share of pass D's rows, default 120) only moves whole
+    rows of the row-dot pass D -- and with them the CTA pieces of the partitioned forward sweep --
+    between CTAs: same iteration counts, Z equal to rounding, invariants and oracle parity at
+    every setting."""
+    d, e, w = W.problem(cfg, n)
+    dd, de, dw = (torch.tensor(x, dtype=torch.float64, device="cuda:0") for x in (d, e, w))
+    old = os.environ.get("TINV_CTA0")
+    out = {}
+    try:
+        for v in ("0", "120", "600"):
+            os.environ["TINV_CTA0"] = v
+            Z, rc = handle.eigvecs(dd, de, dw, seed=1)
+            out[v] = (Z.clone(), rc, handle.stats()["iters_hist"])
+    finally:
+        if old is None:
+            del os.environ["TINV_CTA0"]
+        else:
+            os.environ["TINV_CTA0"] = old
+    Zo, info = O.eigvecs(d, e, w, seed=1)
+    for v, (Z, rc, hist) in out.items():
+        assert rc == 0 and hist == out["0"][2], (v, rc, hist)
+        res, orth = invariants_gpu(torch, d, e, w, Z)
+        assert res <= 10.0 and orth <= 10.0, (v, res, orth)
+        wv, ws, _, _ = parity_report(w, O.tnorm(d, e), Z.cpu().numpy(), Zo)
+        assert wv <= TOL_VEC and ws >= 1 - TOL_SUB, (v, wv, ws)
