@@ -1211,7 +1211,10 @@ static int eigvecs_run(tinv_t h, int64_t n, const double* d, const double* e, co
         ca.cta0_pm = getenv("TINV_CTA0") ? std::max(0, std::min(900, atoi(getenv("TINV_CTA0")))) : 120;
         ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
         ca.a2 = getenv("TINV_A2") ? atoi(getenv("TINV_A2")) : 1;
-        ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : 8;
+        // ~8 bands per sweep, 3..8 chunks each (measured: cfg3 4, cfg4 4, cfg5 6-8 chunks best; larger
+        // bands delay the fused pass A2 behind the sweep, smaller ones cost more publications)
+        const int band_def = (int)std::max<int64_t>(3, std::min<int64_t>(8, ((n + 255) / 256 + 4) / 8));
+        ca.band_ch = getenv("TINV_BANDCH") ? std::max(1, atoi(getenv("TINV_BANDCH"))) : band_def;
         ca.sweep2 = getenv("TINV_SWEEP2") ? atoi(getenv("TINV_SWEEP2")) : 2;
         ca.a2c = getenv("TINV_A2C") ? atoi(getenv("TINV_A2C")) : 1;
         ca.tyr = getenv("TINV_TYR") ? atoi(getenv("TINV_TYR")) : 1;
