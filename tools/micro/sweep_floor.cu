@@ -5,6 +5,7 @@
 //  D  as C with 32-row batches
 //  E  as C, the next batch's loads issued between the chain's FMAs (manual 2-batch unroll)
 //  F  as C with t scaled by 1e-310 (every x subnormal)
+//  H  as C, the first 4 rows of the next batch loaded during the current one; I the same with 8-row batches
 //  G  as C with t scaled by 1e-300 and |b|, |c| ~ 1e-3 (x decays through the subnormal range)
 #include <cstdio>
 #include <vector>
@@ -101,6 +102,54 @@ __global__ void probe(const double* bcg, const double* tg, int n, long long* cyc
         cyc[4] = clock64() - t0;
         acc += x1;
     }
+    {   // H: as C, the operands of the first 4 rows of the next batch loaded during this one
+        double x1 = 0.0, x2 = 0.0;
+        long long t0 = clock64();
+        const int top = (n & ~15);
+        double hb[4], hc[4], ht[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) { const double2 v = BC[top - 4 + u]; hb[u] = v.x; hc[u] = v.y; ht[u] = tf[top - 4 + u]; }
+        for (int u0 = top - 16; u0 >= 0; u0 -= 16) {
+            double b[16], c[16], t[16], xv[16];
+#pragma unroll
+            for (int u = 12; u < 16; u++) { b[u] = hb[u - 12]; c[u] = hc[u - 12]; t[u] = ht[u - 12]; }
+#pragma unroll
+            for (int u = 0; u < 12; u++) { const double2 v = BC[u0 + u]; b[u] = v.x; c[u] = v.y; t[u] = tf[u0 + u]; }
+            const int un = u0 >= 16 ? u0 - 16 : 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++) { const double2 v = BC[un + 12 + u]; hb[u] = v.x; hc[u] = v.y; ht[u] = tf[un + 12 + u]; }
+#pragma unroll
+            for (int u = 15; u >= 0; u--) { xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u])); x2 = x1; x1 = xv[u]; }
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) *reinterpret_cast<double2*>(xo + u0 + u) = make_double2(xv[u], xv[u + 1]);
+        }
+        cyc[7] = clock64() - t0;
+        acc += x1;
+    }
+    {   // I: 8-row batches with the same 4-row head
+        double x1 = 0.0, x2 = 0.0;
+        long long t0 = clock64();
+        const int top = (n & ~15);
+        double hb[4], hc[4], ht[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) { const double2 v = BC[top - 4 + u]; hb[u] = v.x; hc[u] = v.y; ht[u] = tf[top - 4 + u]; }
+        for (int u0 = top - 8; u0 >= 0; u0 -= 8) {
+            double b[8], c[8], t[8], xv[8];
+#pragma unroll
+            for (int u = 4; u < 8; u++) { b[u] = hb[u - 4]; c[u] = hc[u - 4]; t[u] = ht[u - 4]; }
+#pragma unroll
+            for (int u = 0; u < 4; u++) { const double2 v = BC[u0 + u]; b[u] = v.x; c[u] = v.y; t[u] = tf[u0 + u]; }
+            const int un = u0 >= 8 ? u0 - 8 : 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++) { const double2 v = BC[un + 4 + u]; hb[u] = v.x; hc[u] = v.y; ht[u] = tf[un + 4 + u]; }
+#pragma unroll
+            for (int u = 7; u >= 0; u--) { xv[u] = fma(-b[u], x1, fma(-c[u], x2, t[u])); x2 = x1; x1 = xv[u]; }
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) *reinterpret_cast<double2*>(xo + u0 + u) = make_double2(xv[u], xv[u + 1]);
+        }
+        cyc[8] = clock64() - t0;
+        acc += x1;
+    }
     {   // F, G: subnormal operands
         for (int i = 0; i < n; i++) tf[i] = tg[i] * 1e-310;
         double x1 = 0.0, x2 = 0.0;
@@ -125,14 +174,14 @@ int main() {
     for (auto& v : bc) v = 0.5 * U(g);
     for (auto& v : t) v = U(g);
     double *dbc, *dt, *sink; long long* dc;
-    cudaMalloc(&dbc, 16 * n); cudaMalloc(&dt, 8 * n); cudaMalloc(&dc, 64); cudaMalloc(&sink, 8);
+    cudaMalloc(&dbc, 16 * n); cudaMalloc(&dt, 8 * n); cudaMalloc(&dc, 128); cudaMalloc(&sink, 8);
     cudaMemcpy(dbc, bc.data(), 16 * n, cudaMemcpyHostToDevice);
     cudaMemcpy(dt, t.data(), 8 * n, cudaMemcpyHostToDevice);
     size_t smem = (size_t)(n + 2) * 16 + 16 * n + 64;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int rep = 0; rep < 2; rep++) probe<<<1, 256, smem>>>(dbc, dt, n, dc, sink);
-    long long h[8]; cudaMemcpy(h, dc, 64, cudaMemcpyDeviceToHost);
-    const char* nm[7] = {"A 1 DFMA/row, regs", "B recurrence, regs", "C 16-batch smem", "D 32-batch smem", "E 2-set interleaved",
-                         "F C, subnormal x", "G C, x decaying"};
-    for (int v = 0; v < 7; v++) printf("%-22s %.2f cycles/row (%s)\n", nm[v], (double)h[v] / n, cudaGetErrorString(cudaGetLastError()));
+    long long h[16]; cudaMemcpy(h, dc, 128, cudaMemcpyDeviceToHost);
+    const char* nm[9] = {"A 1 DFMA/row, regs", "B recurrence, regs", "C 16-batch smem", "D 32-batch smem", "E 2-set interleaved",
+                         "F C, subnormal x", "G C, x decaying", "H C + 4-row head", "I 8-batch + 4-row head"};
+    for (int v = 0; v < 9; v++) printf("%-22s %.2f cycles/row (%s)\n", nm[v], (double)h[v] / n, cudaGetErrorString(cudaGetLastError()));
 }
