@@ -1,6 +1,7 @@
 """Randomised parity sweep of the device path against the oracle (seeded): random, clustered
 (thread-block-cluster sizes 1..8, m up to 64), glued-Wilkinson, Laplacian-like and diagonal-
-dominant problems at n in [2, 2500], all three reorthogonalisation modes.  Prints one line per case and
+dominant problems at n in [2, 2500], single wide clusters and the paper's Type 1 / Type 2
+matrices, all three reorthogonalisation modes.  Prints one line per case and
 a summary; exits 1 on any failure."""
 import os
 import sys
@@ -27,7 +28,16 @@ def clustered(n, sizes, rng):
 
 
 def case(k, rng):
-    kind = k % 5
+    kind = k % 7
+    if kind == 5:   # one wide cluster (persistent kernel: look-ahead blocks, deferred D, window passes)
+        n = int(rng.integers(70, 1400))
+        d, e = W.make("cfg4", n, int(rng.integers(1 << 30)))
+        return f"giant cluster n={n}", d, e, W.eigenvalues(d, e)
+    if kind == 6:   # the paper's Type 1 / Type 2 matrices: wide + narrow clusters mixed
+        n = int(rng.integers(100, 1300))
+        t = "type1" if (k // 7) % 2 == 0 else "type2"
+        d, e = W.make(t, n, 0)
+        return f"{t} n={n}", d, e, W.eigenvalues(d, e)
     if kind == 0:
         n = int(rng.integers(2, 2500))
         d, e = W.random_sym(n, int(rng.integers(1 << 30)))
@@ -60,7 +70,8 @@ def main():
     fails = 0
     for k in range(cases):
         name, d, e, w = case(k, rng)
-        mode = "mgs" if k % 7 == 3 else ("ordinary" if k % 7 == 5 else "cwy")
+        mk = (k + k // 7) % 7   # every kind of problem meets every mode
+        mode = "mgs" if mk == 3 else ("ordinary" if mk == 5 else "cwy")
         h.set_reorth(mode)
         dev = torch.device("cuda:0")
         dt, et, wt = (torch.tensor(a, dtype=torch.float64, device=dev) for a in (d, e if len(d) > 1 else np.zeros(1), w))
