@@ -907,7 +907,9 @@ static int eigvecs_run(tinv_t h, int64_t n, const double* d, const double* e, co
                 for (int c : rgroups[q].cl) vec += (double)(cs[c + 1] - cs[c] - 1) + (handover ? h->leader_w : 0.0);
                 // measured: a unit spends about the same time per vector whatever its CTA
                 // count (fewer rows per CTA but more exchange), so SM-time ~ vectors x CTAs
-                // a group's share scale (measured on cfg2: the 2-CTA units are the critical ones);
+                // a group's share scale: the 2-CTA units are the critical ones on cfg2 (cWY 1.041 ms at
+                // 1.15, 1.067 at 1.0) and on Type 1 n = 2100 (2.454 at 1.15, 2.507 at 1.0, 2.415 at 1.3);
+                // cfg1, Type 3 and the wide-cluster configs do not react (sched_consts_r02be.txt);
                 // TINV_SPLIT="cs:f,..." overrides
                 double sf = (rgroups[q].cs == 2) ? 1.15 : 1.0;
                 if (const char* v = getenv("TINV_SPLIT")) {
@@ -934,7 +936,11 @@ static int eigvecs_run(tinv_t h, int64_t n, const double* d, const double* e, co
         // group's) and whose Y row fits its columns, so the larger-CS units that finish their
         // long chains early absorb smaller clusters.  Load = weight x per-vector cost of the
         // unit's CS (relative; TINV_CS_COST="cs:f,..." overrides).
-        double csf[9] = {1.0, 1.5, 1.25, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0};   // tuned on cfg2
+        // per-vector cost of 1- and 2-CTA units relative to 4/8-CTA ones: swept on cfg1, cfg2, Type 1
+        // and Type 3 (profiles/r02/sched_consts_r02be.txt).  Only cfg2 and Type 1 at n = 2100 react:
+        // cfg2 prefers 1.5 / 1.25 (cWY 1.041 ms; 1.073 with all 1), Type 1 prefers all 1 (2.356 ms;
+        // 2.454 with 1.5 / 1.25); 1.25 / 1.1 is within 1.3% of the best on both.
+        double csf[9] = {1.0, 1.25, 1.1, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0};
         if (const char* v = getenv("TINV_CS_COST")) {
             int k; double f; const char* q = v;
             while (sscanf(q, "%d:%lf", &k, &f) == 2) {

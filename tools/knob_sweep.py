@@ -15,6 +15,7 @@ ap.add_argument("--config", default="cfg4")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--knob", required=True)
 ap.add_argument("--values", required=True)
+ap.add_argument("--sep", default=",", help="separator of --values (for values that contain commas)")
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--rounds", type=int, default=1, help="repeat the whole value list (drift check)")
 args = ap.parse_args()
@@ -25,8 +26,9 @@ h = Tinv(0)
 h.set_profiling(True)
 Z, rc = h.eigvecs(dd, de, dw, seed=1)   # allocation + warm-up
 keys = ("first", "TT", "BC", "TN", "D", "solve_back", "solve_wait")
+kms = ("batched_lu", "cwy")
 for rnd in range(args.rounds):
-    for v in args.values.split(","):
+    for v in args.values.split(args.sep):
         os.environ[args.knob] = v
         ts = []
         for _ in range(args.reps):
@@ -38,5 +40,6 @@ for rnd in range(args.rounds):
             ts.append(t0.elapsed_time(t1))
         st = h.stats()
         ph = st["cwy_phase_ms"]
-        print(f"{args.config} {args.knob}={v} rc={rc} ms={min(ts):.2f} " +
+        print(f"{args.config} n={len(d)} {args.knob}={v} rc={rc} ms={min(ts):.3f} " +
+              " ".join(f"{k}_ms={st['kernel_ms'][k]:.3f}" for k in kms) + " " +
               " ".join(f"{k}={ph[k]:.1f}" for k in keys if k in ph), flush=True)
