@@ -1213,7 +1213,7 @@ static int eigvecs_run(tinv_t h, int64_t n, const double* d, const double* e, co
         ca.prof_p1 = getenv("TINV_PROF_P1") ? atoi(getenv("TINV_PROF_P1")) : (1 << 30);
         ca.vcap = vcap;
         ca.nstg = nstg;
-        ca.piece_cost = getenv("TINV_PIECE_COST") ? atoi(getenv("TINV_PIECE_COST")) : 4000;
+        ca.piece_cost = getenv("TINV_PIECE_COST") ? atoi(getenv("TINV_PIECE_COST")) : 10000;
         ca.cta0_pm = getenv("TINV_CTA0") ? std::max(0, std::min(900, atoi(getenv("TINV_CTA0")))) : 120;
         ca.prof_sel = getenv("TINV_PROF_SEL") ? atoi(getenv("TINV_PROF_SEL")) : 0;
         ca.a2 = getenv("TINV_A2") ? atoi(getenv("TINV_A2")) : 1;
